@@ -1,0 +1,89 @@
+/* lbk.h — C ABI of the B200 block-LU engine (paper_2512_04389_b200).
+ *
+ * The reference (lublock 0.1.0, pure Python) has no FFI: its boundary is the
+ * Python API of module lublock.factorize (pkg/src/lublock/__init__.py:33-42).
+ * Every entry point below replaces one reference function; the mapping is
+ * given next to each declaration.  Plain pointers and sizes only: no C++ or
+ * torch types cross this boundary, no exceptions, no exit().  Every function
+ * returns an lbk status code (0 = OK); device functions additionally fill an
+ * lbk_status record with the failing block/column.
+ *
+ * Two shared objects implement it:
+ *   liblbk_host.so  — structure path (symbolic, partition, levels), CPU
+ *   liblbk.so       — device engine (sm_100a CUDA kernels + scheduler)
+ */
+#ifndef LBK_H_
+#define LBK_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (map onto pkg/src/lublock/errors.py) ------------------ */
+#define LBK_OK 0
+#define LBK_ERR_ZERO_PIVOT 1        /* errors.ZeroPivot(block, col)        errors.py:66-75 */
+#define LBK_ERR_SUPPORT 2           /* errors.SupportViolation             errors.py:78-82 */
+#define LBK_ERR_DIM_MISMATCH 3      /* errors.DimensionMismatch            errors.py:43-44 */
+#define LBK_ERR_CUDA 4              /* CUDA runtime failure (msg holds cudaGetErrorString) */
+#define LBK_ERR_NCCL 5              /* NCCL failure */
+#define LBK_ERR_OOM 6               /* host or device allocation failure */
+#define LBK_ERR_PIVOT_SWAP 7        /* a diagonal block needs a row swap while its block row
+                                       is stored sparse: the wrapper re-runs in dense mode */
+#define LBK_ERR_BAD_ARG 8           /* errors.BadParams */
+
+typedef struct lbk_status {
+  int32_t code;
+  int32_t block; /* ZeroPivot: diagonal block index (lowest failing one) */
+  int32_t col;   /* ZeroPivot: local column inside that block          */
+  int32_t pad;
+  char msg[256];
+} lbk_status;
+
+/* ======================================================================== *
+ * Host structure path (liblbk_host.so).  run -> fetch -> free protocol: run
+ * computes and reports the output sizes, the caller allocates, fetch copies.
+ * ======================================================================== */
+
+/* symbolic_factorize(a_sym) -> FilledPattern        symbolic.py:57-108
+ * Input: symmetrized CSC (col_ptr[n+1], row_idx[nnz], sorted rows).
+ * Output: col_ptr[n+1], row_idx[nnz_filled] of L+L^T+I, (col,row)-sorted;
+ * parent[n] = elimination tree. */
+int lbk_symbolic_run(int64_t n, const int64_t* col_ptr, const int64_t* row_idx,
+                     void** handle, int64_t* nnz_filled);
+int lbk_symbolic_fetch(void* handle, int64_t* col_ptr, int64_t* row_idx, int64_t* parent);
+void lbk_symbolic_free(void* handle);
+
+/* _require_symmetric_full_diag(col_ptr, row_idx, n)     symbolic.py:46-54
+ * 0 = ok, 1 = missing diagonal (*ndiag = count), 2 = not symmetric,
+ * 3 = rows not strictly increasing within a column. */
+int lbk_check_symmetric(int64_t n, const int64_t* col_ptr, const int64_t* row_idx, int64_t* ndiag);
+
+/* partition(f, a, plan) -> BlockGrid                 grid.py:85-148
+ * Output block table (7 x nblocks, row-major by field):
+ *   bi, bj, nrows, ncols, nnz, colptr_offset, entry_offset
+ * in column-major block order (the reference dict order), pooled local
+ * col_ptr (sum of ncols+1), local row_idx and values (nnz_filled each),
+ * block_nnz[p*p] row-major. */
+int lbk_partition_run(int64_t n, const int64_t* f_col_ptr, const int64_t* f_row_idx,
+                      const int64_t* a_col_ptr, const int64_t* a_row_idx,
+                      const double* a_values, int64_t p, const int64_t* positions,
+                      void** handle, int64_t* nblocks, int64_t* colptr_len);
+int lbk_partition_fetch(void* handle, int64_t* table, int64_t* col_ptr, int64_t* row_idx,
+                        double* values, int64_t* block_nnz);
+void lbk_partition_free(void* handle);
+
+/* dependency_levels(grid) -> DependencyTree            grid.py:223-378 */
+int lbk_levels_run(int64_t p, int64_t nblocks, const int64_t* table, const int64_t* col_ptr,
+                   const int64_t* row_idx, void** handle, int64_t* ntasks, int64_t* npreds);
+int lbk_levels_fetch(void* handle, int8_t* kinds, int32_t* steps, int32_t* rows, int32_t* cols,
+                     int64_t* weights, int64_t* costs, int32_t* levels, int64_t* pred_ptr,
+                     int32_t* pred_idx);
+void lbk_levels_free(void* handle);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LBK_H_ */
