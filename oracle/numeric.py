@@ -1,0 +1,178 @@
+"""Oracle restatement of the reference numerical factorization (TEST INFRASTRUCTURE ONLY).
+
+Serial topological execution of the task DAG over a dense scratch copy of
+every stored block, like pkg/src/lublock/factorize.py:245-384 with
+workers=1.  Kernels (dense loops, rank-1 updates over the full trailing
+block — the reference restricts to structural nonzeros, which only skips
+exact-zero products, factorize.py:72-73):
+
+* GETRF  factorize.py:38-78   block-local partial pivoting, first argmax,
+  ZeroPivot test ``piv == 0 or piv < tol * colmax_at_entry``, static pivot
+  replacement keeps the sign;
+* GESSM  factorize.py:326-337 + 98-109  perm applied to the U panel, unit
+  lower forward substitution;
+* TSTRF  factorize.py:338-345 + 112-130 right upper solve;
+* SSSSM  factorize.py:307-325  tgt -= L @ U with the support checks.
+
+Returns dense blocks + perms, and ``export`` turns them into per-block CSC
+with exact zeros dropped (factorize.py:179-192, 370-381).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import scipy.sparse as sp
+from scipy.sparse.linalg import spsolve_triangular
+
+from .structure import GESSM, GETRF, SSSSM, TSTRF, Block
+
+
+class OracleZeroPivot(Exception):
+    def __init__(self, block, col):
+        self.block, self.col = block, col
+        super().__init__(f"zero pivot in block {block} col {col}")
+
+
+class OracleSupportViolation(Exception):
+    pass
+
+
+def dense(b: Block) -> np.ndarray:
+    d = np.zeros((b.nrows, b.ncols))
+    d[b.row_idx, np.repeat(np.arange(b.ncols), np.diff(b.col_ptr))] = b.values
+    return d
+
+
+def getrf(d, pivot_tol=1e-12, static_eps=None, block=0):
+    """In-place LU with pivoting confined to the block; returns (perm, swapped)."""
+    m = d.shape[0]
+    perm = np.arange(m)
+    swapped = False
+    colmax = np.abs(d).max(axis=0) if m else np.zeros(0)
+    for k in range(m):
+        mags = np.abs(d[k:, k])
+        off = int(np.argmax(mags))
+        piv = mags[off]
+        if piv == 0.0 or piv < pivot_tol * colmax[k]:
+            if static_eps is None:
+                raise OracleZeroPivot(block, k)
+            d[k, k] = static_eps if d[k, k] == 0.0 else math.copysign(static_eps, d[k, k])
+        elif off:
+            d[[k, k + off]] = d[[k + off, k]]
+            perm[[k, k + off]] = perm[[k + off, k]]
+            swapped = True
+        if k + 1 < m:
+            d[k + 1:, k] /= d[k, k]
+            d[k + 1:, k + 1:] -= np.outer(d[k + 1:, k], d[k, k + 1:])
+    return perm, swapped
+
+
+def gessm(lsrc, x):
+    """x <- L^-1 x, L = unit lower part of lsrc."""
+    for k in range(lsrc.shape[0] - 1):
+        x[k + 1:] -= np.outer(lsrc[k + 1:, k], x[k])
+
+
+def tstrf(x, usrc):
+    """x <- x U^-1, U = upper part (with diagonal) of usrc."""
+    m = usrc.shape[1]
+    for k in range(m):
+        x[:, k] /= usrc[k, k]
+        if k + 1 < m:
+            x[:, k + 1:] -= np.outer(x[:, k], usrc[k, k + 1:])
+
+
+def factorize(grid, tree, pivot_tol=1e-12, static_pivot=None):
+    """Serial DAG execution; returns (state: {(bi,bj): dense}, perms: list)."""
+    state = {k: dense(b) for k, b in grid.blocks.items()}
+    perms = [None] * grid.p
+    static_eps = None if static_pivot is None else float(static_pivot) * (grid.value_max or 1.0)
+    checking = True
+    outside = {}
+    for t in range(len(tree.kinds)):
+        kind, i, r, c = int(tree.kinds[t]), int(tree.steps[t]), int(tree.rows[t]), int(tree.cols[t])
+        if kind == SSSSM:
+            prod = state[(r, i)] @ state[(i, c)]
+            tgt = state.get((r, c))
+            if tgt is None:
+                if prod.any():
+                    raise OracleSupportViolation(f"step {i} hits empty block ({r},{c})")
+                continue
+            if checking:
+                if (r, c) not in outside:
+                    b = grid.blocks[(r, c)]
+                    mask = np.ones((b.nrows, b.ncols), bool)
+                    mask[b.row_idx, np.repeat(np.arange(b.ncols), np.diff(b.col_ptr))] = False
+                    outside[(r, c)] = mask
+                if prod[outside[(r, c)]].any():
+                    raise OracleSupportViolation(f"step {i} writes outside support of ({r},{c})")
+            tgt -= prod
+        elif kind == GESSM:
+            x = state[(i, c)]
+            if perms[i] is not None:
+                x[:] = x[perms[i]]
+            gessm(state[(i, i)], x)
+        elif kind == TSTRF:
+            tstrf(state[(r, i)], state[(i, i)])
+        else:
+            perm, swapped = getrf(state[(i, i)], pivot_tol, static_eps, i)
+            perms[i] = perm if swapped else None
+            if swapped:
+                checking = False
+    for i in range(grid.p):
+        if perms[i] is None:
+            perms[i] = np.arange(int(grid.positions[i + 1] - grid.positions[i]))
+    return state, perms
+
+
+def to_block(d) -> Block:
+    """Dense -> CSC dropping exact zeros (factorize.py:179-192)."""
+    cols, rows = np.nonzero(d.T)
+    cp = np.concatenate([[0], np.cumsum(np.bincount(cols, minlength=d.shape[1]))]).astype(np.int64)
+    return Block(d.shape[0], d.shape[1], cp, rows.astype(np.int64), d.T[cols, rows])
+
+
+def export(state):
+    """(l_blocks, u_blocks): strictly lower -> L, strictly upper -> U, diagonal split."""
+    lb, ub = {}, {}
+    for (bi, bj), d in state.items():
+        if bi > bj:
+            lb[(bi, bj)] = to_block(d)
+        elif bi < bj:
+            ub[(bi, bj)] = to_block(d)
+        else:
+            lb[(bi, bj)] = to_block(np.tril(d, -1) + np.eye(d.shape[0]))
+            ub[(bi, bj)] = to_block(np.triu(d))
+    return lb, ub
+
+
+def assemble(n, positions, blocks):
+    rows, cols, vals = [], [], []
+    for (bi, bj), b in blocks.items():
+        rows.append(b.row_idx + positions[bi])
+        cols.append(np.repeat(np.arange(b.ncols), np.diff(b.col_ptr)) + positions[bj])
+        vals.append(b.values)
+    return sp.coo_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                         shape=(n, n)).tocsr()
+
+
+def perm_global(positions, perms):
+    return np.concatenate([positions[i] + perms[i] for i in range(len(perms))])
+
+
+def residual(a, n, positions, lb, ub, perms):
+    """||P A - L U||_F / ||A||_F (factorize.py:438-448)."""
+    A = sp.csc_matrix((a.values, a.row_idx, a.col_ptr), shape=(n, n)).tocsr()
+    diff = (A[perm_global(positions, perms), :] - assemble(n, positions, lb) @ assemble(n, positions, ub)).tocoo()
+    num = math.sqrt(float(np.sum(diff.data ** 2)))
+    den = math.sqrt(float(np.sum(a.values ** 2)))
+    return 0.0 if den == 0 and num == 0 else (math.inf if den == 0 else num / den)
+
+
+def solve(n, positions, lb, ub, perms, b):
+    """x = U^-1 L^-1 b[perm] (factorize.py:451-457)."""
+    y = spsolve_triangular(assemble(n, positions, lb), np.asarray(b, float)[perm_global(positions, perms)],
+                           lower=True)
+    return spsolve_triangular(assemble(n, positions, ub), y, lower=False)
