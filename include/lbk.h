@@ -82,6 +82,66 @@ int lbk_levels_fetch(void* handle, int8_t* kinds, int32_t* steps, int32_t* rows,
                      int32_t* pred_idx);
 void lbk_levels_free(void* handle);
 
+/* ======================================================================== *
+ * Device engine (liblbk.so).  One lbk_ctx per GPU.  Replaces
+ *   lublock.factorize.factorize(grid, tree, workers, pivot_tol,
+ *                               static_pivot, dense_blas)   factorize.py:245-384
+ * split into plan (structure, once) + numeric (values, every call), the way
+ * a refactorization with a fixed pattern is driven.
+ * ======================================================================== */
+typedef struct lbk_ctx lbk_ctx;
+
+int lbk_create(lbk_ctx** ctx, int device, lbk_status* st);
+void lbk_destroy(lbk_ctx* ctx);
+
+/* Upload the block structure (the pooled BlockGrid of lbk_partition_fetch:
+ * table[7 x nblocks], local col_ptr pool, local row_idx pool) and the
+ * DependencyTree arrays (grid.py:172-181); builds the per-level work lists
+ * (items of `chunk` columns/rows) and the CUDA graph lazily. */
+int lbk_plan(lbk_ctx* ctx, int64_t n, int64_t p, const int64_t* positions, int64_t nblocks,
+             const int64_t* table, const int64_t* col_ptr, const int64_t* row_idx, int64_t ntasks,
+             const int8_t* kinds, const int32_t* steps, const int32_t* rows, const int32_t* cols,
+             const int32_t* levels, const int64_t* costs, int32_t chunk, lbk_status* st);
+
+/* Pristine A values in pool order, kept resident on the device. */
+int lbk_upload_values(lbk_ctx* ctx, const double* values, lbk_status* st);
+
+/* Device-resident factorization of the resident A values (reset + level
+ * graph).  static_eps = NaN disables static pivoting (factorize.py:267-269).
+ * *ms = device time of the level graph.  ZeroPivot -> LBK_ERR_ZERO_PIVOT
+ * with st->block/col = the lowest failing (block, local column). */
+int lbk_factorize(lbk_ctx* ctx, double pivot_tol, double static_eps, float* ms, lbk_status* st);
+
+/* End-to-end: host A values in, host factor values (pool order, in place of
+ * A's pattern) and per-diagonal-row local permutations out. */
+int lbk_factorize_host(lbk_ctx* ctx, const double* a_values, double* lu_values, int32_t* perms,
+                       double pivot_tol, double static_eps, lbk_status* st);
+
+/* Copy the last factorization's values / perms to the host. */
+int lbk_download(lbk_ctx* ctx, double* lu_values, int32_t* perms, lbk_status* st);
+
+/* Overwrite the per-diagonal-row permutations (pool order of the diagonal
+ * blocks).  Used by the kernel-level entry points factor_u_panel
+ * (factorize.py:150-156), which take an explicit perm_i, when the plan
+ * holds no GETRF task to produce it. */
+int lbk_set_perms(lbk_ctx* ctx, const int32_t* perms, lbk_status* st);
+
+/* Page-locked host memory for the end-to-end path. */
+int lbk_host_alloc(void** ptr, int64_t bytes);
+void lbk_host_free(void* ptr);
+
+/* info[0] = launched levels, info[1] = work items, info[2] = diagonal rows,
+ * info[3] = stored entries. */
+int lbk_plan_info(lbk_ctx* ctx, int64_t* info);
+
+/* One instrumented replay: device ms of every launched level (load-balance
+ * evidence next to metrics.level_work_stats, pkg/src/lublock/metrics.py:63-90). */
+int lbk_level_times(lbk_ctx* ctx, double pivot_tol, double static_eps, float* out_ms, lbk_status* st);
+
+/* Launched-level table (4 x nlevels: item offset, items, warps, acc length)
+ * and, if items != NULL, the work items (6 x total: kind, a, b, c, begin, end). */
+int lbk_plan_levels(lbk_ctx* ctx, int64_t* levels, int32_t* items);
+
 #ifdef __cplusplus
 }
 #endif

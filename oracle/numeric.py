@@ -65,14 +65,22 @@ def getrf(d, pivot_tol=1e-12, static_eps=None, block=0):
             swapped = True
         if k + 1 < m:
             d[k + 1:, k] /= d[k, k]
-            d[k + 1:, k + 1:] -= np.outer(d[k + 1:, k], d[k, k + 1:])
+            # rank-1 update on the nonzero rows x nonzero columns only: the
+            # skipped terms are exact-zero products (same bits, far less work
+            # on sparse blocks — this is also what the reference does)
+            rows = k + 1 + np.flatnonzero(d[k + 1:, k])
+            cols = k + 1 + np.flatnonzero(d[k, k + 1:])
+            if len(rows) and len(cols):
+                d[np.ix_(rows, cols)] -= np.outer(d[rows, k], d[k, cols])
     return perm, swapped
 
 
 def gessm(lsrc, x):
     """x <- L^-1 x, L = unit lower part of lsrc."""
     for k in range(lsrc.shape[0] - 1):
-        x[k + 1:] -= np.outer(lsrc[k + 1:, k], x[k])
+        rows = k + 1 + np.flatnonzero(lsrc[k + 1:, k])
+        if len(rows):
+            x[rows] -= np.outer(lsrc[rows, k], x[k])
 
 
 def tstrf(x, usrc):
@@ -81,7 +89,10 @@ def tstrf(x, usrc):
     for k in range(m):
         x[:, k] /= usrc[k, k]
         if k + 1 < m:
-            x[:, k + 1:] -= np.outer(x[:, k], usrc[k, k + 1:])
+            rows = np.flatnonzero(x[:, k])
+            cols = k + 1 + np.flatnonzero(usrc[k, k + 1:])
+            if len(rows) and len(cols):
+                x[np.ix_(rows, cols)] -= np.outer(x[rows, k], usrc[k, cols])
 
 
 def factorize(grid, tree, pivot_tol=1e-12, static_pivot=None):
