@@ -197,6 +197,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--levels-out", default=None, help="write per-level device times + work to this .npz")
+    ap.add_argument("--dense-threshold", type=float, default=0.5,
+                    help="density tag for the FP64 DMMA kernels (reference: 0.5); <0 disables")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -210,9 +212,11 @@ def main():
     flops_t, bytes_t = task_work(g, t)
     total_flops = float(flops_t.sum())
     t0 = time.perf_counter()
-    eng = Engine(g, t, device=local)
+    dt = None if args.dense_threshold < 0 else args.dense_threshold
+    eng = Engine(g, t, device=local, dense_threshold=dt, dense_kernels=dt is not None)
     eng.upload()
-    log(f"[bench] plan: {eng.n_launch_levels} launched levels, {eng.n_items} items, {time.perf_counter() - t0:.1f}s")
+    log(f"[bench] plan: {eng.n_launch_levels} levels, {eng.n_launches} launches, {eng.n_items} sparse items, "
+        f"{eng.n_gemm_tiles} DMMA tiles, {eng.n_dense_items} dense items, {time.perf_counter() - t0:.1f}s")
 
     for _ in range(max(args.warmup, 0)):
         eng.run_device()
@@ -249,7 +253,7 @@ def main():
     if len(kept) != len(lvl_ms):  # levels with only skipped tasks are not launched
         lvl_bytes = lvl_bytes[: len(lvl_ms)]
         lvl_flops = lvl_flops[: len(lvl_ms)]
-    kern_s = float(lvl_ms.sum()) / 1e3
+    kern_s = max(float(lvl_ms.sum()) / 1e3, 1e-12)
     peak, peak_src = peaks()
     achieved = float(bytes_t.sum()) / kern_s / 1e9
     traffic = None
@@ -284,13 +288,13 @@ def main():
                     "path": "Engine.run_host -> lbk_factorize_host (C-ABI), pinned host buffers"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "kernel": "level_kernel",
-                         "launches_per_step": int(eng.n_launch_levels),
+                         "launches_per_step": int(eng.n_launches), "dense_threshold": dt,
                          "algorithmic_bytes_per_step": float(bytes_t.sum()),
                          "mean_launch_ms": float(lvl_ms.mean()), "peak_source": peak_src,
                          "fp64_gflops_in_kernel": total_flops / kern_s / 1e9},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
-            "gpu_launches": int(args.steps * eng.n_launch_levels),
+            "gpu_launches": int(args.steps * eng.n_launches),
         }
         print(json.dumps(line), flush=True)
     eng.close()

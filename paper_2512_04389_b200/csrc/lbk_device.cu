@@ -315,6 +315,12 @@ __global__ void __launch_bounds__(256) level_kernel(const Item* __restrict__ ite
   }
 }
 
+}  // namespace
+
+#include "lbk_dense.cuh"
+
+namespace {
+
 // ------------------------------------------------------------------ host ----
 
 template <class T>
@@ -335,10 +341,16 @@ struct DevBuf {
 };
 
 struct Level {
-  int64_t item_off;
+  int64_t item_off;   // generic (sparse) items
   int32_t nitems;
   int32_t warps;
   int32_t acc_len;
+  int64_t gemm_off;   // dense SSSSM tiles
+  int32_t ngemm;
+  int64_t dense_off;  // dense GETRF / GESSM / TSTRF items
+  int32_t ndense;
+  int32_t dense_smem; // bytes
+  int32_t dense_threads;
 };
 
 }  // namespace
@@ -362,8 +374,13 @@ struct lbk_ctx {
   DevBuf<int32_t> colptr, rows, csr_ptr, csr_col, csr_pos, diag_csc, diag_csr, lv_cols, lv_ptr, perm;
   DevBuf<double> vals, vals0;
   DevBuf<Item> items;
+  DevBuf<lbk_dense::GemmItem> gitems;
+  DevBuf<lbk_dense::DenseItem> ditems;
   DevBuf<unsigned long long> err;
   int64_t ndiag_rows = 0;
+  int64_t total_gemm = 0, total_dense = 0;
+  cudaStream_t aux[2] = {nullptr, nullptr};
+  cudaEvent_t fork = nullptr, join[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -436,6 +453,16 @@ int lbk_create(lbk_ctx** out, int device, lbk_status* st) {
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(lbk_dense::dgemm_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             lbk_dense::GEMM_SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(lbk_dense::dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_SMEM);
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+    e = cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->join[k], cudaEventDisableTiming);
+  }
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     delete c;
     return cuda_fail(st, e, "lbk_create");
@@ -452,6 +479,11 @@ void lbk_destroy(lbk_ctx* c) {
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   if (c->stream) cudaStreamDestroy(c->stream);
+  for (int k = 0; k < 2; ++k) {
+    if (c->aux[k]) cudaStreamDestroy(c->aux[k]);
+    if (c->join[k]) cudaEventDestroy(c->join[k]);
+  }
+  if (c->fork) cudaEventDestroy(c->fork);
   delete c;
 }
 
@@ -460,7 +492,8 @@ void lbk_destroy(lbk_ctx* c) {
 int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t nblocks,
              const int64_t* table, const int64_t* colptr, const int64_t* rowidx, int64_t ntasks,
              const int8_t* kinds, const int32_t* steps, const int32_t* trows, const int32_t* tcols,
-             const int32_t* tlevels, const int64_t* costs, int32_t chunk, lbk_status* st) {
+             const int32_t* tlevels, const int64_t* costs, int32_t chunk, int32_t flags,
+             lbk_status* st) {
   if (!c) return fail(st, LBK_ERR_BAD_ARG, "null ctx");
   LBK_CUDA(cudaSetDevice(c->device), st);
   const int64_t nb = nblocks;
@@ -582,6 +615,12 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         per[lv].push_back(it);
       }
     };
+    using lbk_dense::DenseItem;
+    using lbk_dense::GemmItem;
+    const bool dense_on = (flags & 1) != 0;
+    std::vector<std::vector<GemmItem>> gper(nlevels);
+    std::vector<std::vector<DenseItem>> dper(nlevels);
+    std::vector<int32_t> dsmem(nlevels, 0);
     for (int64_t t = 0; t < ntasks; ++t) {
       const int kind = kinds[t];
       const int64_t i = steps[t], r = trows[t], cc = tcols[t];
@@ -591,24 +630,45 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       if (kind == KIND_GETRF) {
         it.a = static_cast<int32_t>(bid[i * p + i]);
         it.b = static_cast<int32_t>(i);
-        // row swaps are representable only if the diagonal block and every U
-        // panel of block row i store their full rectangle (dense mode)
-        it.c = hb[it.a].full;
-        for (int64_t j = i + 1; j < p && it.c; ++j)
-          if (bid[i * p + j] >= 0 && !hb[bid[i * p + j]].full) it.c = 0;
+        // row swaps are representable only when every block stores its full
+        // rectangle (flags bit 1, the dense-scratch mode): a swapped U panel
+        // feeds products that may leave any sparse target's pattern
+        it.c = (flags & 2) ? 1 : 0;
         it.begin = 0;
         it.end = 1;
+        if (dense_on && hb[it.a].full) {
+          DenseItem d{0, it.a, it.b, it.c, 0, static_cast<int32_t>(i)};
+          dper[lv].push_back(d);
+          dsmem[lv] = std::max(dsmem[lv], (hb[it.a].nrows + 64) * 8);
+          continue;
+        }
         per[lv].push_back(it);
         lvl_acc[lv] = std::max(lvl_acc[lv], hb[it.a].nrows);
       } else if (kind == KIND_GESSM) {
         it.a = static_cast<int32_t>(bid[i * p + i]);
         it.b = static_cast<int32_t>(bid[i * p + cc]);
         it.c = hb[it.b].full;  // permute on the fly only for full panels
+        if (dense_on && hb[it.a].full && hb[it.b].full) {
+          for (int32_t s = 0; s < hb[it.b].ncols; s += lbk_dense::STRIP) {
+            DenseItem d{1, it.a, it.b, 1, s, static_cast<int32_t>(i)};
+            dper[lv].push_back(d);
+          }
+          dsmem[lv] = std::max(dsmem[lv], (hb[it.a].nrows + 64) * 8);
+          continue;
+        }
         lvl_acc[lv] = std::max(lvl_acc[lv], hb[it.b].nrows);
         add_range(lv, it, hb[it.b].ncols);
       } else if (kind == KIND_TSTRF) {
         it.a = static_cast<int32_t>(bid[i * p + i]);
         it.b = static_cast<int32_t>(bid[r * p + i]);
+        if (dense_on && hb[it.a].full && hb[it.b].full) {
+          for (int32_t s = 0; s < hb[it.b].nrows; s += lbk_dense::STRIP) {
+            DenseItem d{2, it.a, it.b, 0, s, static_cast<int32_t>(i)};
+            dper[lv].push_back(d);
+          }
+          dsmem[lv] = std::max(dsmem[lv], 64 * 8);
+          continue;
+        }
         lvl_acc[lv] = std::max(lvl_acc[lv], hb[it.b].ncols);
         add_range(lv, it, hb[it.b].nrows);
       } else {
@@ -621,25 +681,45 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         it.a = static_cast<int32_t>(bid[r * p + i]);
         it.b = static_cast<int32_t>(bid[i * p + cc]);
         it.c = static_cast<int32_t>(tgt);
+        if (dense_on && hb[it.a].full && hb[it.b].full && hb[tgt].full) {
+          for (int32_t n0 = 0; n0 < hb[tgt].ncols; n0 += lbk_dense::GBN)
+            for (int32_t m0 = 0; m0 < hb[tgt].nrows; m0 += lbk_dense::GBM)
+              gper[lv].push_back(GemmItem{it.a, it.b, it.c, m0, n0, 0});
+          continue;
+        }
         lvl_acc[lv] = std::max(lvl_acc[lv], hb[tgt].nrows);
         add_range(lv, it, hb[tgt].ncols);
       }
     }
     std::vector<Item> all;
+    std::vector<GemmItem> gall;
+    std::vector<DenseItem> dall;
     c->levels.clear();
     for (int32_t lv = 0; lv < nlevels; ++lv) {
-      if (per[lv].empty()) continue;
-      if (static_cast<int64_t>(lvl_acc[lv]) * 8 > MAX_SMEM)
+      if (per[lv].empty() && gper[lv].empty() && dper[lv].empty()) continue;
+      if (static_cast<int64_t>(lvl_acc[lv]) * 8 > MAX_SMEM || dsmem[lv] > MAX_SMEM)
         return fail(st, LBK_ERR_BAD_ARG, "block span too large for the shared-memory accumulator");
-      Level L;
+      Level L{};
       L.item_off = static_cast<int64_t>(all.size());
       L.nitems = static_cast<int32_t>(per[lv].size());
       L.acc_len = lvl_acc[lv];
       L.warps = choose_warps(L.acc_len);
       all.insert(all.end(), per[lv].begin(), per[lv].end());
+      L.gemm_off = static_cast<int64_t>(gall.size());
+      L.ngemm = static_cast<int32_t>(gper[lv].size());
+      gall.insert(gall.end(), gper[lv].begin(), gper[lv].end());
+      L.dense_off = static_cast<int64_t>(dall.size());
+      L.ndense = static_cast<int32_t>(dper[lv].size());
+      L.dense_smem = dsmem[lv];
+      L.dense_threads = 256;
+      for (const DenseItem& d : dper[lv])
+        if (d.kind == 0) L.dense_threads = 512;
+      dall.insert(dall.end(), dper[lv].begin(), dper[lv].end());
       c->levels.push_back(L);
     }
     c->total_items = static_cast<int64_t>(all.size());
+    c->total_gemm = static_cast<int64_t>(gall.size());
+    c->total_dense = static_cast<int64_t>(dall.size());
     c->hblk = hb;
     LBK_CUDA(c->blk.upload(hb), st);
     LBK_CUDA(c->colptr.upload(hcp), st);
@@ -652,6 +732,8 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     LBK_CUDA(c->lv_cols.upload(hlvc), st);
     LBK_CUDA(c->lv_ptr.upload(hlvp), st);
     LBK_CUDA(c->items.upload(all), st);
+    LBK_CUDA(c->gitems.upload(gall), st);
+    LBK_CUDA(c->ditems.upload(dall), st);
     LBK_CUDA(c->perm.alloc(hdcsc.size()), st);
     LBK_CUDA(c->vals.alloc(nnz), st);
     LBK_CUDA(c->vals0.alloc(nnz), st);
@@ -679,6 +761,42 @@ int lbk_upload_values(lbk_ctx* c, const double* values, lbk_status* st) {
 
 namespace {
 
+// Capture every level into the current capture of c->stream: the generic
+// (sparse) items on the main stream, dense GEMM tiles and dense
+// GETRF/GESSM/TSTRF items on two forked branches, joined before the next
+// level.  With `evs`, an external (timing-capable) event record node closes
+// each level.
+void capture_levels(lbk_ctx* c, double pivot_tol, double static_eps, std::vector<cudaEvent_t>* evs) {
+  DevPools P = pools(c);
+  cudaMemsetAsync(c->err.p, 0xff, 2 * sizeof(unsigned long long), c->stream);
+  if (evs) cudaEventRecordWithFlags((*evs)[0], c->stream, cudaEventRecordExternal);
+  for (size_t l = 0; l < c->levels.size(); ++l) {
+    const Level& L = c->levels[l];
+    const bool g = L.ngemm > 0, d = L.ndense > 0;
+    if (g || d) cudaEventRecord(c->fork, c->stream);
+    if (g) {
+      cudaStreamWaitEvent(c->aux[0], c->fork, 0);
+      lbk_dense::dgemm_tile_kernel<<<L.ngemm, 256, lbk_dense::GEMM_SMEM, c->aux[0]>>>(
+          c->gitems.p + L.gemm_off, P);
+      cudaEventRecord(c->join[0], c->aux[0]);
+    }
+    if (d) {
+      cudaStreamWaitEvent(c->aux[1], c->fork, 0);
+      lbk_dense::dense_kernel<<<L.ndense, L.dense_threads, L.dense_smem, c->aux[1]>>>(
+          c->ditems.p + L.dense_off, P, pivot_tol, static_eps);
+      cudaEventRecord(c->join[1], c->aux[1]);
+    }
+    if (L.nitems) {
+      const size_t smem = static_cast<size_t>(L.warps) * L.acc_len * sizeof(double);
+      level_kernel<<<L.nitems, L.warps * 32, smem, c->stream>>>(c->items.p + L.item_off, P, L.acc_len,
+                                                                pivot_tol, static_eps);
+    }
+    if (g) cudaStreamWaitEvent(c->stream, c->join[0], 0);
+    if (d) cudaStreamWaitEvent(c->stream, c->join[1], 0);
+    if (evs) cudaEventRecordWithFlags((*evs)[l + 1], c->stream, cudaEventRecordExternal);
+  }
+}
+
 int build_graph(lbk_ctx* c, double pivot_tol, double static_eps, lbk_status* st) {
   if (c->graph && ((c->plan_pivot_tol == pivot_tol) ||
                    (std::isnan(c->plan_pivot_tol) && std::isnan(pivot_tol))) &&
@@ -688,15 +806,9 @@ int build_graph(lbk_ctx* c, double pivot_tol, double static_eps, lbk_status* st)
     cudaGraphExecDestroy(c->graph);
     c->graph = nullptr;
   }
-  DevPools P = pools(c);
   cudaGraph_t g;
   LBK_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), st);
-  cudaMemsetAsync(c->err.p, 0xff, 2 * sizeof(unsigned long long), c->stream);
-  for (const Level& L : c->levels) {
-    const size_t smem = static_cast<size_t>(L.warps) * L.acc_len * sizeof(double);
-    level_kernel<<<L.nitems, L.warps * 32, smem, c->stream>>>(c->items.p + L.item_off, P, L.acc_len,
-                                                              pivot_tol, static_eps);
-  }
+  capture_levels(c, pivot_tol, static_eps, nullptr);
   cudaError_t e = cudaStreamEndCapture(c->stream, &g);
   if (e != cudaSuccess) return cuda_fail(st, e, "graph capture");
   e = cudaGraphInstantiate(&c->graph, g, 0);
@@ -811,21 +923,12 @@ int lbk_level_times(lbk_ctx* c, double pivot_tol, double static_eps, float* out_
   const size_t nl = c->levels.size();
   std::vector<cudaEvent_t> ev(nl + 1);
   for (auto& e : ev) LBK_CUDA(cudaEventCreate(&e), st);
-  DevPools P = pools(c);
   cudaGraph_t g;
   cudaGraphExec_t ge = nullptr;
   LBK_CUDA(cudaMemcpyAsync(c->vals.p, c->vals0.p, c->nnz * sizeof(double), cudaMemcpyDeviceToDevice,
                            c->stream), st);
   LBK_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), st);
-  cudaMemsetAsync(c->err.p, 0xff, 2 * sizeof(unsigned long long), c->stream);
-  cudaEventRecord(ev[0], c->stream);
-  for (size_t l = 0; l < nl; ++l) {
-    const Level& L = c->levels[l];
-    const size_t smem = static_cast<size_t>(L.warps) * L.acc_len * sizeof(double);
-    level_kernel<<<L.nitems, L.warps * 32, smem, c->stream>>>(c->items.p + L.item_off, P, L.acc_len,
-                                                              pivot_tol, static_eps);
-    cudaEventRecord(ev[l + 1], c->stream);
-  }
+  capture_levels(c, pivot_tol, static_eps, &ev);
   LBK_CUDA(cudaStreamEndCapture(c->stream, &g), st);
   cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
   cudaGraphDestroy(g);
@@ -869,11 +972,17 @@ int lbk_plan_levels(lbk_ctx* c, int64_t* levels /* 4 x nlevels */, int32_t* item
 }
 
 // Plan statistics: levels launched, work items, diagonal rows.
-int lbk_plan_info(lbk_ctx* c, int64_t* info /* [4] */) {
+int lbk_plan_info(lbk_ctx* c, int64_t* info /* [8] */) {
   info[0] = static_cast<int64_t>(c->levels.size());
   info[1] = c->total_items;
   info[2] = c->ndiag_rows;
   info[3] = c->nnz;
+  info[4] = c->total_gemm;
+  info[5] = c->total_dense;
+  int64_t launches = 0;
+  for (const Level& L : c->levels) launches += (L.nitems > 0) + (L.ngemm > 0) + (L.ndense > 0);
+  info[6] = launches;
+  info[7] = 0;
   return 0;
 }
 

@@ -32,6 +32,7 @@ from .matrix_io import CscMatrix
 
 DEFAULT_PIVOT_TOL = 1e-12
 DEFAULT_CHUNK = 8
+DEFAULT_DENSE_THRESHOLD = 0.5  # reference density tag (factorize.py:274)
 
 P = _native.ptr
 i64p, i32p, i8p, f64p = _native.c_i64p, _native.c_i32p, _native.c_i8p, _native.c_f64p
@@ -53,7 +54,7 @@ def _dev():
     d(lib, "lbk_create", C.c_int, [C.POINTER(vp), C.c_int, st])
     d(lib, "lbk_destroy", None, [vp])
     d(lib, "lbk_plan", C.c_int, [vp, C.c_int64, C.c_int64, i64p, C.c_int64, i64p, i64p, i64p, C.c_int64,
-                                 i8p, i32p, i32p, i32p, i32p, i64p, C.c_int32, st])
+                                 i8p, i32p, i32p, i32p, i32p, i64p, C.c_int32, C.c_int32, st])
     d(lib, "lbk_upload_values", C.c_int, [vp, f64p, st])
     d(lib, "lbk_factorize", C.c_int, [vp, C.c_double, C.c_double, C.POINTER(C.c_float), st])
     d(lib, "lbk_factorize_host", C.c_int, [vp, f64p, f64p, i32p, C.c_double, C.c_double, st])
@@ -105,11 +106,18 @@ class Engine:
     """
 
     def __init__(self, grid, tree, *, device: int = 0, chunk: int = DEFAULT_CHUNK, pool: GridPool | None = None,
-                 dense: bool = False):
+                 dense: bool = False, dense_threshold: float | None = DEFAULT_DENSE_THRESHOLD,
+                 dense_kernels: bool = True):
         self.lib = _dev()
         self.grid = grid
         self.tree = tree
-        self.pool = pool if pool is not None else pool_grid(grid)
+        base = pool if pool is not None else pool_grid(grid)
+        if dense:
+            base = densify_pool(grid, base, 0.0)
+        elif dense_threshold is not None:
+            base = densify_pool(grid, base, dense_threshold)
+        self.pool = base
+        self.dense_threshold = 0.0 if dense else dense_threshold
         self.device = device
         ctx = C.c_void_p()
         st = _native.LbkStatus()
@@ -142,13 +150,15 @@ class Engine:
         t, cp, ri, k, s, r, c, lv, co = self._keep
         rc = self.lib.lbk_plan(ctx, grid.n, grid.p, P(pos, i64p), pl.nblocks, P(t, i64p), P(cp, i64p),
                                P(ri, i64p), len(k), P(k, i8p), P(s, i32p), P(r, i32p), P(c, i32p),
-                               P(lv, i32p), P(co, i64p), int(chunk), C.byref(st))
+                               P(lv, i32p), P(co, i64p), int(chunk),
+                               (1 if dense_kernels else 0) | (2 if dense else 0), C.byref(st))
         if rc:
             _native.raise_status(st, "lbk_plan")
         self.nnz = int(pl.values.shape[0])
-        info = np.zeros(4, np.int64)
+        info = np.zeros(8, np.int64)
         self.lib.lbk_plan_info(ctx, P(info, i64p))
         self.n_launch_levels, self.n_items, self.n_diag_rows = int(info[0]), int(info[1]), int(info[2])
+        self.n_gemm_tiles, self.n_dense_items, self.n_launches = int(info[4]), int(info[5]), int(info[6])
         self._resident = False
 
     def close(self):
@@ -322,14 +332,39 @@ def build_factors(grid, pool: GridPool, values: np.ndarray, perms_pool: np.ndarr
     return LUFactors(n=grid.n, plan=grid.plan, l_blocks=lb, u_blocks=ub, perms=perms)
 
 
-def densify_pool(grid, pool: GridPool) -> GridPool:
-    """Every stored block widened to its full rectangle (the reference's dense
-    scratch, factorize.py:265): makes block-local row swaps representable."""
-    t = pool.table.copy()
+def densify_pool(grid, pool: GridPool, threshold: float = 0.0) -> GridPool:
+    """Widen every block with nnz >= threshold * nrows * ncols to its full
+    rectangle (column-major dense tile, ld = nrows).
+
+    threshold 0.5 is the reference's density tag (nnz*2 >= nrows*ncols,
+    factorize.py:271-275): those blocks run on the FP64 DMMA kernels.
+    threshold 0 widens every block (the reference's dense scratch,
+    factorize.py:265) and makes block-local row swaps representable.
+    Positions outside the filled pattern stay exactly zero and are dropped
+    again on export (factorize.py:179-192), so the exported structure is
+    unchanged.
+    """
+    tb = pool.table
+    widen = tb[4] * 1.0 >= threshold * tb[2] * tb[3]
+    if threshold == 0.5:
+        widen = tb[4] * 2 >= tb[2] * tb[3]
+    widen &= tb[4] < tb[2] * tb[3]  # already full blocks need no copy
+    if not widen.any():
+        return pool
+    t = tb.copy()
     cps, ris, vals = [], [], []
     cpo = ento = 0
     for b in range(pool.nblocks):
         bi, bj, nr, nc, nz, co, eo = (int(x) for x in pool.table[:, b])
+        if not widen[b]:
+            cps.append(pool.col_ptr[co:co + nc + 1])
+            ris.append(pool.row_idx[eo:eo + nz])
+            vals.append(pool.values[eo:eo + nz])
+            t[5, b] = cpo
+            t[6, b] = ento
+            cpo += nc + 1
+            ento += nz
+            continue
         d = np.zeros((nr, nc))
         cols = np.repeat(np.arange(nc), np.diff(pool.col_ptr[co:co + nc + 1]))
         d[pool.row_idx[eo:eo + nz], cols] = pool.values[eo:eo + nz]
@@ -345,8 +380,9 @@ def densify_pool(grid, pool: GridPool) -> GridPool:
                     values=np.concatenate(vals))
 
 
-def engine_for(grid, tree, *, device: int = 0, dense: bool = False, chunk: int = DEFAULT_CHUNK) -> Engine:
-    """Cached device plan of (grid, tree); dense=True uses full-rectangle blocks."""
+def engine_for(grid, tree, *, device: int = 0, dense: bool = False, chunk: int = DEFAULT_CHUNK,
+               dense_threshold: float | None = DEFAULT_DENSE_THRESHOLD) -> Engine:
+    """Cached device plan of (grid, tree); dense=True uses full-rectangle blocks everywhere."""
     cache = getattr(grid, "_lbk_engines", None)
     if cache is None:
         cache = {}
@@ -354,20 +390,17 @@ def engine_for(grid, tree, *, device: int = 0, dense: bool = False, chunk: int =
             grid._lbk_engines = cache
         except AttributeError:
             pass
-    key = (id(tree), device, dense, chunk)
+    key = (id(tree), device, dense, chunk, dense_threshold)
     eng = cache.get(key)
     if eng is None or eng.tree is not tree:
-        pool = pool_grid(grid)
-        if dense:
-            pool = densify_pool(grid, pool)
-        eng = Engine(grid, tree, device=device, chunk=chunk, pool=pool, dense=dense)
+        eng = Engine(grid, tree, device=device, chunk=chunk, dense=dense, dense_threshold=dense_threshold)
         cache[key] = eng
     return eng
 
 
 def factorize(grid, tree, workers: int = 1, pivot_tol: float = DEFAULT_PIVOT_TOL,
               static_pivot: float | None = None, dense_blas: bool = False, *, device: int = 0,
-              chunk: int = DEFAULT_CHUNK) -> LUFactors:
+              chunk: int = DEFAULT_CHUNK, dense_threshold: float | None = DEFAULT_DENSE_THRESHOLD) -> LUFactors:
     """Blocked right-looking LU on the B200 (factorize.py:245-384).
 
     ``workers`` is accepted for signature compatibility and ignored: the
@@ -380,7 +413,7 @@ def factorize(grid, tree, workers: int = 1, pivot_tol: float = DEFAULT_PIVOT_TOL
     if workers < 1:
         raise DimensionMismatch(f"workers must be >= 1, got {workers}")
     for dense in (False, True):
-        eng = engine_for(grid, tree, device=device, dense=dense, chunk=chunk)
+        eng = engine_for(grid, tree, device=device, dense=dense, chunk=chunk, dense_threshold=dense_threshold)
         vals_in = np.ascontiguousarray(eng.pool.values, dtype=np.float64)
         out = np.empty(eng.nnz, np.float64)
         perms = np.empty(max(eng.n_diag_rows, 1), np.int32)
@@ -463,7 +496,7 @@ def _run_mini(blocks, positions, tasks, perms=None, pivot_tol=DEFAULT_PIVOT_TOL,
     keys, pool = _full_pool(blocks)
     n = int(positions[-1])
     g = _MiniGrid(n, positions, pool)
-    eng = Engine(g, _MiniTree(tasks), pool=pool)
+    eng = Engine(g, _MiniTree(tasks), pool=pool, dense=True)
     try:
         eng.upload(pool.values)
         if perms is not None:
