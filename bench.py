@@ -197,8 +197,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--levels-out", default=None, help="write per-level device times + work to this .npz")
-    ap.add_argument("--dense-threshold", type=float, default=0.5,
-                    help="density tag for the FP64 DMMA kernels (reference: 0.5); <0 disables")
+    ap.add_argument("--dense-threshold", type=float, default=0.25,
+                    help="compressed-tile density tag for the FP64 DMMA kernels; <0 = CSC kernels only")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -215,8 +215,10 @@ def main():
     dt = None if args.dense_threshold < 0 else args.dense_threshold
     eng = Engine(g, t, device=local, dense_threshold=dt, dense_kernels=dt is not None)
     eng.upload()
-    log(f"[bench] plan: {eng.n_launch_levels} levels, {eng.n_launches} launches, {eng.n_items} sparse items, "
-        f"{eng.n_gemm_tiles} DMMA tiles, {eng.n_dense_items} dense items, {time.perf_counter() - t0:.1f}s")
+    log(f"[bench] plan: {eng.n_launch_levels} levels, {eng.n_launches} launches, {eng.n_items} CSC items, "
+        f"{eng.n_gemm_tiles} DMMA tiles, {eng.n_dense_items} panel items, {eng.n_tile_items} tiled-GETRF items; "
+        f"blocks sparse/rect/full {eng.n_sparse_blocks}/{eng.n_rect_blocks}/{eng.n_full_blocks}, "
+        f"working entries {eng.nnz_work / 1e6:.1f}M vs {eng.nnz / 1e6:.1f}M; {time.perf_counter() - t0:.1f}s")
 
     for _ in range(max(args.warmup, 0)):
         eng.run_device()

@@ -97,12 +97,17 @@ void lbk_destroy(lbk_ctx* ctx);
 /* Upload the block structure (the pooled BlockGrid of lbk_partition_fetch:
  * table[7 x nblocks], local col_ptr pool, local row_idx pool) and the
  * DependencyTree arrays (grid.py:172-181); builds the per-level work lists
- * (items of `chunk` columns/rows) and the CUDA graph lazily.  flags bit 0:
- * route full-rectangle (density-tagged) blocks to the FP64 DMMA kernels. */
+ * (items of `chunk` columns/rows) and the CUDA graph lazily.
+ * flags bit 0: DMMA storage — diagonal blocks become full dense tiles (tiled
+ *   multi-CTA GETRF) and every block whose nonempty-rows x nonempty-columns
+ *   rectangle holds >= tau of its entries becomes a compressed dense tile
+ *   (SSSSM/GESSM/TSTRF on FP64 tensor cores); other blocks stay CSC;
+ * flags bit 1: dense-scratch mode — every block a full tile, true row swaps
+ *   (the reference's dense scratch, factorize.py:265). */
 int lbk_plan(lbk_ctx* ctx, int64_t n, int64_t p, const int64_t* positions, int64_t nblocks,
              const int64_t* table, const int64_t* col_ptr, const int64_t* row_idx, int64_t ntasks,
              const int8_t* kinds, const int32_t* steps, const int32_t* rows, const int32_t* cols,
-             const int32_t* levels, const int64_t* costs, int32_t chunk, int32_t flags,
+             const int32_t* levels, const int64_t* costs, int32_t chunk, int32_t flags, double tau,
              lbk_status* st);
 
 /* Pristine A values in pool order, kept resident on the device. */
@@ -132,9 +137,10 @@ int lbk_set_perms(lbk_ctx* ctx, const int32_t* perms, lbk_status* st);
 int lbk_host_alloc(void** ptr, int64_t bytes);
 void lbk_host_free(void* ptr);
 
-/* info[0] = launched levels, info[1] = sparse work items, info[2] = diagonal
- * rows, info[3] = stored entries, info[4] = dense GEMM tiles, info[5] = dense
- * GETRF/GESSM/TSTRF items, info[6] = kernel launches per factorization. */
+/* info[12]: [0] launched levels, [1] CSC work items, [2] diagonal rows,
+ * [3] reference entries, [4] DMMA SSSSM tiles, [5] panel/exact items,
+ * [6] kernel launches per factorization, [7] working entries, [8..10]
+ * SPARSE/RECT/FULL blocks, [11] tiled-GETRF items. */
 int lbk_plan_info(lbk_ctx* ctx, int64_t* info);
 
 /* One instrumented replay: device ms of every launched level (load-balance

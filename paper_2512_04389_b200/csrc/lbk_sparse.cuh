@@ -1,0 +1,262 @@
+// lbk_sparse.cuh — warp-per-column / warp-per-row kernels on the CSC view.
+//
+// One warp owns one column (SSSSM, GESSM) or one row (TSTRF) of the output
+// block and keeps a dense accumulator of the block's span in shared memory
+// (scatter -> update -> gather, SPEC factorize DESIGN DECISIONS).  All
+// updates into one accumulator are issued by one warp in the reference's
+// order, so results are deterministic; GETRF/GESSM/TSTRF use separately
+// rounded mul/sub and true division like the reference's numpy loops
+// (factorize.py:38-130) and reproduce its bits on sparse blocks.
+
+#pragma once
+
+#include "lbk_common.cuh"
+
+namespace lbk {
+
+// C(k,j) -= L(k,i) U(i,j); Gustavson by target column (factorize.py:307-325).
+__device__ void ssssm_item(const Item& it, const DevPools& P, double* acc) {
+  const BlockDev L = P.blk[it.a], U = P.blk[it.b], C = P.blk[it.c];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int32_t* Lcp = P.colptr + L.cp;
+  const int32_t* Lr = P.rows + L.ent;
+  const double* Lv = P.vals + L.ent;
+  const int32_t* Ucp = P.colptr + U.cp;
+  const int32_t* Ur = P.rows + U.ent;
+  const double* Uv = P.vals + U.ent;
+  const int32_t* Ccp = P.colptr + C.cp;
+  const int32_t* Cr = P.rows + C.ent;
+  double* Cv = P.vals + C.ent;
+  for (int c = it.begin + warp; c < it.end; c += nw) {
+    const int u0 = Ucp[c], u1 = Ucp[c + 1];
+    if (u0 == u1) continue;
+    const int c0 = Ccp[c], c1 = Ccp[c + 1];
+    for (int e = c0 + lane; e < c1; e += 32) acc[Cr[e]] = 0.0;
+    __syncwarp();
+    for (int e = u0; e < u1; ++e) {
+      const double u = Uv[e];
+      if (u == 0.0) continue;  // exact-zero operand: no contribution (warp-uniform)
+      const int r = Ur[e];
+      const int l0 = Lcp[r], l1 = Lcp[r + 1];
+      for (int f = l0 + lane; f < l1; f += 32) acc[Lr[f]] = fma(Lv[f], u, acc[Lr[f]]);
+      __syncwarp();
+    }
+    for (int e = c0 + lane; e < c1; e += 32) Cv[e] -= acc[Cr[e]];
+    __syncwarp();
+  }
+}
+
+// X(i,j) <- L_ii^{-1} P_i X(i,j); one warp per column of X (factorize.py:98-109).
+__device__ void gessm_item(const Item& it, const DevPools& P, double* acc) {
+  const BlockDev D = P.blk[it.a], X = P.blk[it.b];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int32_t* Dcp = P.colptr + D.cp;
+  const int32_t* Dr = P.rows + D.ent;
+  const double* Dv = P.vals + D.ent;
+  const int32_t* perm = P.perm + D.dg;
+  const int32_t* Xcp = P.colptr + X.cp;
+  const int32_t* Xr = P.rows + X.ent;
+  double* Xv = P.vals + X.ent;
+  const bool dfull = D.store == STORE_FULL;
+  const int m = D.nrows;
+  const bool permute = (it.c != 0) && X.store == STORE_FULL;
+  for (int c = it.begin + warp; c < it.end; c += nw) {
+    const int x0 = Xcp[c], x1 = Xcp[c + 1];
+    if (x0 == x1) continue;
+    if (permute) {
+      for (int e = x0 + lane; e < x1; e += 32) acc[Xr[e]] = Xv[x0 + perm[Xr[e]]];
+    } else {
+      for (int e = x0 + lane; e < x1; e += 32) acc[Xr[e]] = Xv[e];
+    }
+    __syncwarp();
+    if (dfull) {
+      // dense L_ii: restrict the solve to X's own rows (the result pattern is
+      // closed under L, so other rows stay exactly zero)
+      for (int e = x0; e < x1; ++e) {
+        const int k = Xr[e];
+        const double xk = acc[k];
+        const double* lk = Dv + static_cast<size_t>(k) * m;
+        for (int f = e + 1 + lane; f < x1; f += 32) {
+          const int q = Xr[f];
+          acc[q] = dsub_mul(acc[q], lk[q], xk);
+        }
+        __syncwarp();
+      }
+    } else {
+      const int32_t* dpos = P.diag_csc + D.dg;
+      for (int e = x0; e < x1; ++e) {
+        const int k = Xr[e];
+        const double xk = acc[k];
+        const int f1 = Dcp[k + 1];
+        for (int f = dpos[k] + 1 + lane; f < f1; f += 32) {
+          const int q = Dr[f];
+          acc[q] = dsub_mul(acc[q], Dv[f], xk);
+        }
+        __syncwarp();
+      }
+    }
+    for (int e = x0 + lane; e < x1; e += 32) Xv[e] = acc[Xr[e]];
+    __syncwarp();
+  }
+}
+
+// X(k,i) <- X(k,i) U_ii^{-1}; one warp per row of X via its CSR index (factorize.py:112-130).
+__device__ void tstrf_item(const Item& it, const DevPools& P, double* acc) {
+  const BlockDev D = P.blk[it.a], X = P.blk[it.b];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const double* Dv = P.vals + D.ent;
+  const int32_t* Xrp = P.csr_ptr + X.rp;
+  const int32_t* Xcc = P.csr_col + X.csr;
+  const int32_t* Xcpos = P.csr_pos + X.csr;
+  double* Xv = P.vals + X.ent;
+  const bool dfull = D.store == STORE_FULL;
+  const int m = D.nrows;
+  for (int q = it.begin + warp; q < it.end; q += nw) {
+    const int r0 = Xrp[q], r1 = Xrp[q + 1];
+    if (r0 == r1) continue;
+    for (int e = r0 + lane; e < r1; e += 32) acc[Xcc[e]] = Xv[Xcpos[e]];
+    __syncwarp();
+    if (dfull) {
+      for (int e = r0; e < r1; ++e) {
+        const int k = Xcc[e];
+        const double xk = __ddiv_rn(acc[k], Dv[static_cast<size_t>(k) * m + k]);
+        __syncwarp();
+        if (lane == 0) acc[k] = xk;
+        for (int f = e + 1 + lane; f < r1; f += 32) {
+          const int j = Xcc[f];
+          acc[j] = dsub_mul(acc[j], xk, Dv[static_cast<size_t>(j) * m + k]);
+        }
+        __syncwarp();
+      }
+    } else {
+      const int32_t* Dcsc = P.diag_csc + D.dg;
+      const int32_t* Drow = P.diag_csr + D.dg;
+      const int32_t* Drp = P.csr_ptr + D.rp;
+      const int32_t* Dcc = P.csr_col + D.csr;
+      const int32_t* Dcpos = P.csr_pos + D.csr;
+      for (int e = r0; e < r1; ++e) {
+        const int k = Xcc[e];
+        const double xk = __ddiv_rn(acc[k], Dv[Dcsc[k]]);
+        __syncwarp();
+        if (lane == 0) acc[k] = xk;
+        const int g1 = Drp[k + 1];
+        for (int g = Drow[k] + 1 + lane; g < g1; g += 32) {
+          const int j = Dcc[g];
+          acc[j] = dsub_mul(acc[j], xk, Dv[Dcpos[g]]);
+        }
+        __syncwarp();
+      }
+    }
+    for (int e = r0 + lane; e < r1; e += 32) Xv[Xcpos[e]] = acc[Xcc[e]];
+    __syncwarp();
+  }
+}
+
+// Left-looking LU of a SPARSE diagonal block (all-sparse mode): the CTA
+// owns the block, warps take the columns of one intra-block level at a time.
+__device__ void getrf_item(const Item& it, const DevPools& P, double* acc, double pivot_tol,
+                           double static_eps) {
+  const BlockDev D = P.blk[it.a];
+  const int step = it.b;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int32_t* Dcp = P.colptr + D.cp;
+  const int32_t* Dr = P.rows + D.ent;
+  double* Dv = P.vals + D.ent;
+  const int32_t* dpos = P.diag_csc + D.dg;
+  int32_t* perm = P.perm + D.dg;
+  const int32_t* lvc = P.lv_cols + D.lvc;
+  const int32_t* lvp = P.lv_ptr + D.lvp;
+  const bool use_static = !isnan(static_eps);
+  const int m = D.nrows;
+  for (int r = threadIdx.x; r < m; r += blockDim.x) perm[r] = r;
+  __syncthreads();
+  for (int lv = 0; lv < D.nlev; ++lv) {
+    for (int idx = lvp[lv] + warp; idx < lvp[lv + 1]; idx += nw) {
+      const int c = lvc[idx];
+      const int d0 = Dcp[c], d1 = Dcp[c + 1], dp = dpos[c];
+      double cmax = 0.0;
+      for (int e = d0 + lane; e < d1; e += 32) {
+        const double v = Dv[e];
+        acc[Dr[e]] = v;
+        cmax = fmax(cmax, fabs(v));
+      }
+      for (int o = 16; o; o >>= 1) cmax = fmax(cmax, __shfl_xor_sync(0xffffffffu, cmax, o));
+      __syncwarp();
+      for (int e = d0; e < dp; ++e) {
+        const int k = Dr[e];
+        const double xk = acc[k];
+        const int f1 = Dcp[k + 1];
+        for (int f = dpos[k] + 1 + lane; f < f1; f += 32) {
+          const int q = Dr[f];
+          acc[q] = dsub_mul(acc[q], Dv[f], xk);
+        }
+        __syncwarp();
+      }
+      double best = -1.0;
+      int brow = m;
+      for (int e = dp + lane; e < d1; e += 32) {
+        const int q = Dr[e];
+        const double a = fabs(acc[q]);
+        if (a > best || (a == best && q < brow)) { best = a; brow = q; }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int orow = __shfl_xor_sync(0xffffffffu, brow, o);
+        if (ob > best || (ob == best && orow < brow)) { best = ob; brow = orow; }
+      }
+      if (best == 0.0 || best < pivot_tol * cmax) {
+        if (use_static) {
+          if (lane == 0) {
+            const double cur = acc[c];
+            acc[c] = (cur == 0.0) ? static_eps : copysign(static_eps, cur);
+          }
+        } else if (lane == 0) {
+          record(&P.err[0], step, c);
+        }
+      } else if (brow != c && lane == 0) {
+        record(&P.err[1], step, c);  // sparse storage cannot represent the swap
+      }
+      __syncwarp();
+      const double piv = acc[c];
+      for (int e = dp + 1 + lane; e < d1; e += 32) {
+        const int q = Dr[e];
+        acc[q] = __ddiv_rn(acc[q], piv);
+      }
+      __syncwarp();
+      for (int e = d0 + lane; e < d1; e += 32) Dv[e] = acc[Dr[e]];
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) level_kernel(const Item* __restrict__ items, DevPools P, int acc_len,
+                                                    double pivot_tol, double static_eps) {
+  extern __shared__ double smem[];
+  const Item it = items[blockIdx.x];
+  double* acc = smem + static_cast<size_t>(threadIdx.x >> 5) * acc_len;
+  switch (it.kind) {
+    case KIND_SSSSM: ssssm_item(it, P, acc); break;
+    case KIND_GESSM: gessm_item(it, P, acc); break;
+    case KIND_TSTRF: tstrf_item(it, P, acc); break;
+    default: getrf_item(it, P, acc, pivot_tol, static_eps); break;
+  }
+}
+
+// I/O between the reference layout (pool order of the filled pattern) and
+// the working layout: work[map[e]] = in[e] / out[e] = work[map[e]].
+__global__ void scatter_kernel(const double* __restrict__ in, const int64_t* __restrict__ map,
+                               double* __restrict__ work, int64_t n) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    work[map[e]] = in[e];
+}
+
+__global__ void gather_kernel(const double* __restrict__ work, const int64_t* __restrict__ map,
+                              double* __restrict__ out, int64_t n) {
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[e] = work[map[e]];
+}
+
+}  // namespace lbk

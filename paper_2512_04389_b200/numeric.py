@@ -32,7 +32,10 @@ from .matrix_io import CscMatrix
 
 DEFAULT_PIVOT_TOL = 1e-12
 DEFAULT_CHUNK = 8
-DEFAULT_DENSE_THRESHOLD = 0.5  # reference density tag (factorize.py:274)
+# compressed-tile tag: a block whose nonempty-rows x nonempty-columns rectangle
+# holds >= this fraction of entries runs on the DMMA kernels (the reference's
+# own dense tag is 0.5 of the FULL block, factorize.py:274)
+DEFAULT_DENSE_THRESHOLD = 0.25
 
 P = _native.ptr
 i64p, i32p, i8p, f64p = _native.c_i64p, _native.c_i32p, _native.c_i8p, _native.c_f64p
@@ -54,7 +57,7 @@ def _dev():
     d(lib, "lbk_create", C.c_int, [C.POINTER(vp), C.c_int, st])
     d(lib, "lbk_destroy", None, [vp])
     d(lib, "lbk_plan", C.c_int, [vp, C.c_int64, C.c_int64, i64p, C.c_int64, i64p, i64p, i64p, C.c_int64,
-                                 i8p, i32p, i32p, i32p, i32p, i64p, C.c_int32, C.c_int32, st])
+                                 i8p, i32p, i32p, i32p, i32p, i64p, C.c_int32, C.c_int32, C.c_double, st])
     d(lib, "lbk_upload_values", C.c_int, [vp, f64p, st])
     d(lib, "lbk_factorize", C.c_int, [vp, C.c_double, C.c_double, C.POINTER(C.c_float), st])
     d(lib, "lbk_factorize_host", C.c_int, [vp, f64p, f64p, i32p, C.c_double, C.c_double, st])
@@ -108,16 +111,15 @@ class Engine:
     def __init__(self, grid, tree, *, device: int = 0, chunk: int = DEFAULT_CHUNK, pool: GridPool | None = None,
                  dense: bool = False, dense_threshold: float | None = DEFAULT_DENSE_THRESHOLD,
                  dense_kernels: bool = True):
+        """dense=True: dense-scratch mode (every block a full tile, true row swaps).
+        dense_threshold: tau of the compressed-tile tag (see include/lbk.h lbk_plan);
+        None / dense_kernels=False keeps every block CSC (sparse kernels only)."""
         self.lib = _dev()
         self.grid = grid
         self.tree = tree
-        base = pool if pool is not None else pool_grid(grid)
-        if dense:
-            base = densify_pool(grid, base, 0.0)
-        elif dense_threshold is not None:
-            base = densify_pool(grid, base, dense_threshold)
-        self.pool = base
-        self.dense_threshold = 0.0 if dense else dense_threshold
+        self.pool = pool if pool is not None else pool_grid(grid)
+        use_tiles = dense_kernels and dense_threshold is not None
+        self.dense_threshold = 0.0 if dense else (dense_threshold if use_tiles else None)
         self.device = device
         ctx = C.c_void_p()
         st = _native.LbkStatus()
@@ -151,14 +153,19 @@ class Engine:
         rc = self.lib.lbk_plan(ctx, grid.n, grid.p, P(pos, i64p), pl.nblocks, P(t, i64p), P(cp, i64p),
                                P(ri, i64p), len(k), P(k, i8p), P(s, i32p), P(r, i32p), P(c, i32p),
                                P(lv, i32p), P(co, i64p), int(chunk),
-                               (1 if dense_kernels else 0) | (2 if dense else 0), C.byref(st))
+                               (1 if (use_tiles or dense) else 0) | (2 if dense else 0),
+                               float(dense_threshold if use_tiles else 1.0), C.byref(st))
         if rc:
             _native.raise_status(st, "lbk_plan")
         self.nnz = int(pl.values.shape[0])
-        info = np.zeros(8, np.int64)
+        info = np.zeros(12, np.int64)
         self.lib.lbk_plan_info(ctx, P(info, i64p))
+        self.info = info
         self.n_launch_levels, self.n_items, self.n_diag_rows = int(info[0]), int(info[1]), int(info[2])
         self.n_gemm_tiles, self.n_dense_items, self.n_launches = int(info[4]), int(info[5]), int(info[6])
+        self.nnz_work = int(info[7])
+        self.n_sparse_blocks, self.n_rect_blocks, self.n_full_blocks = int(info[8]), int(info[9]), int(info[10])
+        self.n_tile_items = int(info[11])
         self._resident = False
 
     def close(self):
@@ -330,54 +337,6 @@ def build_factors(grid, pool: GridPool, values: np.ndarray, perms_pool: np.ndarr
             perms.append(np.arange(s))
         off += s
     return LUFactors(n=grid.n, plan=grid.plan, l_blocks=lb, u_blocks=ub, perms=perms)
-
-
-def densify_pool(grid, pool: GridPool, threshold: float = 0.0) -> GridPool:
-    """Widen every block with nnz >= threshold * nrows * ncols to its full
-    rectangle (column-major dense tile, ld = nrows).
-
-    threshold 0.5 is the reference's density tag (nnz*2 >= nrows*ncols,
-    factorize.py:271-275): those blocks run on the FP64 DMMA kernels.
-    threshold 0 widens every block (the reference's dense scratch,
-    factorize.py:265) and makes block-local row swaps representable.
-    Positions outside the filled pattern stay exactly zero and are dropped
-    again on export (factorize.py:179-192), so the exported structure is
-    unchanged.
-    """
-    tb = pool.table
-    widen = tb[4] * 1.0 >= threshold * tb[2] * tb[3]
-    if threshold == 0.5:
-        widen = tb[4] * 2 >= tb[2] * tb[3]
-    widen &= tb[4] < tb[2] * tb[3]  # already full blocks need no copy
-    if not widen.any():
-        return pool
-    t = tb.copy()
-    cps, ris, vals = [], [], []
-    cpo = ento = 0
-    for b in range(pool.nblocks):
-        bi, bj, nr, nc, nz, co, eo = (int(x) for x in pool.table[:, b])
-        if not widen[b]:
-            cps.append(pool.col_ptr[co:co + nc + 1])
-            ris.append(pool.row_idx[eo:eo + nz])
-            vals.append(pool.values[eo:eo + nz])
-            t[5, b] = cpo
-            t[6, b] = ento
-            cpo += nc + 1
-            ento += nz
-            continue
-        d = np.zeros((nr, nc))
-        cols = np.repeat(np.arange(nc), np.diff(pool.col_ptr[co:co + nc + 1]))
-        d[pool.row_idx[eo:eo + nz], cols] = pool.values[eo:eo + nz]
-        cps.append(np.arange(nc + 1, dtype=np.int64) * nr)
-        ris.append(np.tile(np.arange(nr, dtype=np.int64), nc))
-        vals.append(d.T.ravel())
-        t[4, b] = nr * nc
-        t[5, b] = cpo
-        t[6, b] = ento
-        cpo += nc + 1
-        ento += nr * nc
-    return GridPool(table=t, col_ptr=np.concatenate(cps), row_idx=np.concatenate(ris),
-                    values=np.concatenate(vals))
 
 
 def engine_for(grid, tree, *, device: int = 0, dense: bool = False, chunk: int = DEFAULT_CHUNK,
