@@ -245,26 +245,57 @@ def main():
     e2e_s = max_over_ranks((time.perf_counter() - t0) / ke, world)
     e2e_value = world * total_flops / e2e_s / 1e9
 
-    # per-level device times (instrumented replay) -> roofline of the level kernel
-    lvl_ms = eng.level_times()
-    lv, items = eng.plan_levels()
-    task_level = t.levels_of
-    kept = np.unique(task_level)
-    lvl_bytes = np.bincount(task_level, weights=bytes_t, minlength=t.n_levels)[kept]
-    lvl_flops = np.bincount(task_level, weights=flops_t, minlength=t.n_levels)[kept]
-    if len(kept) != len(lvl_ms):  # levels with only skipped tasks are not launched
-        lvl_bytes = lvl_bytes[: len(lvl_ms)]
-        lvl_flops = lvl_flops[: len(lvl_ms)]
-    kern_s = max(float(lvl_ms.sum()) / 1e3, 1e-12)
-    peak, peak_src = peaks()
-    achieved = float(bytes_t.sum()) / kern_s / 1e9
+    # per-level / per-kernel-family device times (instrumented replay) -> roofline
+    lvl = eng.level_times()  # [levels x 5]: level, DMMA SSSSM, panel, tiled GETRF, CSC kernel
+    routes = eng.task_routes()
+    fam_names = {1: "gemm_map_kernel (DMMA SSSSM)", 2: "panel_kernel (DMMA GESSM/TSTRF)",
+                 3: "tiled GETRF (tile_getrf/trsm/gemm)", 0: "level_kernel (CSC SSSSM/GESSM/TSTRF)"}
+    fam_col = {1: 1, 2: 2, 3: 3, 0: 4}
+    fams = {}
+    for r, col in fam_col.items():
+        sel = routes == r
+        ms_f = float(lvl[:, col].sum())
+        fams[r] = {"kernel": fam_names[r], "ms": ms_f, "tasks": int(sel.sum()),
+                   "gflop": float(flops_t[sel].sum()) / 1e9, "gbytes": float(bytes_t[sel].sum()) / 1e9,
+                   "launches": int((lvl[:, col] > 0).sum())}
+    dom = max(fams, key=lambda r: fams[r]["ms"])
+    hbm_peak, hbm_src = peaks()
+    try:
+        from paper_2512_04389_b200.numeric import fp64_peak
+
+        dmma_peak, dfma_peak = fp64_peak(local)
+    except Exception as exc:  # pragma: no cover
+        log(f"[bench] fp64 peak probe failed: {exc}")
+        dmma_peak, dfma_peak = float("nan"), float("nan")
+    for r, fv in fams.items():
+        s = max(fv["ms"], 1e-9) / 1e3
+        fv["tflops"] = fv["gflop"] / s / 1e3
+        fv["gbs"] = fv["gbytes"] / s
+        fv["frac_fp64_tensor"] = fv["tflops"] / dmma_peak if dmma_peak == dmma_peak else None
+        fv["frac_hbm"] = fv["gbs"] / hbm_peak
+    D = fams[dom]
+    if dom in (1, 2, 3):
+        roof = {"bound": "tensor", "achieved": D["tflops"], "peak": dmma_peak, "unit": "TFLOP/s",
+                "frac": D["tflops"] / dmma_peak if dmma_peak == dmma_peak else None,
+                "peak_source": "FP64 DMMA.8x8x4 register loop measured on this GPU by csrc/lbk_peak.cu "
+                               "(MEASURED_PEAKS.json has no FP64 entry)"}
+    else:
+        roof = {"bound": "hbm", "achieved": D["gbs"], "peak": hbm_peak, "unit": "GB/s",
+                "frac": D["gbs"] / hbm_peak, "peak_source": hbm_src}
     traffic = None
     tp = os.path.join(REPO, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+    roof.update({"traffic": traffic, "kernel": D["kernel"], "launches_per_step": D["launches"],
+                 "algorithmic": "flops = 2*tree.costs (SSSSM), GETRF/panel formulas of SURVEY 8d; "
+                                "bytes = 8 B/value + 4 B/index per touched block",
+                 "by_kernel": {fams[r]["kernel"]: {k: v for k, v in fams[r].items() if k != "kernel"}
+                               for r in fams},
+                 "fp64_peaks_tflops": {"dmma": dmma_peak, "dfma": dfma_peak},
+                 "hbm_peak_gbs": hbm_peak})
     if args.levels_out:
-        np.savez(args.levels_out, level_ms=lvl_ms, level_bytes=lvl_bytes, level_flops=lvl_flops,
-                 levels=lv, kinds=t.kinds, levels_of=t.levels_of, costs=t.costs)
+        np.savez(args.levels_out, level_ms=lvl, routes=routes, flops=flops_t, bytes=bytes_t,
+                 kinds=t.kinds, levels_of=t.levels_of, costs=t.costs)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -288,12 +319,11 @@ def main():
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "seconds_per_step": e2e_s,
                     "h2d_bytes_per_step": 8 * eng.nnz, "d2h_bytes_per_step": 8 * eng.nnz + 4 * eng.n_diag_rows,
                     "path": "Engine.run_host -> lbk_factorize_host (C-ABI), pinned host buffers"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "kernel": "level_kernel",
-                         "launches_per_step": int(eng.n_launches), "dense_threshold": dt,
-                         "algorithmic_bytes_per_step": float(bytes_t.sum()),
-                         "mean_launch_ms": float(lvl_ms.mean()), "peak_source": peak_src,
-                         "fp64_gflops_in_kernel": total_flops / kern_s / 1e9},
+            "roofline": roof,
+            "plan": {"dense_threshold": dt, "launches_per_step": int(eng.n_launches),
+                     "blocks_sparse_rect_full": [eng.n_sparse_blocks, eng.n_rect_blocks, eng.n_full_blocks],
+                     "working_entries": eng.nnz_work, "reference_entries": eng.nnz,
+                     "level_ms_sum": float(lvl[:, 0].sum())},
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": int(args.steps * eng.n_launches),

@@ -42,18 +42,21 @@ typedef struct lbk_status {
 } lbk_status;
 
 /* ======================================================================== *
- * Host structure path (liblbk_host.so).  run -> fetch -> free protocol: run
- * computes and reports the output sizes, the caller allocates, fetch copies.
+ * Host structure path (liblbk_host.so).  Large outputs: count first, the
+ * caller allocates, fill writes straight into the caller's buffers.
  * ======================================================================== */
 
 /* symbolic_factorize(a_sym) -> FilledPattern        symbolic.py:57-108
  * Input: symmetrized CSC (col_ptr[n+1], row_idx[nnz], sorted rows).
- * Output: col_ptr[n+1], row_idx[nnz_filled] of L+L^T+I, (col,row)-sorted;
- * parent[n] = elimination tree. */
-int lbk_symbolic_run(int64_t n, const int64_t* col_ptr, const int64_t* row_idx,
-                     void** handle, int64_t* nnz_filled);
-int lbk_symbolic_fetch(void* handle, int64_t* col_ptr, int64_t* row_idx, int64_t* parent);
-void lbk_symbolic_free(void* handle);
+ * nnz: *nnz_filled = nnz(L+L^T+I).  fill: col_ptr[n+1], row_idx[nnz_filled]
+ * (col,row)-sorted; parent[n] = elimination tree (may be NULL). */
+int lbk_symbolic_nnz(int64_t n, const int64_t* col_ptr, const int64_t* row_idx, int64_t* nnz_filled);
+int lbk_symbolic_fill(int64_t n, const int64_t* col_ptr, const int64_t* row_idx, int64_t* out_col_ptr,
+                      int64_t* out_row_idx, int64_t* parent);
+
+/* diag_block_pointer(f).blockptr (Alg. 2)             features.py:44-54
+ * blockptr[n+1]; the pattern must be symmetric with a full diagonal. */
+int lbk_blockptr(int64_t n, const int64_t* col_ptr, const int64_t* row_idx, int64_t* blockptr);
 
 /* _require_symmetric_full_diag(col_ptr, row_idx, n)     symbolic.py:46-54
  * 0 = ok, 1 = missing diagonal (*ndiag = count), 2 = not symmetric,
@@ -61,18 +64,18 @@ void lbk_symbolic_free(void* handle);
 int lbk_check_symmetric(int64_t n, const int64_t* col_ptr, const int64_t* row_idx, int64_t* ndiag);
 
 /* partition(f, a, plan) -> BlockGrid                 grid.py:85-148
- * Output block table (7 x nblocks, row-major by field):
- *   bi, bj, nrows, ncols, nnz, colptr_offset, entry_offset
- * in column-major block order (the reference dict order), pooled local
- * col_ptr (sum of ncols+1), local row_idx and values (nnz_filled each),
- * block_nnz[p*p] row-major. */
-int lbk_partition_run(int64_t n, const int64_t* f_col_ptr, const int64_t* f_row_idx,
-                      const int64_t* a_col_ptr, const int64_t* a_row_idx,
-                      const double* a_values, int64_t p, const int64_t* positions,
-                      void** handle, int64_t* nblocks, int64_t* colptr_len);
-int lbk_partition_fetch(void* handle, int64_t* table, int64_t* col_ptr, int64_t* row_idx,
-                        double* values, int64_t* block_nnz);
-void lbk_partition_free(void* handle);
+ * count: number of stored blocks and pooled col_ptr length.  fill: block
+ * table (7 x nblocks, row-major by field: bi, bj, nrows, ncols, nnz,
+ * colptr_offset, entry_offset) in column-major block order (the reference
+ * dict order), pooled local col_ptr, local row_idx and values (A's values
+ * scattered, 0.0 at fill), block_nnz[p*p] row-major.  Returns
+ * LBK_ERR_DIM_MISMATCH if A is not covered by the filled pattern. */
+int lbk_partition_count(int64_t n, const int64_t* f_col_ptr, const int64_t* f_row_idx, int64_t p,
+                        const int64_t* positions, int64_t* nblocks, int64_t* colptr_len);
+int lbk_partition_fill(int64_t n, const int64_t* f_col_ptr, const int64_t* f_row_idx,
+                       const int64_t* a_col_ptr, const int64_t* a_row_idx, const double* a_values,
+                       int64_t p, const int64_t* positions, int64_t nblocks, int64_t* table,
+                       int64_t* col_ptr, int64_t* row_idx, double* values, int64_t* block_nnz);
 
 /* dependency_levels(grid) -> DependencyTree            grid.py:223-378 */
 int lbk_levels_run(int64_t p, int64_t nblocks, const int64_t* table, const int64_t* col_ptr,
@@ -127,6 +130,12 @@ int lbk_factorize_host(lbk_ctx* ctx, const double* a_values, double* lu_values, 
 /* Copy the last factorization's values / perms to the host. */
 int lbk_download(lbk_ctx* ctx, double* lu_values, int32_t* perms, lbk_status* st);
 
+/* Working-layout values of the last factorization (*nwork entries; pass
+ * work = NULL to query the size).  In dense-scratch mode every block is a
+ * full column-major tile in pool block order: the caller rebuilds blocks
+ * whose support moved under row swaps (factorize.py:370-381). */
+int lbk_download_work(lbk_ctx* ctx, double* work, int64_t* nwork, lbk_status* st);
+
 /* Overwrite the per-diagonal-row permutations (pool order of the diagonal
  * blocks).  Used by the kernel-level entry points factor_u_panel
  * (factorize.py:150-156), which take an explicit perm_i, when the plan
@@ -143,8 +152,20 @@ void lbk_host_free(void* ptr);
  * SPARSE/RECT/FULL blocks, [11] tiled-GETRF items. */
 int lbk_plan_info(lbk_ctx* ctx, int64_t* info);
 
-/* One instrumented replay: device ms of every launched level (load-balance
- * evidence next to metrics.level_work_stats, pkg/src/lublock/metrics.py:63-90). */
+/* Per task of the DependencyTree: the kernel family that executes it
+ * (-1 skipped: zero-work update; 0 CSC kernel; 1 DMMA SSSSM; 2 panel solve;
+ * 3 tiled GETRF).  route[ntasks]. */
+int lbk_task_routes(lbk_ctx* ctx, int8_t* route);
+
+/* FP64 throughput microbenchmark (register-resident DMMA.8x8x4 and DFMA
+ * loops on every SM): the dense-block roofline denominator, which
+ * MEASURED_PEAKS.json does not carry.  TFLOP/s out. */
+int lbk_fp64_peak(int device, double* tflops_dmma, double* tflops_dfma);
+
+/* One instrumented replay: device ms of every launched level and of each
+ * kernel family inside it, out_ms[nlevels x 5] = level, DMMA SSSSM, panel
+ * solves, tiled GETRF, CSC kernel (load-balance evidence next to
+ * metrics.level_work_stats, pkg/src/lublock/metrics.py:63-90). */
 int lbk_level_times(lbk_ctx* ctx, double pivot_tol, double static_eps, float* out_ms, lbk_status* st);
 
 /* Launched-level table (4 x nlevels: item offset, items, warps, acc length)

@@ -63,15 +63,14 @@ def host_lib():
             raise ImportError(f"{HOST_LIB} missing: run __graft_entry__.build() first")
         lib = C.CDLL(HOST_LIB)
         i64 = C.c_int64
-        _declare(lib, "lbk_symbolic_run", C.c_int, [i64, c_i64p, c_i64p, c_vpp, c_i64p])
-        _declare(lib, "lbk_symbolic_fetch", C.c_int, [C.c_void_p, c_i64p, c_i64p, c_i64p])
-        _declare(lib, "lbk_symbolic_free", None, [C.c_void_p])
+        _declare(lib, "lbk_symbolic_nnz", C.c_int, [i64, c_i64p, c_i64p, c_i64p])
+        _declare(lib, "lbk_symbolic_fill", C.c_int, [i64, c_i64p, c_i64p, c_i64p, c_i64p, c_i64p])
+        _declare(lib, "lbk_blockptr", C.c_int, [i64, c_i64p, c_i64p, c_i64p])
         _declare(lib, "lbk_check_symmetric", C.c_int, [i64, c_i64p, c_i64p, c_i64p])
-        _declare(lib, "lbk_partition_run", C.c_int,
-                 [i64, c_i64p, c_i64p, c_i64p, c_i64p, c_f64p, i64, c_i64p, c_vpp, c_i64p, c_i64p])
-        _declare(lib, "lbk_partition_fetch", C.c_int,
-                 [C.c_void_p, c_i64p, c_i64p, c_i64p, c_f64p, c_i64p])
-        _declare(lib, "lbk_partition_free", None, [C.c_void_p])
+        _declare(lib, "lbk_partition_count", C.c_int, [i64, c_i64p, c_i64p, i64, c_i64p, c_i64p, c_i64p])
+        _declare(lib, "lbk_partition_fill", C.c_int,
+                 [i64, c_i64p, c_i64p, c_i64p, c_i64p, c_f64p, i64, c_i64p, i64, c_i64p, c_i64p, c_i64p,
+                  c_f64p, c_i64p])
         _declare(lib, "lbk_levels_run", C.c_int,
                  [i64, i64, c_i64p, c_i64p, c_i64p, c_vpp, c_i64p, c_i64p])
         _declare(lib, "lbk_levels_fetch", C.c_int,

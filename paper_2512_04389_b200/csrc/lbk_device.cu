@@ -97,6 +97,7 @@ struct lbk_ctx {
   std::vector<BlockDev> hblk;
   std::vector<Level> levels;
   std::vector<SubStep> subs;
+  std::vector<int8_t> route;  // per task: -1 skipped, 0 CSC kernel, 1 DMMA SSSSM, 2 panel, 3 tiled GETRF
   int64_t n_generic = 0, n_gemm = 0, n_panel = 0, n_tile = 0;
   int64_t store_count[3] = {0, 0, 0};
   // device
@@ -450,6 +451,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     std::vector<std::vector<DenseItem>> pan(nlevels), exa(nlevels);
     std::vector<int32_t> pan_smem(nlevels, 0), exa_smem(nlevels, 0);
     std::vector<std::vector<int64_t>> tgetrf(nlevels);  // FULL diagonal blocks factored by the tiled GETRF
+    c->route.assign(ntasks, -1);
     auto add_range = [&](int32_t lv, Item base, int32_t count) {
       for (int32_t s = 0; s < count; s += chunk) {
         Item it = base;
@@ -471,6 +473,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           // tiled multi-CTA GETRF (no-swap speculation, verified); the exact
           // single-CTA variant is kept for dense-scratch / static pivoting
           tgetrf[lv].push_back(dblk);
+          c->route[t] = 3;
           DenseItem d{0, static_cast<int32_t>(dblk), static_cast<int32_t>(i), all_full ? 1 : 0, 0,
                       static_cast<int32_t>(i)};
           exa[lv].push_back(d);
@@ -478,6 +481,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         } else {
           it.a = static_cast<int32_t>(dblk);
           it.b = static_cast<int32_t>(i);
+          c->route[t] = 0;
           it.begin = 0;
           it.end = 1;
           gen[lv].push_back(it);
@@ -489,18 +493,21 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         it.b = static_cast<int32_t>(x);
         it.c = all_full ? 1 : 0;  // row permutation of FULL panels (dense-scratch mode)
         if (hb[dblk].store == STORE_FULL && tile_like(x)) {
+          c->route[t] = 2;
           for (int32_t s = 0; s < hb[x].nC; s += STRIP)
             pan[lv].push_back(DenseItem{1, it.a, it.b, it.c, s, static_cast<int32_t>(i)});
           pan_smem[lv] = std::max(pan_smem[lv], (hb[x].nR + 64) * 8);
           continue;
         }
         acc_len[lv] = std::max(acc_len[lv], hb[x].nrows);
+        c->route[t] = 0;
         add_range(lv, it, hb[x].ncols);
       } else if (kind == KIND_TSTRF) {
         const int64_t x = bid[r * p + i];
         it.a = static_cast<int32_t>(dblk);
         it.b = static_cast<int32_t>(x);
         if (hb[dblk].store == STORE_FULL && tile_like(x)) {
+          c->route[t] = 2;
           for (int32_t s = 0; s < hb[x].nR; s += STRIP)
             pan[lv].push_back(DenseItem{2, it.a, it.b, 0, s, static_cast<int32_t>(i)});
           pan_smem[lv] = std::max(pan_smem[lv], 64 * 8);
@@ -509,6 +516,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         if (hb[x].store != STORE_SPARSE || (hb[dblk].store == STORE_SPARSE && hb[dblk].rp < 0))
           return fail(st, LBK_ERR_BAD_ARG, "TSTRF operand without a CSR index");
         acc_len[lv] = std::max(acc_len[lv], hb[x].ncols);
+        c->route[t] = 0;
         add_range(lv, it, hb[x].nrows);
       } else {
         const int64_t tgt = bid[r * p + cc];
@@ -565,12 +573,14 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
             hmaps.insert(hmaps.end(), cm.begin(), cm.end());
           }
           const int32_t task = static_cast<int32_t>(gtasks.size());
+          c->route[t] = 1;
           gtasks.push_back(gt);
           for (int32_t n0 = 0; n0 < hb[ub].nC; n0 += GBN)
             for (int32_t m0 = 0; m0 < hb[lb].nR; m0 += GBM) gem[lv].push_back(GemmItem{task, m0, n0});
           continue;
         }
         acc_len[lv] = std::max(acc_len[lv], hb[tgt].nrows);
+        c->route[t] = 0;
         add_range(lv, it, hb[tgt].ncols);
       }
     }
@@ -728,25 +738,34 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
     const Level& L = c->levels[l];
     const bool has_t = !exact && L.ntcol > 0;
     const bool br[NBRANCH] = {L.ngemm > 0, L.npanel > 0 || (exact && L.nexact > 0), has_t};
+    // instrumented replays: per level [end, gemm b/e, panel b/e, getrf b/e, csc b/e]
+    auto rec = [&](int k, cudaStream_t s) {
+      if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 9 + k], s, cudaEventRecordExternal);
+    };
     if (br[0] || br[1] || br[2]) cudaEventRecord(c->fork, s0);
     if (br[0]) {
       cudaStreamWaitEvent(c->aux[0], c->fork, 0);
+      rec(1, c->aux[0]);
       gemm_map_kernel<<<L.ngemm, 256, GEMM_SMEM, c->aux[0]>>>(c->gitems.p + L.gemm_off, c->gtasks.p, P);
+      rec(2, c->aux[0]);
       cudaEventRecord(c->join[0], c->aux[0]);
     }
     if (br[1]) {
       cudaStreamWaitEvent(c->aux[1], c->fork, 0);
+      rec(3, c->aux[1]);
       if (L.npanel)
         panel_kernel<<<L.npanel, 256, L.panel_smem, c->aux[1]>>>(c->ditems.p + L.panel_off, P, pivot_tol,
                                                                  static_eps);
       if (exact && L.nexact)
         panel_kernel<<<L.nexact, 512, L.exact_smem, c->aux[1]>>>(c->ditems.p + L.exact_off, P, pivot_tol,
                                                                  static_eps);
+      rec(4, c->aux[1]);
       cudaEventRecord(c->join[1], c->aux[1]);
     }
     if (br[2]) {
       cudaStream_t s2 = c->aux[2];
       cudaStreamWaitEvent(s2, c->fork, 0);
+      rec(5, s2);
       getrf_colmax_kernel<<<L.ntcol, 256, 0, s2>>>(c->titems.p + L.tcol_off, P);
       for (int k = 0; k < L.nsub; ++k) {
         const SubStep& S = c->subs[L.sub_off + k];
@@ -755,16 +774,19 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
         if (S.ngemm) tile_gemm_kernel<<<S.ngemm, 128, TGEMM_SMEM, s2>>>(c->titems.p + S.gemm_off, P);
       }
       getrf_finalize_kernel<<<L.ntfin, 256, 0, s2>>>(c->titems.p + L.tfin_off, P, pivot_tol);
+      rec(6, s2);
       cudaEventRecord(c->join[2], s2);
     }
     if (L.nitems) {
       const size_t smem = static_cast<size_t>(L.warps) * L.acc_len * sizeof(double);
+      rec(7, s0);
       level_kernel<<<L.nitems, L.warps * 32, smem, s0>>>(c->items.p + L.item_off, P, L.acc_len, pivot_tol,
                                                          static_eps);
+      rec(8, s0);
     }
     for (int k = 0; k < NBRANCH; ++k)
       if (br[k]) cudaStreamWaitEvent(s0, c->join[k], 0);
-    if (evs) cudaEventRecordWithFlags((*evs)[l + 1], s0, cudaEventRecordExternal);
+    rec(0, s0);
   }
   gather_kernel<<<148 * 8, 256, 0, s0>>>(c->vals.p, c->map.p, c->vout.p, c->nnz);
 }
@@ -861,6 +883,18 @@ int lbk_download(lbk_ctx* c, double* lu_values, int32_t* perms, lbk_status* st) 
   return 0;
 }
 
+// Working-layout values (every block's tile / CSC in pool block order).  In
+// dense-scratch mode every block is a full column-major tile, so the caller
+// can rebuild blocks whose support moved under row swaps (factorize.py:370-381).
+int lbk_download_work(lbk_ctx* c, double* work, int64_t* nwork, lbk_status* st) {
+  LBK_CUDA(cudaSetDevice(c->device), st);
+  if (nwork) *nwork = c->nnz_work;
+  if (work)
+    LBK_CUDA(cudaMemcpy(work, c->vals.p, c->nnz_work * sizeof(double), cudaMemcpyDeviceToHost), st);
+  ok(st);
+  return 0;
+}
+
 int lbk_set_perms(lbk_ctx* c, const int32_t* perms, lbk_status* st) {
   LBK_CUDA(cudaSetDevice(c->device), st);
   if (c->ndiag_rows)
@@ -880,11 +914,12 @@ void lbk_host_free(void* ptr) {
 }
 
 // Per-level device times: one instrumented replay (external event record
-// nodes between the levels); out_ms[nlevels].
+// nodes around every level and every kernel family of the level);
+// out_ms[nlevels x 5] = level, DMMA SSSSM, panel solves, tiled GETRF, CSC kernel.
 int lbk_level_times(lbk_ctx* c, double pivot_tol, double static_eps, float* out_ms, lbk_status* st) {
   LBK_CUDA(cudaSetDevice(c->device), st);
   const size_t nl = c->levels.size();
-  std::vector<cudaEvent_t> ev(nl + 1);
+  std::vector<cudaEvent_t> ev(1 + nl * 9);
   for (auto& e : ev) LBK_CUDA(cudaEventCreate(&e), st);
   cudaGraph_t g;
   cudaGraphExec_t ge = nullptr;
@@ -896,8 +931,19 @@ int lbk_level_times(lbk_ctx* c, double pivot_tol, double static_eps, float* out_
   if (e != cudaSuccess) return cuda_fail(st, e, "instrumented graph");
   e = cudaGraphLaunch(ge, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  const bool exact = (c->flags & 2) != 0 || !std::isnan(static_eps);
   if (e == cudaSuccess)
-    for (size_t l = 0; l < nl; ++l) cudaEventElapsedTime(&out_ms[l], ev[l], ev[l + 1]);
+    for (size_t l = 0; l < nl; ++l) {
+      const Level& L = c->levels[l];
+      const size_t b = 1 + l * 9, prev = l ? 1 + (l - 1) * 9 : 0;
+      float* o = out_ms + l * 5;
+      for (int k = 0; k < 5; ++k) o[k] = 0.f;
+      cudaEventElapsedTime(&o[0], ev[prev], ev[b]);
+      if (L.ngemm) cudaEventElapsedTime(&o[1], ev[b + 1], ev[b + 2]);
+      if (L.npanel || (exact && L.nexact)) cudaEventElapsedTime(&o[2], ev[b + 3], ev[b + 4]);
+      if (!exact && L.ntcol) cudaEventElapsedTime(&o[3], ev[b + 5], ev[b + 6]);
+      if (L.nitems) cudaEventElapsedTime(&o[4], ev[b + 7], ev[b + 8]);
+    }
   cudaGraphExecDestroy(ge);
   for (auto& x : ev) cudaEventDestroy(x);
   if (e != cudaSuccess) return cuda_fail(st, e, "instrumented replay");
@@ -914,6 +960,11 @@ int lbk_plan_levels(lbk_ctx* c, int64_t* levels, int32_t* items) {
     levels[3 * nl + l] = c->levels[l].npanel;
   }
   (void)items;
+  return 0;
+}
+
+int lbk_task_routes(lbk_ctx* c, int8_t* route) {
+  if (!c->route.empty()) std::memcpy(route, c->route.data(), c->route.size());
   return 0;
 }
 

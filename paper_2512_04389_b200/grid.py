@@ -137,27 +137,23 @@ def partition(f: FilledPattern, a: CscMatrix, plan: BlockingPlan) -> BlockGrid:
     pos = np.ascontiguousarray(plan.positions, dtype=np.int64)
     p = plan.p
     lib = _native.host_lib()
-    h = C.c_void_p()
     nb = C.c_int64()
     cpl = C.c_int64()
     P = _native.ptr
     i64 = _native.c_i64p
-    rc = lib.lbk_partition_run(n, P(fcp, i64), P(fri, i64), P(acp, i64), P(ari, i64),
-                               P(av, _native.c_f64p), p, P(pos, i64), C.byref(h), C.byref(nb),
-                               C.byref(cpl))
+    rc = lib.lbk_partition_count(n, P(fcp, i64), P(fri, i64), p, P(pos, i64), C.byref(nb), C.byref(cpl))
     _native.check_host(rc, "partition")
-    try:
-        nblocks = nb.value
-        table = np.empty((7, nblocks), np.int64)
-        col_ptr = np.empty(cpl.value, np.int64)
-        nnzf = int(fcp[-1])
-        row_idx = np.empty(nnzf, np.int64)
-        values = np.empty(nnzf, np.float64)
-        block_nnz = np.empty((p, p), np.int64)
-        lib.lbk_partition_fetch(h, P(table, i64), P(col_ptr, i64), P(row_idx, i64),
+    nblocks = nb.value
+    table = np.empty((7, nblocks), np.int64)
+    col_ptr = np.empty(cpl.value, np.int64)
+    nnzf = int(fcp[-1])
+    row_idx = np.empty(nnzf, np.int64)
+    values = np.empty(nnzf, np.float64)
+    block_nnz = np.empty((p, p), np.int64)
+    rc = lib.lbk_partition_fill(n, P(fcp, i64), P(fri, i64), P(acp, i64), P(ari, i64), P(av, _native.c_f64p),
+                                p, P(pos, i64), nblocks, P(table, i64), P(col_ptr, i64), P(row_idx, i64),
                                 P(values, _native.c_f64p), P(block_nnz, i64))
-    finally:
-        lib.lbk_partition_free(h)
+    _native.check_host(rc, "partition")
     pool = GridPool(table=table, col_ptr=col_ptr, row_idx=row_idx, values=values)
     blocks = {}
     for b in range(nblocks):

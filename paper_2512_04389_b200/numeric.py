@@ -67,9 +67,20 @@ def _dev():
     d(lib, "lbk_host_free", None, [vp])
     d(lib, "lbk_plan_info", C.c_int, [vp, i64p])
     d(lib, "lbk_level_times", C.c_int, [vp, C.c_double, C.c_double, C.POINTER(C.c_float), st])
+    d(lib, "lbk_fp64_peak", C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)])
+    d(lib, "lbk_task_routes", C.c_int, [vp, i8p])
+    d(lib, "lbk_download_work", C.c_int, [vp, f64p, i64p, st])
     d(lib, "lbk_plan_levels", C.c_int, [vp, i64p, i32p])
     _native._dev = lib
     return lib
+
+
+def fp64_peak(device: int = 0) -> tuple[float, float]:
+    """Measured FP64 tensor (DMMA) and DFMA TFLOP/s of this device (csrc/lbk_peak.cu)."""
+    a, b = C.c_double(), C.c_double()
+    if _dev().lbk_fp64_peak(device, C.byref(a), C.byref(b)):
+        raise DeviceError("lbk_fp64_peak failed")
+    return a.value, b.value
 
 
 def pinned_empty(nbytes_or_count, dtype=np.float64):
@@ -212,15 +223,32 @@ class Engine:
         return st
 
     def level_times(self, pivot_tol=DEFAULT_PIVOT_TOL, static_pivot=None) -> np.ndarray:
-        """Device ms of every launched level from one instrumented replay."""
+        """[levels x 5] device ms from one instrumented replay: level, DMMA SSSSM,
+        panel solves, tiled GETRF, CSC kernel."""
         if not self._resident:
             self.upload()
-        out = np.zeros(self.n_launch_levels, np.float32)
+        out = np.zeros((self.n_launch_levels, 5), np.float32)
         st = _native.LbkStatus()
         self.lib.lbk_level_times(self.ctx, pivot_tol, self._eps(static_pivot, self.grid.value_max),
                                  out.ctypes.data_as(C.POINTER(C.c_float)), C.byref(st))
         _native.raise_status(st, "lbk_level_times")
         return out
+
+    def download_work(self) -> np.ndarray:
+        """Working-layout values (dense-scratch mode: full tiles in pool block order)."""
+        n = C.c_int64()
+        st = _native.LbkStatus()
+        self.lib.lbk_download_work(self.ctx, None, C.byref(n), C.byref(st))
+        out = np.empty(n.value, np.float64)
+        if self.lib.lbk_download_work(self.ctx, P(out, f64p), C.byref(n), C.byref(st)):
+            _native.raise_status(st, "lbk_download_work")
+        return out
+
+    def task_routes(self) -> np.ndarray:
+        """Kernel family per task: -1 skipped, 0 CSC, 1 DMMA SSSSM, 2 panel, 3 tiled GETRF."""
+        r = np.zeros(self.tree.task_count, np.int8)
+        self.lib.lbk_task_routes(self.ctx, P(r, i8p))
+        return r
 
     def plan_levels(self):
         """(levels[4, L], items[6, T]) of the launched schedule."""
@@ -339,6 +367,36 @@ def build_factors(grid, pool: GridPool, values: np.ndarray, perms_pool: np.ndarr
     return LUFactors(n=grid.n, plan=grid.plan, l_blocks=lb, u_blocks=ub, perms=perms)
 
 
+def _block_from_tile(d: np.ndarray) -> SparseBlock:
+    """Dense tile -> CSC dropping exact zeros (factorize.py:179-192)."""
+    cols, rows = np.nonzero(d.T)
+    cp = np.zeros(d.shape[1] + 1, np.int64)
+    np.cumsum(np.bincount(cols, minlength=d.shape[1]), out=cp[1:])
+    return SparseBlock(d.shape[0], d.shape[1], cp, rows.astype(np.int64), d.T[cols, rows])
+
+
+def build_factors_full(grid, pool: GridPool, work: np.ndarray, perms_pool: np.ndarray) -> LUFactors:
+    """LUFactors from dense-scratch mode (every block a full tile in pool block
+    order): supports that moved under row swaps are rebuilt like the reference."""
+    t = pool.table
+    lb, ub = {}, {}
+    off = 0
+    for b in range(pool.nblocks):
+        bi, bj, nr, nc = (int(x) for x in t[:4, b])
+        d = work[off:off + nr * nc].reshape(nc, nr).T
+        off += nr * nc
+        if bi > bj:
+            lb[(bi, bj)] = _block_from_tile(d)
+        elif bi < bj:
+            ub[(bi, bj)] = _block_from_tile(d)
+        else:
+            lb[(bi, bi)] = _block_from_tile(np.tril(d, -1) + np.eye(nr))
+            ub[(bi, bi)] = _block_from_tile(np.triu(d))
+    f = build_factors(grid, GridPool(table=t[:, :0], col_ptr=pool.col_ptr, row_idx=pool.row_idx,
+                                     values=pool.values), pool.values[:0], perms_pool)
+    return LUFactors(n=grid.n, plan=grid.plan, l_blocks=lb, u_blocks=ub, perms=f.perms)
+
+
 def engine_for(grid, tree, *, device: int = 0, dense: bool = False, chunk: int = DEFAULT_CHUNK,
                dense_threshold: float | None = DEFAULT_DENSE_THRESHOLD) -> Engine:
     """Cached device plan of (grid, tree); dense=True uses full-rectangle blocks everywhere."""
@@ -380,6 +438,8 @@ def factorize(grid, tree, workers: int = 1, pivot_tol: float = DEFAULT_PIVOT_TOL
         if st.code == _native.LBK_ERR_PIVOT_SWAP and not dense:
             continue
         _native.raise_status(st, "factorize")
+        if dense:
+            return build_factors_full(grid, eng.pool, eng.download_work(), perms[: eng.n_diag_rows])
         return build_factors(grid, eng.pool, out, perms[: eng.n_diag_rows])
     raise DeviceError("unreachable")  # pragma: no cover
 

@@ -76,19 +76,16 @@ def symbolic_factorize(a_sym: CscMatrix, *, validate: bool = True) -> FilledPatt
     if validate:
         require_symmetric_full_diag(cp, ri, n)
     lib = _native.host_lib()
-    h = C.c_void_p()
     nnz = C.c_int64()
-    rc = lib.lbk_symbolic_run(n, _native.ptr(cp, _native.c_i64p), _native.ptr(ri, _native.c_i64p),
-                              C.byref(h), C.byref(nnz))
-    _native.check_host(rc, "symbolic_factorize")
-    try:
-        out_cp = np.empty(n + 1, np.int64)
-        out_ri = np.empty(nnz.value, np.int64)
-        lib.lbk_symbolic_fetch(h, _native.ptr(out_cp, _native.c_i64p),
-                               _native.ptr(out_ri, _native.c_i64p), None)
-    finally:
-        lib.lbk_symbolic_free(h)
-    return FilledPattern(n=n, col_ptr=out_cp, row_idx=out_ri)
+    P, i64 = _native.ptr, _native.c_i64p
+    _native.check_host(lib.lbk_symbolic_nnz(n, P(cp, i64), P(ri, i64), C.byref(nnz)), "symbolic_factorize")
+    out_cp = np.empty(n + 1, np.int64)
+    out_ri = np.empty(nnz.value, np.int64)
+    _native.check_host(lib.lbk_symbolic_fill(n, P(cp, i64), P(ri, i64), P(out_cp, i64), P(out_ri, i64), None),
+                       "symbolic_factorize")
+    f = FilledPattern(n=n, col_ptr=out_cp, row_idx=out_ri)
+    f._verified = True  # symmetric with a full diagonal by construction
+    return f
 
 
 def fill_ratio(a: CscMatrix, f: FilledPattern) -> float:
