@@ -628,29 +628,52 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       }
       L.ntcol = static_cast<int32_t>(tall.size() - L.tcol_off);
       L.sub_off = static_cast<int64_t>(c->subs.size());
+      // tile occupancy of each diagonal block from its filled pattern: the
+      // block's own LU fills only inside the (elimination-closed) pattern, so
+      // structurally zero tiles never need a TRSM or a trailing update
+      std::vector<std::vector<char>> occ(tgetrf[lv].size());
+      for (size_t q = 0; q < tgetrf[lv].size(); ++q) {
+        const int64_t b = tgetrf[lv][q];
+        const int m = hb[b].nrows, nt = (m + TS - 1) / TS;
+        occ[q].assign(static_cast<size_t>(nt) * nt, all_full ? 1 : 0);
+        if (all_full) continue;
+        const int64_t* scp = colptr + T_cp[b];
+        const int64_t* sri = rowidx + T_ent[b];
+        for (int col = 0; col < m; ++col)
+          for (int64_t e = scp[col]; e < scp[col + 1]; ++e) occ[q][(col / TS) * nt + sri[e] / TS] = 1;
+      }
       for (int kb = 0; kb < maxm; kb += TS) {
         SubStep s{};
+        const int tk = kb / TS;
         s.getrf_off = static_cast<int64_t>(tall.size());
         for (int64_t b : tgetrf[lv])
           if (kb < hb[b].nrows) tall.push_back(TileItem{static_cast<int32_t>(b), static_cast<int32_t>(T_bi[b]), kb, 0, 0, 0});
         s.ngetrf = static_cast<int32_t>(tall.size() - s.getrf_off);
         s.trsm_off = static_cast<int64_t>(tall.size());
-        for (int64_t b : tgetrf[lv]) {
-          const int m = hb[b].nrows;
+        for (size_t q = 0; q < tgetrf[lv].size(); ++q) {
+          const int64_t b = tgetrf[lv][q];
+          const int m = hb[b].nrows, nt = (m + TS - 1) / TS;
           if (kb >= m) continue;
           for (int o = kb + TS; o < m; o += TS) {
-            tall.push_back(TileItem{static_cast<int32_t>(b), static_cast<int32_t>(T_bi[b]), kb, o, 0, 0});
-            tall.push_back(TileItem{static_cast<int32_t>(b), static_cast<int32_t>(T_bi[b]), kb, 0, o, 1});
+            const int to = o / TS;
+            if (occ[q][tk * nt + to])  // L tile (o, kb): column tk, row to
+              tall.push_back(TileItem{static_cast<int32_t>(b), static_cast<int32_t>(T_bi[b]), kb, o, 0, 0});
+            if (occ[q][to * nt + tk])  // U tile (kb, o): column to, row tk
+              tall.push_back(TileItem{static_cast<int32_t>(b), static_cast<int32_t>(T_bi[b]), kb, 0, o, 1});
           }
         }
         s.ntrsm = static_cast<int32_t>(tall.size() - s.trsm_off);
         s.gemm_off = static_cast<int64_t>(tall.size());
-        for (int64_t b : tgetrf[lv]) {
-          const int m = hb[b].nrows;
+        for (size_t q = 0; q < tgetrf[lv].size(); ++q) {
+          const int64_t b = tgetrf[lv][q];
+          const int m = hb[b].nrows, nt = (m + TS - 1) / TS;
           if (kb >= m) continue;
-          for (int c0 = kb + TS; c0 < m; c0 += TS)
+          for (int c0 = kb + TS; c0 < m; c0 += TS) {
+            if (!occ[q][(c0 / TS) * nt + tk]) continue;  // U tile (kb, c0) empty
             for (int r0 = kb + TS; r0 < m; r0 += TS)
-              tall.push_back(TileItem{static_cast<int32_t>(b), static_cast<int32_t>(T_bi[b]), kb, r0, c0, 0});
+              if (occ[q][tk * nt + r0 / TS])  // L tile (r0, kb)
+                tall.push_back(TileItem{static_cast<int32_t>(b), static_cast<int32_t>(T_bi[b]), kb, r0, c0, 0});
+          }
         }
         s.ngemm = static_cast<int32_t>(tall.size() - s.gemm_off);
         c->subs.push_back(s);
