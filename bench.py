@@ -251,6 +251,11 @@ def main():
     fam_names = {1: "gemm_map_kernel (DMMA SSSSM)", 2: "panel_kernel (DMMA GESSM/TSTRF)",
                  3: "tiled GETRF (tile_getrf/trsm/gemm)", 0: "level_kernel (CSC SSSSM/GESSM/TSTRF)"}
     fam_col = {1: 1, 2: 2, 3: 3, 0: 4}
+    if float(lvl[:, 2].sum()) == 0.0 and (routes == 2).any():
+        # persistent executor: panel solves run inside the same tile-DAG launch as GETRF
+        fam_names[3] = "exec_kernel (tile-DAG: GETRF + GESSM/TSTRF panels)"
+        del fam_col[2]
+        routes = np.where(routes == 2, 3, routes)
     fams = {}
     for r, col in fam_col.items():
         sel = routes == r

@@ -26,7 +26,11 @@
 #include "../../include/lbk.h"
 #include "lbk_common.cuh"
 #include "lbk_dense.cuh"
+#include "lbk_exec.cuh"
 #include "lbk_sparse.cuh"
+
+#include <array>
+#include <cstdlib>
 
 using namespace lbk;
 
@@ -77,9 +81,61 @@ struct Level {
   int32_t nsub;
   int64_t tfin_off;   // finalize items
   int32_t ntfin;
+  int64_t exec_off, sptr_off, succ_off;  // persistent tile-DAG executor (tiled mode)
+  int32_t nexec;
 };
 
 constexpr int NBRANCH = 3;
+
+// Builds one level's tile-DAG for the persistent executor: tasks get a
+// priority key (elimination sub-step first); flush() orders them by key
+// (topological within every DAG) and emits counters and successor lists.
+struct ExecBuilder {
+  std::vector<XTask> t;
+  std::vector<int64_t> key;
+  std::vector<std::vector<int>> preds;
+  int add(int type, int64_t a, int64_t d, int r, int c, int k, int32_t step, int64_t prio, std::vector<int> deps) {
+    XTask x{};
+    x.type = static_cast<int8_t>(type);
+    x.r = static_cast<int16_t>(r);
+    x.c = static_cast<int16_t>(c);
+    x.k = static_cast<int16_t>(k);
+    x.a = static_cast<int32_t>(a);
+    x.d = static_cast<int32_t>(d);
+    x.step = step;
+    t.push_back(x);
+    key.push_back(prio);
+    std::sort(deps.begin(), deps.end());
+    deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
+    if (!deps.empty() && deps.front() < 0) deps.erase(deps.begin());
+    preds.push_back(std::move(deps));
+    return static_cast<int>(t.size()) - 1;
+  }
+  void flush(Level* L, std::vector<XTask>* tasks, std::vector<int32_t>* sptr, std::vector<int32_t>* succ,
+             std::vector<int32_t>* deps0) {
+    const int n = static_cast<int>(t.size());
+    std::vector<int> order(n), pos(n);
+    for (int i = 0; i < n; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return key[x] < key[y]; });
+    for (int i = 0; i < n; ++i) pos[order[i]] = i;
+    std::vector<std::vector<int>> out(n);
+    for (int i = 0; i < n; ++i)
+      for (int p : preds[i]) out[pos[p]].push_back(pos[i]);
+    L->exec_off = static_cast<int64_t>(tasks->size());
+    L->nexec = n;
+    L->sptr_off = static_cast<int64_t>(sptr->size());
+    L->succ_off = static_cast<int64_t>(succ->size());
+    int32_t acc = 0;
+    for (int i = 0; i < n; ++i) {
+      tasks->push_back(t[order[i]]);
+      deps0->push_back(static_cast<int32_t>(preds[order[i]].size()));
+      sptr->push_back(acc);
+      for (int s2 : out[i]) succ->push_back(s2);
+      acc += static_cast<int32_t>(out[i].size());
+    }
+    sptr->push_back(acc);
+  }
+};
 
 }  // namespace
 
@@ -112,6 +168,11 @@ struct lbk_ctx {
   DevBuf<GemmItem> gitems;
   DevBuf<DenseItem> ditems;
   DevBuf<TileItem> titems;
+  DevBuf<XTask> xtasks;
+  DevBuf<int32_t> xsptr, xsucc, xdeps0;
+  DevBuf<int> xdeps, xheads;
+  int64_t n_exec = 0;
+  bool use_exec = true;
 };
 
 namespace {
@@ -206,6 +267,8 @@ int lbk_create(lbk_ctx** out, int device, lbk_status* st) {
     e = cudaFuncSetAttribute(tile_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TRSM_SMEM);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(tile_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TGEMM_SMEM);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, EXEC_SMEM);
+  c->use_exec = std::getenv("LBK_NO_EXEC") == nullptr;
   for (int k = 0; k < NBRANCH && e == cudaSuccess; ++k) {
     e = cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->join[k], cudaEventDisableTiming);
@@ -449,6 +512,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     std::vector<GemmTask> gtasks;
     std::vector<int32_t> hmaps;
     std::vector<std::vector<DenseItem>> pan(nlevels), exa(nlevels);
+    std::vector<std::vector<std::array<int32_t, 4>>> ptask(nlevels);  // (kind, diag blk, panel blk, step)
     std::vector<int32_t> pan_smem(nlevels, 0), exa_smem(nlevels, 0);
     std::vector<std::vector<int64_t>> tgetrf(nlevels);  // FULL diagonal blocks factored by the tiled GETRF
     c->route.assign(ntasks, -1);
@@ -496,6 +560,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           c->route[t] = 2;
           for (int32_t s = 0; s < hb[x].nC; s += STRIP)
             pan[lv].push_back(DenseItem{1, it.a, it.b, it.c, s, static_cast<int32_t>(i)});
+          ptask[lv].push_back({1, it.a, it.b, static_cast<int32_t>(i)});
           pan_smem[lv] = std::max(pan_smem[lv], (hb[x].nR + 64) * 8);
           continue;
         }
@@ -510,6 +575,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           c->route[t] = 2;
           for (int32_t s = 0; s < hb[x].nR; s += STRIP)
             pan[lv].push_back(DenseItem{2, it.a, it.b, 0, s, static_cast<int32_t>(i)});
+          ptask[lv].push_back({2, it.a, it.b, static_cast<int32_t>(i)});
           pan_smem[lv] = std::max(pan_smem[lv], 64 * 8);
           continue;
         }
@@ -589,6 +655,8 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     std::vector<GemmItem> mall;
     std::vector<DenseItem> dall;
     std::vector<TileItem> tall;
+    std::vector<XTask> xtasks;
+    std::vector<int32_t> xsucc_ptr, xsucc, xdeps0;
     c->levels.clear();
     c->subs.clear();
     for (int32_t lv = 0; lv < nlevels; ++lv) {
@@ -684,12 +752,76 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         for (int c0 = 0; c0 < hb[b].nrows; c0 += 256)
           tall.push_back(TileItem{static_cast<int32_t>(b), static_cast<int32_t>(T_bi[b]), 0, 0, c0, 0});
       L.ntfin = static_cast<int32_t>(tall.size() - L.tfin_off);
+      // ---- persistent tile-DAG executor work of this level (tiled mode) ----
+      {
+        ExecBuilder X;
+        for (size_t q = 0; q < tgetrf[lv].size(); ++q) {
+          const int64_t b = tgetrf[lv][q];
+          const int m = hb[b].nrows, nt = (m + XT - 1) / XT;
+          const int32_t stp = static_cast<int32_t>(T_bi[b]);
+          const int col = X.add(X_COLMAX, static_cast<int32_t>(b), static_cast<int32_t>(b), 0, 0, 0, stp, -1, {});
+          std::vector<int> last(static_cast<size_t>(nt) * nt, col), lt(nt, -1), ut(nt, -1), fin_deps;
+          auto L_ = [&](int r, int cc) -> int& { return last[static_cast<size_t>(cc) * nt + r]; };
+          for (int kb = 0; kb < nt; ++kb) {
+            const int g = X.add(X_GETRF, b, b, kb, kb, kb, stp, kb * 4, {L_(kb, kb)});
+            L_(kb, kb) = g;
+            fin_deps.push_back(g);
+            for (int r = kb + 1; r < nt; ++r) {
+              lt[r] = -1;
+              if (!occ[q][static_cast<size_t>(kb) * nt + r]) continue;
+              lt[r] = X.add(X_TRSM_L, b, b, r, kb, kb, stp, kb * 4 + 1, {g, L_(r, kb)});
+              L_(r, kb) = lt[r];
+              fin_deps.push_back(lt[r]);
+            }
+            for (int cc = kb + 1; cc < nt; ++cc) {
+              ut[cc] = -1;
+              if (!occ[q][static_cast<size_t>(cc) * nt + kb]) continue;
+              ut[cc] = X.add(X_TRSM_U, b, b, kb, cc, kb, stp, kb * 4 + 1, {g, L_(kb, cc)});
+              L_(kb, cc) = ut[cc];
+            }
+            for (int cc = kb + 1; cc < nt; ++cc) {
+              if (ut[cc] < 0) continue;
+              for (int r = kb + 1; r < nt; ++r) {
+                if (lt[r] < 0) continue;
+                const int t2 = X.add(X_GEMM, b, b, r, cc, kb, stp, kb * 4 + 2, {lt[r], ut[cc], L_(r, cc)});
+                L_(r, cc) = t2;
+              }
+            }
+          }
+          X.add(X_FINAL, b, b, 0, 0, 0, stp, 1 << 30, fin_deps);
+        }
+        for (const auto& pt : ptask[lv]) {
+          const int32_t dblk = pt[1], xb = pt[2], stp = pt[3];
+          const int tr = (hb[xb].nR + XT - 1) / XT, tc = (hb[xb].nC + XT - 1) / XT;
+          std::vector<int> last(static_cast<size_t>(tr) * tc, -1);
+          auto L_ = [&](int r, int cc) -> int& { return last[static_cast<size_t>(cc) * tr + r]; };
+          if (pt[0] == 1) {  // GESSM: forward substitution down the row blocks
+            for (int kb = 0; kb < tr; ++kb)
+              for (int cc = 0; cc < tc; ++cc) {
+                const int d = X.add(X_PG_DIAG, xb, dblk, kb, cc, kb, stp, kb * 4 + 1, {L_(kb, cc)});
+                L_(kb, cc) = d;
+                for (int r = kb + 1; r < tr; ++r)
+                  L_(r, cc) = X.add(X_PG_UPD, xb, dblk, r, cc, kb, stp, kb * 4 + 2, {d, L_(r, cc)});
+              }
+          } else {  // TSTRF: substitution along the column blocks
+            for (int kb = 0; kb < tc; ++kb)
+              for (int r = 0; r < tr; ++r) {
+                const int d = X.add(X_PT_DIAG, xb, dblk, r, kb, kb, stp, kb * 4 + 1, {L_(r, kb)});
+                L_(r, kb) = d;
+                for (int cc = kb + 1; cc < tc; ++cc)
+                  L_(r, cc) = X.add(X_PT_UPD, xb, dblk, r, cc, kb, stp, kb * 4 + 2, {d, L_(r, cc)});
+              }
+          }
+        }
+        X.flush(&L, &xtasks, &xsucc_ptr, &xsucc, &xdeps0);
+      }
       c->levels.push_back(L);
     }
     c->n_generic = static_cast<int64_t>(gall.size());
     c->n_gemm = static_cast<int64_t>(mall.size());
     c->n_panel = static_cast<int64_t>(dall.size());
     c->n_tile = static_cast<int64_t>(tall.size());
+    c->n_exec = static_cast<int64_t>(xtasks.size());
     c->hblk = hb;
     LBK_CUDA(c->blk.upload(hb), st);
     LBK_CUDA(c->colptr.upload(hcp), st);
@@ -710,6 +842,12 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     LBK_CUDA(c->gitems.upload(mall), st);
     LBK_CUDA(c->ditems.upload(dall), st);
     LBK_CUDA(c->titems.upload(tall), st);
+    LBK_CUDA(c->xtasks.upload(xtasks), st);
+    LBK_CUDA(c->xsptr.upload(xsucc_ptr), st);
+    LBK_CUDA(c->xsucc.upload(xsucc), st);
+    LBK_CUDA(c->xdeps0.upload(xdeps0), st);
+    LBK_CUDA(c->xdeps.alloc(xdeps0.size()), st);
+    LBK_CUDA(c->xheads.alloc(c->levels.size()), st);
     LBK_CUDA(c->perm.alloc(ndiag), st);
     LBK_CUDA(c->colmax.alloc(ndiag), st);
     LBK_CUDA(c->bmax.alloc(ndiag), st);
@@ -756,11 +894,16 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
   cudaMemsetAsync(c->err.p, 0xff, 2 * sizeof(unsigned long long), s0);
   cudaMemsetAsync(c->vals.p, 0, c->nnz_work * sizeof(double), s0);
   scatter_kernel<<<148 * 8, 256, 0, s0>>>(c->vin.p, c->map.p, c->vals.p, c->nnz);
+  const bool use_exec = !exact && c->use_exec;
+  if (use_exec && c->n_exec) {
+    cudaMemcpyAsync(c->xdeps.p, c->xdeps0.p, c->n_exec * sizeof(int), cudaMemcpyDeviceToDevice, s0);
+    cudaMemsetAsync(c->xheads.p, 0, c->levels.size() * sizeof(int), s0);
+  }
   if (evs) cudaEventRecordWithFlags((*evs)[0], s0, cudaEventRecordExternal);
   for (size_t l = 0; l < c->levels.size(); ++l) {
     const Level& L = c->levels[l];
-    const bool has_t = !exact && L.ntcol > 0;
-    const bool br[NBRANCH] = {L.ngemm > 0, L.npanel > 0 || (exact && L.nexact > 0), has_t};
+    const bool has_t = !exact && (use_exec ? L.nexec > 0 : L.ntcol > 0);
+    const bool br[NBRANCH] = {L.ngemm > 0, (!use_exec && L.npanel > 0) || (exact && L.nexact > 0), has_t};
     // instrumented replays: per level [end, gemm b/e, panel b/e, getrf b/e, csc b/e]
     auto rec = [&](int k, cudaStream_t s) {
       if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 9 + k], s, cudaEventRecordExternal);
@@ -789,14 +932,26 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
       cudaStream_t s2 = c->aux[2];
       cudaStreamWaitEvent(s2, c->fork, 0);
       rec(5, s2);
-      getrf_colmax_kernel<<<L.ntcol, 256, 0, s2>>>(c->titems.p + L.tcol_off, P);
-      for (int k = 0; k < L.nsub; ++k) {
-        const SubStep& S = c->subs[L.sub_off + k];
-        if (S.ngetrf) tile_getrf_kernel<<<S.ngetrf, 256, 0, s2>>>(c->titems.p + S.getrf_off, P);
-        if (S.ntrsm) tile_trsm_kernel<<<S.ntrsm, 128, TRSM_SMEM, s2>>>(c->titems.p + S.trsm_off, P);
-        if (S.ngemm) tile_gemm_kernel<<<S.ngemm, 128, TGEMM_SMEM, s2>>>(c->titems.p + S.gemm_off, P);
+      if (use_exec) {
+        XLevel X;
+        X.tasks = c->xtasks.p + L.exec_off;
+        X.succ_ptr = c->xsptr.p + L.sptr_off;
+        X.succ = c->xsucc.p + L.succ_off;
+        X.deps = c->xdeps.p + L.exec_off;
+        X.head = c->xheads.p + l;
+        X.ntasks = L.nexec;
+        const int grid = std::max(1, std::min(L.nexec, 148 * 2));
+        exec_kernel<<<grid, 256, EXEC_SMEM, s2>>>(X, P, pivot_tol);
+      } else {
+        getrf_colmax_kernel<<<L.ntcol, 256, 0, s2>>>(c->titems.p + L.tcol_off, P);
+        for (int k = 0; k < L.nsub; ++k) {
+          const SubStep& S = c->subs[L.sub_off + k];
+          if (S.ngetrf) tile_getrf_kernel<<<S.ngetrf, 256, 0, s2>>>(c->titems.p + S.getrf_off, P);
+          if (S.ntrsm) tile_trsm_kernel<<<S.ntrsm, 128, TRSM_SMEM, s2>>>(c->titems.p + S.trsm_off, P);
+          if (S.ngemm) tile_gemm_kernel<<<S.ngemm, 128, TGEMM_SMEM, s2>>>(c->titems.p + S.gemm_off, P);
+        }
+        getrf_finalize_kernel<<<L.ntfin, 256, 0, s2>>>(c->titems.p + L.tfin_off, P, pivot_tol);
       }
-      getrf_finalize_kernel<<<L.ntfin, 256, 0, s2>>>(c->titems.p + L.tfin_off, P, pivot_tol);
       rec(6, s2);
       cudaEventRecord(c->join[2], s2);
     }
@@ -1004,7 +1159,12 @@ int lbk_plan_info(lbk_ctx* c, int64_t* info) {
   info[5] = c->n_panel;
   int64_t launches = 2;  // scatter + gather
   for (const Level& L : c->levels) {
-    launches += (L.nitems > 0) + (L.ngemm > 0) + (L.npanel > 0);
+    launches += (L.nitems > 0) + (L.ngemm > 0);
+    if (c->use_exec) {
+      launches += L.nexec > 0;
+      continue;
+    }
+    launches += L.npanel > 0;
     if (L.ntcol) {
       launches += 2;
       for (int k = 0; k < L.nsub; ++k) {

@@ -213,3 +213,23 @@ def test_c2_full_size_properties():
     x = M.solve(f, b)
     relres = float(np.linalg.norm(a.to_scipy() @ x - b) / np.linalg.norm(b))
     assert relres < 1e-12
+
+
+@pytest.mark.parametrize("kind,n,bs", [("dense", 300, 150), ("random_spd", 2400, 400), ("arrowhead", 1500, 500)])
+def test_large_blocks_tile_dag_vs_oracle(kind, n, bs):
+    """Diagonal blocks of several 64-tiles and compressed panels: tile-DAG executor
+    (tiled GETRF with verified no-swap speculation, panel solves, DMMA SSSSM)."""
+    kw = {"random_spd": {"bandwidth": 60, "density": 0.3}, "arrowhead": {"b": 200}}.get(kind, {})
+    a = generate(kind, n, **kw)
+    g, t = grid_tree(a, M.regular_plan(n, bs).positions)
+    f = M.factorize(g, t)
+    oa = OS.Csc(n, a.col_ptr, a.row_idx, a.values)
+    og = OS.partition(n, *OS.symbolic(OS.symmetrize(oa)), oa, g.plan.positions)
+    state, perms = ON.factorize(og, OS.levels(og))
+    lb, ub = ON.export(state)
+    amax = np.abs(a.values).max()
+    for blocks, ob in ((f.l_blocks, lb), (f.u_blocks, ub)):
+        assert set(blocks) == set(ob)
+        for k in ob:
+            assert np.array_equal(blocks[k].row_idx, ob[k].row_idx), k
+            np.testing.assert_allclose(blocks[k].values, ob[k].values, rtol=0, atol=1e-11 * amax)
