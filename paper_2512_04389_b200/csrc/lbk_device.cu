@@ -759,8 +759,14 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           const int64_t b = tgetrf[lv][q];
           const int m = hb[b].nrows, nt = (m + XT - 1) / XT;
           const int32_t stp = static_cast<int32_t>(T_bi[b]);
-          const int col = X.add(X_COLMAX, static_cast<int32_t>(b), static_cast<int32_t>(b), 0, 0, 0, stp, -1, {});
-          std::vector<int> last(static_cast<size_t>(nt) * nt, col), lt(nt, -1), ut(nt, -1), fin_deps;
+          // column maxima at GETRF entry, one task per column tile; every first
+          // write into column tile c waits for colmax(c)
+          std::vector<int> last(static_cast<size_t>(nt) * nt), lt(nt, -1), ut(nt, -1), fin_deps;
+          for (int cc = 0; cc < nt; ++cc) {
+            const int col = X.add(X_COLMAX, b, b, 0, cc, 0, stp, -1, {});
+            for (int r = 0; r < nt; ++r) last[static_cast<size_t>(cc) * nt + r] = col;
+            fin_deps.push_back(col);
+          }
           auto L_ = [&](int r, int cc) -> int& { return last[static_cast<size_t>(cc) * nt + r]; };
           for (int kb = 0; kb < nt; ++kb) {
             const int g = X.add(X_GETRF, b, b, kb, kb, kb, stp, kb * 4, {L_(kb, kb)});
@@ -979,9 +985,15 @@ int build_graph(lbk_ctx* c, double pivot_tol, double static_eps, lbk_status* st)
   }
   cudaGraph_t g;
   LBK_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), st);
+  (void)cudaGetLastError();
   capture_factorization(c, pivot_tol, static_eps, nullptr);
   cudaError_t e = cudaStreamEndCapture(c->stream, &g);
   if (e != cudaSuccess) return cuda_fail(st, e, "graph capture");
+  e = cudaGetLastError();  // a launch rejected during capture (bad configuration)
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(g);
+    return cuda_fail(st, e, "kernel launch during capture");
+  }
   e = cudaGraphInstantiate(&c->graph, g, 0);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return cuda_fail(st, e, "graph instantiate");

@@ -7,17 +7,22 @@
 // the floating-point order is fixed and results are deterministic).  One
 // launch per level runs all of them: each CTA pulls the next task index
 // (host order is topological), waits for its dependency counter to reach
-// zero, executes it, and decrements its successors' counters.  Tasks are
+// zero, executes it, and decrements its successors' counters.  A task is
 // only ever waited on after an earlier index was taken by a running CTA, so
 // progress is guaranteed without co-residency assumptions.
 //
-// Mutable tiles may have been written by other SMs during the launch: all
-// global reads of tile data use ld.global.cg (L2, bypassing the
+// Tile kernels keep the 64x64 target tile in registers: thread t owns rows
+// 4*(t%16)..+3 and columns 4*(t/16)..+3; one elimination step costs one or two
+// __syncthreads and <= 16 register FMAs per thread.  Updates are applied in
+// the reference's order with separately rounded mul/sub.
+//
+// Mutable tiles may have been written by other SMs during the launch: every
+// global read of tile data uses ld.global.cg (L2, bypassing the
 // non-coherent L1).
 //
 // GETRF speculates "no row swap" and verifies the reference's pivot rule
 // exactly (see lbk_dense.cuh): in-tile and below-tile |d_qc| before scaling
-// feed bmax[c]; FINALIZE compares them with |u_cc| and colmax[c].
+// feed bmax[c]; FINAL compares them with |u_cc| and colmax[c].
 
 #pragma once
 
@@ -27,13 +32,13 @@
 namespace lbk {
 
 constexpr int XT = 64;          // tile edge
-constexpr int XTP = XT + 1;     // padded smem column stride (64 doubles + 1)
+constexpr int XTP = XT + 1;     // padded smem column stride
 constexpr int XS = XT + 4;      // DMMA operand stride
 constexpr int XREG = XT * XS;   // one smem tile region (fits either stride)
-constexpr int EXEC_SMEM = (3 * XREG + XT) * 8;
+constexpr int EXEC_SMEM = (3 * XREG + 4 * XT) * 8;
 
 enum XType : int8_t {
-  X_COLMAX = 0,  // colmax / bmax / perm reset of diagonal block a
+  X_COLMAX = 0,  // colmax / bmax / perm reset of column tile c of diagonal block a
   X_GETRF = 1,   // factor diagonal tile (k,k) of block a
   X_TRSM_L = 2,  // tile (r,k) <- tile U_kk^{-1}
   X_TRSM_U = 3,  // tile (k,c) <- L_kk^{-1} tile
@@ -66,97 +71,216 @@ struct XLevel {
 
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
 
-// load a (nr x nc) tile from column-major global memory (leading dim ld) into
-// smem T[c*XTP + r]; zero padding outside; optional row/column gathers.
+// ---- register tiles: thread owns rows 4*ty+i, columns 4*tx+j ----------------
+struct Reg {
+  double a[4][4];
+};
+
+__device__ __forceinline__ int reg_ty() { return threadIdx.x & 15; }
+__device__ __forceinline__ int reg_tx() { return threadIdx.x >> 4; }
+
+__device__ __forceinline__ void reg_load(Reg& R, const double* G, int ld, int nr, int nc,
+                                         const int32_t* rg = nullptr, const int32_t* cg = nullptr) {
+  const int r0 = 4 * reg_ty(), c0 = 4 * reg_tx();
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = c0 + j;
+    const bool cv = c < nc;
+    const size_t co = cv ? static_cast<size_t>(cg ? cg[c] : c) * ld : 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = r0 + i;
+      R.a[i][j] = (cv && r < nr) ? ldcg(G + co + (rg ? rg[r] : r)) : 0.0;
+    }
+  }
+}
+
+__device__ __forceinline__ void reg_store(double* G, int ld, const Reg& R, int nr, int nc) {
+  const int r0 = 4 * reg_ty(), c0 = 4 * reg_tx();
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (r0 + i < nr && c0 + j < nc) G[static_cast<size_t>(c0 + j) * ld + r0 + i] = R.a[i][j];
+}
+
+// smem tile (XTP stride) -> registers / back
+__device__ __forceinline__ void reg_from_smem(Reg& R, const double* T) {
+  const int r0 = 4 * reg_ty(), c0 = 4 * reg_tx();
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) R.a[i][j] = T[(c0 + j) * XTP + r0 + i];
+}
+
+// max over the 16 threads of one column group (a half warp: tid = 16*tx + ty)
+__device__ __forceinline__ double halfwarp_max(double v) {
+  for (int o = 8; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// LU without row exchange of the n x n register tile; bmax[j] gets max |d_qj|
+// over rows q > j before scaling.  scratch: 4*XT doubles of smem.
+__device__ void reg_lu(Reg& R, int n, unsigned long long* bmax, double* scratch) {
+  const int ty = reg_ty(), tx = reg_tx();
+  double* urow = scratch;           // [2][XT]
+  double* lcol = scratch + 2 * XT;  // [2][XT]
+  for (int j = 0; j < n; ++j) {
+    const int b = (j & 1) * XT;
+    const int jb = j >> 2, jr = j & 3;
+    if (ty == jb) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (i == jr) urow[b + 4 * tx + q] = R.a[i][q];
+    }
+    __syncthreads();
+    const double u = urow[b + j];
+    double mx = 0.0;
+    if (tx == jb) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = 4 * ty + i;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q == jr && r > j && r < n) {
+            const double d = R.a[i][q];
+            mx = fmax(mx, fabs(d));
+            const double l = __ddiv_rn(d, u);
+            R.a[i][q] = l;
+            lcol[b + r] = l;
+          }
+      }
+    }
+    mx = halfwarp_max(mx);  // whole warp participates; only the owners' half is nonzero
+    if (tx == jb && ty == 0 && mx > 0.0) atomic_max_nonneg(&bmax[j], mx);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = 4 * ty + i;
+      if (r <= j || r >= n) continue;
+      const double l = lcol[b + r];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = 4 * tx + q;
+        if (c > j && c < n) R.a[i][q] = dsub_mul(R.a[i][q], l, urow[b + c]);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// X (register tile nr x nc) <- X U^{-1}, U upper (smem, XTP stride, diag included).
+// bmax != nullptr: record max |x_qj| before the division for every column j.
+__device__ void reg_right_upper(Reg& R, int nr, int nc, const double* U, unsigned long long* bmax,
+                                double* scratch) {
+  const int ty = reg_ty(), tx = reg_tx();
+  double* lcol = scratch;  // [2][XT]
+  for (int j = 0; j < nc; ++j) {
+    const int b = (j & 1) * XT;
+    const int jb = j >> 2, jr = j & 3;
+    double mx = 0.0;
+    if (tx == jb) {
+      const double u = U[j * XTP + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = 4 * ty + i;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q == jr && r < nr) {
+            const double d = R.a[i][q];
+            mx = fmax(mx, fabs(d));
+            const double x = __ddiv_rn(d, u);
+            R.a[i][q] = x;
+            lcol[b + r] = x;
+          }
+      }
+    }
+    if (bmax) {
+      mx = halfwarp_max(mx);
+      if (tx == jb && ty == 0 && mx > 0.0) atomic_max_nonneg(&bmax[j], mx);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = 4 * ty + i;
+      if (r >= nr) continue;
+      const double x = lcol[b + r];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = 4 * tx + q;
+        if (c > j && c < nc) R.a[i][q] = dsub_mul(R.a[i][q], x, U[c * XTP + j]);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// X (register tile nr x nc) <- L^{-1} X, L unit lower (smem, XTP stride).
+__device__ void reg_left_unit_lower(Reg& R, int nr, int nc, const double* L, double* scratch) {
+  const int ty = reg_ty(), tx = reg_tx();
+  double* xrow = scratch;  // [2][XT]
+  for (int k = 0; k < nr; ++k) {
+    const int b = (k & 1) * XT;
+    const int kb = k >> 2, kr = k & 3;
+    if (ty == kb) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (i == kr) xrow[b + 4 * tx + q] = R.a[i][q];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = 4 * ty + i;
+      if (r <= k || r >= nr) continue;
+      const double l = L[k * XTP + r];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c = 4 * tx + q;
+        if (c < nc) R.a[i][q] = dsub_mul(R.a[i][q], l, xrow[b + c]);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// ---- smem staging -------------------------------------------------------------
+// (nr x nc) tile, column-major global (ld), optional row/column gathers -> smem T[c*XTP + r]
 __device__ __forceinline__ void load_tile(double* T, const double* G, int ld, int nr, int nc,
                                           const int32_t* rg = nullptr, const int32_t* cg = nullptr) {
   for (int idx = threadIdx.x; idx < XT * XT; idx += blockDim.x) {
-    const int r = idx % XT, c = idx / XT;
+    const int r = idx & (XT - 1), c = idx >> 6;
     double v = 0.0;
-    if (r < nr && c < nc) {
-      const int gr = rg ? rg[r] : r, gc = cg ? cg[c] : c;
-      v = ldcg(G + static_cast<size_t>(gc) * ld + gr);
-    }
+    if (r < nr && c < nc) v = ldcg(G + static_cast<size_t>(cg ? cg[c] : c) * ld + (rg ? rg[r] : r));
     T[c * XTP + r] = v;
   }
 }
 
-__device__ __forceinline__ void store_tile(double* G, int ld, const double* T, int nr, int nc) {
+// DMMA A operand ([k][r], stride XS) / B operand ([c][k], stride XS)
+__device__ __forceinline__ void load_opA(double* As, const double* G, int ld, int nr, int nk,
+                                         const int32_t* rg = nullptr, const int32_t* kg = nullptr) {
   for (int idx = threadIdx.x; idx < XT * XT; idx += blockDim.x) {
-    const int r = idx % XT, c = idx / XT;
-    if (r < nr && c < nc) G[static_cast<size_t>(c) * ld + r] = T[c * XTP + r];
+    const int r = idx & (XT - 1), k = idx >> 6;
+    double v = 0.0;
+    if (r < nr && k < nk) v = ldcg(G + static_cast<size_t>(kg ? kg[k] : k) * ld + (rg ? rg[r] : r));
+    As[k * XS + r] = v;
   }
 }
 
-// Right-looking LU without row exchange of the tile in smem (n x n), 256
-// threads; records max |d_qc| over in-tile rows below the diagonal before
-// scaling into bmax (global, bits) for the block's columns c0 + j.
-__device__ void tile_lu(double* T, int n, unsigned long long* bmax) {
-  const int tid = threadIdx.x, lane = tid & 31;
-  for (int j = 0; j < n; ++j) {
-    const double u = T[j * XTP + j];
-    double mx = 0.0;
-    if (tid < 64) {
-      const int r = tid;
-      if (r > j && r < n) {
-        const double v = T[j * XTP + r];
-        mx = fabs(v);
-        T[j * XTP + r] = __ddiv_rn(v, u);
-      }
-      for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      if (lane == 0 && mx > 0.0) atomic_max_nonneg(&bmax[j], mx);
-    }
-    __syncthreads();
-    const int rows = n - j - 1;
-    for (int idx = tid; idx < rows * rows; idx += blockDim.x) {
-      const int r = j + 1 + idx % rows, c = j + 1 + idx / rows;
-      T[c * XTP + r] = dsub_mul(T[c * XTP + r], T[j * XTP + r], T[c * XTP + j]);
-    }
-    __syncthreads();
+__device__ __forceinline__ void load_opB(double* Bs, const double* G, int ld, int nk, int nc,
+                                         const int32_t* kg = nullptr, const int32_t* cg = nullptr) {
+  for (int idx = threadIdx.x; idx < XT * XT; idx += blockDim.x) {
+    const int k = idx & (XT - 1), c = idx >> 6;
+    double v = 0.0;
+    if (k < nk && c < nc) v = ldcg(G + static_cast<size_t>(cg ? cg[c] : c) * ld + (kg ? kg[k] : k));
+    Bs[c * XS + k] = v;
   }
 }
 
-// X (nr x nc, smem) <- X U^{-1}, U upper (nc x nc, smem, diag included).
-// If bmax != nullptr: record max |x_qj| before the division per column j.
-// Rows are independent: thread q owns row q (<= 64 rows); the column loop is
-// sequential, operands in smem.
-__device__ void tile_right_upper(double* X, int nr, int nc, const double* U, unsigned long long* bmax,
-                                 double* cmx) {
-  const int tid = threadIdx.x;
-  if (bmax)
-    for (int c = tid; c < XT; c += blockDim.x) cmx[c] = 0.0;
-  __syncthreads();
-  if (tid < nr) {
-    for (int j = 0; j < nc; ++j) {
-      const double d = X[j * XTP + tid];
-      if (bmax && d != 0.0)
-        atomicMax(reinterpret_cast<unsigned long long*>(&cmx[j]),
-                  static_cast<unsigned long long>(__double_as_longlong(fabs(d))));
-      const double x = __ddiv_rn(d, U[j * XTP + j]);
-      X[j * XTP + tid] = x;
-      for (int jj = j + 1; jj < nc; ++jj) X[jj * XTP + tid] = dsub_mul(X[jj * XTP + tid], x, U[jj * XTP + j]);
-    }
-  }
-  __syncthreads();
-  if (bmax)
-    for (int c = tid; c < nc; c += blockDim.x)
-      if (cmx[c] != 0.0) atomic_max_nonneg(&bmax[c], cmx[c]);
-}
-
-// X (nr x nc, smem) <- L^{-1} X, L unit lower (nr x nr, smem).  Thread c owns column c.
-__device__ void tile_left_unit_lower(double* X, int nr, int nc, const double* L) {
-  const int tid = threadIdx.x;
-  if (tid < nc) {
-    double* x = X + tid * XTP;
-    for (int k = 0; k < nr; ++k) {
-      const double xk = x[k];
-      for (int r = k + 1; r < nr; ++r) x[r] = dsub_mul(x[r], L[k * XTP + r], xk);
-    }
-  }
-  __syncthreads();
-}
-
-// C (smem, XTP stride) -= A (XS stride, [k][r]) * B (XS stride, [c][k]), 64x64x64, 8 warps of 32x16.
+// target tile (registers via smem T0) -= A * B on DMMA, 64x64x64, 8 warps of 32x16
 __device__ void tile_mma_sub(double* Cs, const double* As, const double* Bs) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
@@ -177,7 +301,6 @@ __device__ void tile_mma_sub(double* Cs, const double* As, const double* Bs) {
 #pragma unroll
       for (int j = 0; j < 2; ++j) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
   }
-  __syncthreads();
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -189,41 +312,28 @@ __device__ void tile_mma_sub(double* Cs, const double* As, const double* Bs) {
   __syncthreads();
 }
 
-// stage a tile as DMMA A operand ([k][r], stride XS) or B operand ([c][k], stride XS)
-__device__ __forceinline__ void load_opA(double* As, const double* G, int ld, int nr, int nk,
-                                         const int32_t* rg = nullptr, const int32_t* kg = nullptr) {
-  for (int idx = threadIdx.x; idx < XT * XT; idx += blockDim.x) {
-    const int r = idx % XT, k = idx / XT;
-    double v = 0.0;
-    if (r < nr && k < nk) v = ldcg(G + static_cast<size_t>(kg ? kg[k] : k) * ld + (rg ? rg[r] : r));
-    As[k * XS + r] = v;
-  }
-}
-
-__device__ __forceinline__ void load_opB(double* Bs, const double* G, int ld, int nk, int nc,
-                                         const int32_t* kg = nullptr, const int32_t* cg = nullptr) {
-  for (int idx = threadIdx.x; idx < XT * XT; idx += blockDim.x) {
-    const int k = idx % XT, c = idx / XT;
-    double v = 0.0;
-    if (k < nk && c < nc) v = ldcg(G + static_cast<size_t>(cg ? cg[c] : c) * ld + (kg ? kg[k] : k));
-    Bs[c * XS + k] = v;
-  }
-}
-
 __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double pivot_tol) {
-  double* T0 = sm;             // target tile (XTP stride)
-  double* T1 = sm + XREG;      // operand tile (XTP stride) / DMMA A (XS stride)
-  double* T2 = sm + 2 * XREG;  // DMMA B (XS stride)
-  double* cmx = sm + 3 * XREG; // per-column scratch
+  double* T0 = sm;                  // target tile (XTP stride)
+  double* T1 = sm + XREG;           // operand tile (XTP stride) / DMMA A (XS stride)
+  double* T2 = sm + 2 * XREG;       // DMMA B (XS stride)
+  double* scratch = sm + 3 * XREG;  // 4*XT doubles
   const BlockDev A = P.blk[tk.a];
+  Reg R;
   switch (tk.type) {
     case X_COLMAX: {
-      const int m = A.nrows;
+      const int m = A.nrows, c0 = tk.c * XT, nc = min(XT, m - c0);
       const double* G = P.vals + A.ent;
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-      for (int c = warp; c < m; c += nw) {
-        double mx = 0.0;
-        for (int r = lane; r < m; r += 32) mx = fmax(mx, fabs(ldcg(G + static_cast<size_t>(c) * m + r)));
+      for (int c = c0 + warp; c < c0 + nc; c += nw) {
+        const double* col = G + static_cast<size_t>(c) * m;
+        double mx0 = 0.0, mx1 = 0.0;
+        int r = lane;
+        for (; r + 32 < m; r += 64) {
+          mx0 = fmax(mx0, fabs(ldcg(col + r)));
+          mx1 = fmax(mx1, fabs(ldcg(col + r + 32)));
+        }
+        if (r < m) mx0 = fmax(mx0, fabs(ldcg(col + r)));
+        double mx = fmax(mx0, mx1);
         for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         if (lane == 0) {
           P.colmax[A.dg + c] = mx;
@@ -236,32 +346,29 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
     case X_GETRF: {
       const int m = A.nrows, k0 = tk.k * XT, n = min(XT, m - k0);
       double* G = P.vals + A.ent + static_cast<size_t>(k0) * m + k0;
-      load_tile(T0, G, m, n, n);
-      __syncthreads();
-      tile_lu(T0, n, P.bmax + A.dg + k0);
-      store_tile(G, m, T0, n, n);
+      reg_load(R, G, m, n, n);
+      reg_lu(R, n, P.bmax + A.dg + k0, scratch);
+      reg_store(G, m, R, n, n);
       break;
     }
     case X_TRSM_L: {
       const int m = A.nrows, k0 = tk.k * XT, r0 = tk.r * XT, nk = min(XT, m - k0), nr = min(XT, m - r0);
-      const double* Gd = P.vals + A.ent + static_cast<size_t>(k0) * m + k0;
       double* G = P.vals + A.ent + static_cast<size_t>(k0) * m + r0;
-      load_tile(T1, Gd, m, nk, nk);
-      load_tile(T0, G, m, nr, nk);
+      load_tile(T1, P.vals + A.ent + static_cast<size_t>(k0) * m + k0, m, nk, nk);
+      reg_load(R, G, m, nr, nk);
       __syncthreads();
-      tile_right_upper(T0, nr, nk, T1, P.bmax + A.dg + k0, cmx);
-      store_tile(G, m, T0, nr, nk);
+      reg_right_upper(R, nr, nk, T1, P.bmax + A.dg + k0, scratch);
+      reg_store(G, m, R, nr, nk);
       break;
     }
     case X_TRSM_U: {
       const int m = A.nrows, k0 = tk.k * XT, c0 = tk.c * XT, nk = min(XT, m - k0), nc = min(XT, m - c0);
-      const double* Gd = P.vals + A.ent + static_cast<size_t>(k0) * m + k0;
       double* G = P.vals + A.ent + static_cast<size_t>(c0) * m + k0;
-      load_tile(T1, Gd, m, nk, nk);
-      load_tile(T0, G, m, nk, nc);
+      load_tile(T1, P.vals + A.ent + static_cast<size_t>(k0) * m + k0, m, nk, nk);
+      reg_load(R, G, m, nk, nc);
       __syncthreads();
-      tile_left_unit_lower(T0, nk, nc, T1);
-      store_tile(G, m, T0, nk, nc);
+      reg_left_unit_lower(R, nk, nc, T1, scratch);
+      reg_store(G, m, R, nk, nc);
       break;
     }
     case X_GEMM: {
@@ -274,7 +381,8 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       load_opB(T2, base + static_cast<size_t>(c0) * m + k0, m, nk, nc);
       __syncthreads();
       tile_mma_sub(T0, T1, T2);
-      store_tile(G, m, T0, nr, nc);
+      reg_from_smem(R, T0);
+      reg_store(G, m, R, nr, nc);
       break;
     }
     case X_FINAL: {
@@ -282,8 +390,8 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       const double* G = P.vals + A.ent;
       for (int c = threadIdx.x; c < m; c += blockDim.x) {
         const double u = fabs(ldcg(G + static_cast<size_t>(c) * m + c));
-        const double below = __longlong_as_double(static_cast<long long>(__ldcg(
-            reinterpret_cast<const unsigned long long*>(P.bmax + A.dg + c))));
+        const double below = __longlong_as_double(static_cast<long long>(
+            __ldcg(reinterpret_cast<const unsigned long long*>(P.bmax + A.dg + c))));
         const double piv = fmax(u, below);
         if (piv == 0.0 || piv < pivot_tol * __ldcg(P.colmax + A.dg + c) || isnan(u)) record(&P.err[0], tk.step, c);
         else if (below > u) record(&P.err[1], tk.step, c);
@@ -295,27 +403,27 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       // GESSM on panel X (rows R_X): L = unit lower of diagonal block D restricted to R_X
       const BlockDev D = P.blk[tk.d];
       const int m = D.nrows, ld = A.nR;
-      const int32_t* R = A.store == STORE_RECT ? P.rlist + A.roff : nullptr;
+      const int32_t* Rl = A.store == STORE_RECT ? P.rlist + A.roff : nullptr;
       const int r0 = tk.r * XT, c0 = tk.c * XT, nr = min(XT, A.nR - r0), nc = min(XT, A.nC - c0);
       double* G = P.vals + A.ent + static_cast<size_t>(c0) * ld + r0;
       const double* Dv = P.vals + D.ent;
       if (tk.type == X_PG_DIAG) {
-        // gathered L_sub = D[R[r0+a], R[r0+b]]
-        if (R) load_tile(T1, Dv, m, nr, nr, R + r0, R + r0);
+        if (Rl) load_tile(T1, Dv, m, nr, nr, Rl + r0, Rl + r0);
         else load_tile(T1, Dv + static_cast<size_t>(r0) * m + r0, m, nr, nr);
-        load_tile(T0, G, ld, nr, nc);
+        reg_load(R, G, ld, nr, nc);
         __syncthreads();
-        tile_left_unit_lower(T0, nr, nc, T1);
+        reg_left_unit_lower(R, nr, nc, T1, scratch);
       } else {
         const int k0 = tk.k * XT, nk = min(XT, A.nR - k0);
         load_tile(T0, G, ld, nr, nc);
-        if (R) load_opA(T1, Dv, m, nr, nk, R + r0, R + k0);
+        if (Rl) load_opA(T1, Dv, m, nr, nk, Rl + r0, Rl + k0);
         else load_opA(T1, Dv + static_cast<size_t>(k0) * m + r0, m, nr, nk);
         load_opB(T2, P.vals + A.ent + static_cast<size_t>(c0) * ld + k0, ld, nk, nc);
         __syncthreads();
         tile_mma_sub(T0, T1, T2);
+        reg_from_smem(R, T0);
       }
-      store_tile(G, ld, T0, nr, nc);
+      reg_store(G, ld, R, nr, nc);
       break;
     }
     case X_PT_DIAG:
@@ -330,9 +438,9 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       if (tk.type == X_PT_DIAG) {
         if (Cl) load_tile(T1, Dv, m, nc, nc, Cl + c0, Cl + c0);
         else load_tile(T1, Dv + static_cast<size_t>(c0) * m + c0, m, nc, nc);
-        load_tile(T0, G, ld, nr, nc);
+        reg_load(R, G, ld, nr, nc);
         __syncthreads();
-        tile_right_upper(T0, nr, nc, T1, nullptr, cmx);
+        reg_right_upper(R, nr, nc, T1, nullptr, scratch);
       } else {
         const int k0 = tk.k * XT, nk = min(XT, A.nC - k0);
         load_tile(T0, G, ld, nr, nc);
@@ -341,8 +449,9 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
         else load_opB(T2, Dv + static_cast<size_t>(c0) * m + k0, m, nk, nc);
         __syncthreads();
         tile_mma_sub(T0, T1, T2);
+        reg_from_smem(R, T0);
       }
-      store_tile(G, ld, T0, nr, nc);
+      reg_store(G, ld, R, nr, nc);
       break;
     }
     default:
@@ -355,10 +464,10 @@ __global__ void __launch_bounds__(256) exec_kernel(XLevel L, DevPools P, double 
   __shared__ int s_t;
   for (;;) {
     if (threadIdx.x == 0) {
-      int t = atomicAdd(L.head, 1);
+      const int t = atomicAdd(L.head, 1);
       if (t < L.ntasks) {
         volatile int* dp = L.deps + t;
-        while (*dp > 0) __nanosleep(64);
+        while (*dp > 0) __nanosleep(32);
         __threadfence();
       }
       s_t = t;
@@ -373,7 +482,6 @@ __global__ void __launch_bounds__(256) exec_kernel(XLevel L, DevPools P, double 
     if (threadIdx.x == 0) {
       for (int e = L.succ_ptr[t]; e < L.succ_ptr[t + 1]; ++e) atomicSub(L.deps + L.succ[e], 1);
     }
-    __syncthreads();
   }
 }
 

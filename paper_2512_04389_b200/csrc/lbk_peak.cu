@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(256) dfma_loop(double* out, int iters) {
 
 extern "C" int lbk_fp64_peak(int device, double* tflops_dmma, double* tflops_dfma) {
   if (cudaSetDevice(device) != cudaSuccess) return LBK_ERR_CUDA;
+  (void)cudaGetLastError();  // clear a stale (non-sticky) error left by an earlier call
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   double* out = nullptr;
