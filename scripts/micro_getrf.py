@@ -1,0 +1,26 @@
+"""Micro benchmark: one dense diagonal block (single-block plan) -> tiled GETRF only."""
+import sys
+import time
+
+import numpy as np
+
+sys.path.insert(0, ".")
+import paper_2512_04389_b200 as M  # noqa: E402
+from paper_2512_04389_b200.numeric import Engine  # noqa: E402
+
+m = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
+nb = int(sys.argv[2]) if len(sys.argv) > 2 else m
+reps = int(sys.argv[3]) if len(sys.argv) > 3 else 5
+a = M.generate("dense", m)
+f = M.symbolic_factorize(M.symmetrize_pattern(a))
+g = M.partition(f, a, M.regular_plan(m, nb))
+t = M.dependency_levels(g)
+eng = Engine(g, t)
+eng.upload()
+for _ in range(2):
+    eng.run_device()
+ms = [eng.run_device() for _ in range(reps)]
+lv = eng.level_times()
+print(f"m={m} bs={nb} p={g.p} tasks={t.task_count} exec_items={eng.n_tile_items} launches={eng.n_launches} "
+      f"ms/step={np.median(ms):.3f} levels_ms={lv[:, 0].sum():.3f} exec_ms={lv[:, 3].sum():.3f} "
+      f"gemm_ms={lv[:, 1].sum():.3f} csc_ms={lv[:, 4].sum():.3f} GF/s={2 / 3 * m ** 3 / np.median(ms) / 1e6:.1f}")
