@@ -173,6 +173,7 @@ struct lbk_ctx {
   DevBuf<int> xdeps, xheads;
   int64_t n_exec = 0;
   bool use_exec = true;
+  DevBuf<unsigned long long> xtrace;  // executor task timeline (instrumented replays only)
 };
 
 namespace {
@@ -946,6 +947,7 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
         X.deps = c->xdeps.p + L.exec_off;
         X.head = c->xheads.p + l;
         X.ntasks = L.nexec;
+        X.trace = (evs && c->xtrace.p) ? c->xtrace.p + 3 * L.exec_off : nullptr;
         const int grid = std::max(1, std::min(L.nexec, 148 * 2));
         exec_kernel<<<grid, 256, EXEC_SMEM, s2>>>(X, P, pivot_tol);
       } else {
@@ -1138,6 +1140,42 @@ int lbk_level_times(lbk_ctx* c, double pivot_tol, double static_eps, float* out_
   for (auto& x : ev) cudaEventDestroy(x);
   if (e != cudaSuccess) return cuda_fail(st, e, "instrumented replay");
   return finish(c, st);
+}
+
+// Executor timeline: one instrumented replay with per-task globaltimer stamps.
+// trace[3 x n] = dequeue, ready (dependencies met), done (ns); info[6 x n] =
+// type, a, r, c, k, level.  *n = executor tasks (call with NULLs to size).
+int lbk_exec_trace(lbk_ctx* c, double pivot_tol, double static_eps, uint64_t* trace, int32_t* info, int64_t* n,
+                   lbk_status* st) {
+  *n = c->n_exec;
+  if (!trace || !info) {
+    ok(st);
+    return 0;
+  }
+  LBK_CUDA(cudaSetDevice(c->device), st);
+  LBK_CUDA(c->xtrace.alloc(3 * std::max<int64_t>(c->n_exec, 1)), st);
+  LBK_CUDA(cudaMemset(c->xtrace.p, 0, 3 * std::max<int64_t>(c->n_exec, 1) * 8), st);
+  std::vector<float> lv(c->levels.size() * 5);
+  const int rc = lbk_level_times(c, pivot_tol, static_eps, lv.data(), st);
+  if (rc == LBK_ERR_CUDA || rc == LBK_ERR_OOM) return rc;
+  LBK_CUDA(cudaMemcpy(trace, c->xtrace.p, 3 * c->n_exec * 8, cudaMemcpyDeviceToHost), st);
+  std::vector<XTask> ht(c->n_exec);
+  LBK_CUDA(cudaMemcpy(ht.data(), c->xtasks.p, c->n_exec * sizeof(XTask), cudaMemcpyDeviceToHost), st);
+  for (size_t l = 0; l < c->levels.size(); ++l)
+    for (int32_t q = 0; q < c->levels[l].nexec; ++q) {
+      const int64_t t = c->levels[l].exec_off + q;
+      const XTask& x = ht[t];
+      int32_t* o = info + 6 * t;
+      o[0] = x.type;
+      o[1] = x.a;
+      o[2] = x.r;
+      o[3] = x.c;
+      o[4] = x.k;
+      o[5] = static_cast<int32_t>(l);
+    }
+  c->xtrace.release();
+  ok(st);
+  return 0;
 }
 
 // levels[4 x nlevels]: generic item offset, generic items, DMMA tiles, panel strips.

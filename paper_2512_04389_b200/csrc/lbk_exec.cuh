@@ -67,7 +67,14 @@ struct XLevel {
   int* deps;   // working dependency counters (reset from a pristine copy per run)
   int* head;   // task counter of this level
   int ntasks;
+  unsigned long long* trace;  // optional: per task [dequeue, ready, done] in ns (globaltimer)
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
 
@@ -466,9 +473,11 @@ __global__ void __launch_bounds__(256) exec_kernel(XLevel L, DevPools P, double 
     if (threadIdx.x == 0) {
       const int t = atomicAdd(L.head, 1);
       if (t < L.ntasks) {
+        if (L.trace) L.trace[3 * t] = gtimer();
         volatile int* dp = L.deps + t;
         while (*dp > 0) __nanosleep(32);
         __threadfence();
+        if (L.trace) L.trace[3 * t + 1] = gtimer();
       }
       s_t = t;
     }
@@ -481,6 +490,7 @@ __global__ void __launch_bounds__(256) exec_kernel(XLevel L, DevPools P, double 
     __syncthreads();
     if (threadIdx.x == 0) {
       for (int e = L.succ_ptr[t]; e < L.succ_ptr[t + 1]; ++e) atomicSub(L.deps + L.succ[e], 1);
+      if (L.trace) L.trace[3 * t + 2] = gtimer();
     }
   }
 }

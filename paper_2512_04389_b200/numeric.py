@@ -70,6 +70,7 @@ def _dev():
     d(lib, "lbk_fp64_peak", C.c_int, [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)])
     d(lib, "lbk_task_routes", C.c_int, [vp, i8p])
     d(lib, "lbk_download_work", C.c_int, [vp, f64p, i64p, st])
+    d(lib, "lbk_exec_trace", C.c_int, [vp, C.c_double, C.c_double, C.POINTER(C.c_uint64), i32p, i64p, st])
     d(lib, "lbk_plan_levels", C.c_int, [vp, i64p, i32p])
     _native._dev = lib
     return lib
@@ -243,6 +244,20 @@ class Engine:
         if self.lib.lbk_download_work(self.ctx, P(out, f64p), C.byref(n), C.byref(st)):
             _native.raise_status(st, "lbk_download_work")
         return out
+
+    def exec_trace(self, pivot_tol=DEFAULT_PIVOT_TOL):
+        """(trace[n,3] ns, info[n,6]) of the persistent executor's tile tasks (one instrumented replay)."""
+        if not self._resident:
+            self.upload()
+        n = C.c_int64()
+        st = _native.LbkStatus()
+        self.lib.lbk_exec_trace(self.ctx, pivot_tol, math.nan, None, None, C.byref(n), C.byref(st))
+        tr = np.zeros((n.value, 3), np.uint64)
+        info = np.zeros((n.value, 6), np.int32)
+        self.lib.lbk_exec_trace(self.ctx, pivot_tol, math.nan, tr.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                P(info, i32p), C.byref(n), C.byref(st))
+        _native.raise_status(st, "lbk_exec_trace")
+        return tr, info
 
     def task_routes(self) -> np.ndarray:
         """Kernel family per task: -1 skipped, 0 CSC, 1 DMMA SSSSM, 2 panel, 3 tiled GETRF."""

@@ -24,3 +24,20 @@ lv = eng.level_times()
 print(f"m={m} bs={nb} p={g.p} tasks={t.task_count} exec_items={eng.n_tile_items} launches={eng.n_launches} "
       f"ms/step={np.median(ms):.3f} levels_ms={lv[:, 0].sum():.3f} exec_ms={lv[:, 3].sum():.3f} "
       f"gemm_ms={lv[:, 1].sum():.3f} csc_ms={lv[:, 4].sum():.3f} GF/s={2 / 3 * m ** 3 / np.median(ms) / 1e6:.1f}")
+
+if "--trace" in sys.argv:
+    tr, info = eng.exec_trace()
+    tr = tr.astype(np.int64)
+    t0 = tr[:, 0][tr[:, 0] > 0].min()
+    names = ["COLMAX", "GETRF", "TRSM_L", "TRSM_U", "GEMM", "FINAL", "PG_DIAG", "PG_UPD", "PT_DIAG", "PT_UPD"]
+    for ty in np.unique(info[:, 0]):
+        sel = info[:, 0] == ty
+        run = (tr[sel, 2] - tr[sel, 1]) / 1e3
+        wait = (tr[sel, 1] - tr[sel, 0]) / 1e3
+        print(f"{names[ty]:8s} n={sel.sum():6d} run us med {np.median(run):7.2f} p90 {np.percentile(run, 90):7.2f}"
+              f" wait med {np.median(wait):8.2f}")
+    g = np.flatnonzero(info[:, 0] == 1)
+    for t in g[:6]:
+        print(f"GETRF k={info[t, 4]} dequeue {(tr[t, 0] - t0) / 1e3:9.1f} ready {(tr[t, 1] - t0) / 1e3:9.1f}"
+              f" done {(tr[t, 2] - t0) / 1e3:9.1f} us")
+    np.savez("gpurun_out/exec_trace.npz", trace=tr, info=info)
