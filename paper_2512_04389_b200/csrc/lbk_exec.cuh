@@ -78,180 +78,123 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
 
-// ---- register tiles: thread owns rows 4*ty+i, columns 4*tx+j ----------------
-struct Reg {
-  double a[4][4];
+// ---- register tiles -------------------------------------------------------------
+// 256 threads = 64 lines x 4 lanes: thread (line = tid/4, q = tid%4) owns the 16
+// entries 4*i+q (i = 0..15) of its line (a row for right solves, a column for
+// left solves).  The 4 lanes of a line sit in one warp, so the value produced
+// at step j is broadcast with one shuffle: no CTA barrier in the solves.
+struct Line {
+  double x[16];
 };
 
-__device__ __forceinline__ int reg_ty() { return threadIdx.x & 15; }
-__device__ __forceinline__ int reg_tx() { return threadIdx.x >> 4; }
+__device__ __forceinline__ int line_id() { return threadIdx.x >> 2; }
+__device__ __forceinline__ int line_q() { return threadIdx.x & 3; }
 
-__device__ __forceinline__ void reg_load(Reg& R, const double* G, int ld, int nr, int nc,
+// row `r` of a column-major tile: entries (r, 4i+q)
+__device__ __forceinline__ void row_load(Line& L, const double* G, int ld, int nr, int nc,
                                          const int32_t* rg = nullptr, const int32_t* cg = nullptr) {
-  const int r0 = 4 * reg_ty(), c0 = 4 * reg_tx();
+  const int r = line_id(), q = line_q();
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int c = c0 + j;
-    const bool cv = c < nc;
-    const size_t co = cv ? static_cast<size_t>(cg ? cg[c] : c) * ld : 0;
+  for (int i = 0; i < 16; ++i) {
+    const int c = 4 * i + q;
+    L.x[i] = (r < nr && c < nc) ? ldcg(G + static_cast<size_t>(cg ? cg[c] : c) * ld + (rg ? rg[r] : r)) : 0.0;
+  }
+}
+
+__device__ __forceinline__ void row_store(double* G, int ld, const Line& L, int nr, int nc) {
+  const int r = line_id(), q = line_q();
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = r0 + i;
-      R.a[i][j] = (cv && r < nr) ? ldcg(G + co + (rg ? rg[r] : r)) : 0.0;
+  for (int i = 0; i < 16; ++i) {
+    const int c = 4 * i + q;
+    if (r < nr && c < nc) G[static_cast<size_t>(c) * ld + r] = L.x[i];
+  }
+}
+
+// column `c` of a column-major tile: entries (4i+q, c)
+__device__ __forceinline__ void col_load(Line& L, const double* G, int ld, int nr, int nc) {
+  const int c = line_id(), q = line_q();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int r = 4 * i + q;
+    L.x[i] = (r < nr && c < nc) ? ldcg(G + static_cast<size_t>(c) * ld + r) : 0.0;
+  }
+}
+
+__device__ __forceinline__ void col_store(double* G, int ld, const Line& L, int nr, int nc) {
+  const int c = line_id(), q = line_q();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int r = 4 * i + q;
+    if (r < nr && c < nc) G[static_cast<size_t>(c) * ld + r] = L.x[i];
+  }
+}
+
+// X (rows in registers, nc columns) <- X U^{-1}; U upper in smem (XTP stride).
+// rinv[j] = 1/u_jj precomputed (smem).  bmax: per column max |x_rj| before
+// scaling, accumulated in smem cm[] then flushed by the caller.
+template <bool kCheck>
+__device__ __forceinline__ void line_right_upper(Line& L, int nc, const double* U, const double* rinv,
+                                                 unsigned long long* cm) {
+  const int q = line_q(), lane = threadIdx.x & 31, base = lane & ~3;
+#pragma unroll
+  for (int j = 0; j < XT; ++j) {
+    if (j >= nc) break;
+    const int jq = j & 3, ji = j >> 2;
+    double v = 0.0;
+    if (q == jq) {
+      const double d = L.x[ji];
+      if (kCheck && d != 0.0)
+        atomicMax(&cm[j], static_cast<unsigned long long>(__double_as_longlong(fabs(d))));
+      v = d * rinv[j];
+      L.x[ji] = v;
+    }
+    const double xj = __shfl_sync(0xffffffffu, v, base | jq);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int c = 4 * i + q;
+      if (c > j && c < nc) L.x[i] = dsub_mul(L.x[i], xj, U[c * XTP + j]);
     }
   }
 }
 
-__device__ __forceinline__ void reg_store(double* G, int ld, const Reg& R, int nr, int nc) {
-  const int r0 = 4 * reg_ty(), c0 = 4 * reg_tx();
+// X (columns in registers, nr rows) <- L^{-1} X; L unit lower in smem (XTP stride).
+__device__ __forceinline__ void line_left_unit_lower(Line& X, int nr, const double* Lm) {
+  const int q = line_q(), lane = threadIdx.x & 31, base = lane & ~3;
 #pragma unroll
-  for (int j = 0; j < 4; ++j)
+  for (int k = 0; k < XT; ++k) {
+    if (k >= nr) break;
+    const int kq = k & 3, ki = k >> 2;
+    const double xk = __shfl_sync(0xffffffffu, X.x[ki], base | kq);
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (r0 + i < nr && c0 + j < nc) G[static_cast<size_t>(c0 + j) * ld + r0 + i] = R.a[i][j];
+    for (int i = 0; i < 16; ++i) {
+      const int r = 4 * i + q;
+      if (r > k && r < nr) X.x[i] = dsub_mul(X.x[i], Lm[k * XTP + r], xk);
+    }
+  }
 }
 
-// smem tile (XTP stride) -> registers / back
-__device__ __forceinline__ void reg_from_smem(Reg& R, const double* T) {
-  const int r0 = 4 * reg_ty(), c0 = 4 * reg_tx();
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) R.a[i][j] = T[(c0 + j) * XTP + r0 + i];
-}
-
-// max over the 16 threads of one column group (a half warp: tid = 16*tx + ty)
-__device__ __forceinline__ double halfwarp_max(double v) {
-  for (int o = 8; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-
-// LU without row exchange of the n x n register tile; bmax[j] gets max |d_qj|
-// over rows q > j before scaling.  scratch: 4*XT doubles of smem.
-__device__ void reg_lu(Reg& R, int n, unsigned long long* bmax, double* scratch) {
-  const int ty = reg_ty(), tx = reg_tx();
-  double* urow = scratch;           // [2][XT]
-  double* lcol = scratch + 2 * XT;  // [2][XT]
+// LU without row exchange of the n x n tile in smem (XTP stride), one
+// barrier per elimination step.  Thread (r, q) updates row r, columns 4i+q;
+// the 4 lanes of a row compute l_rj redundantly (true division), the owner of
+// column j writes it back after a __syncwarp.  bmax[j] gets max |d_rj| over
+// rows r > j before scaling.
+__device__ void smem_lu(double* T, int n, unsigned long long* bmax) {
+  const int r = line_id(), q = line_q(), lane = threadIdx.x & 31;
   for (int j = 0; j < n; ++j) {
-    const int b = (j & 1) * XT;
-    const int jb = j >> 2, jr = j & 3;
-    if (ty == jb) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (i == jr) urow[b + 4 * tx + q] = R.a[i][q];
+    const double u = T[j * XTP + j];
+    const bool act = r > j && r < n;
+    const double d = act ? T[j * XTP + r] : 0.0;
+    const double l = act ? __ddiv_rn(d, u) : 0.0;
+    double mx = (q == 0) ? fabs(d) : 0.0;
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0 && mx > 0.0) atomic_max_nonneg(&bmax[j], mx);
+    __syncwarp();
+    if (act) {
+      if (q == (j & 3)) T[j * XTP + r] = l;
+      for (int c = j + 1 + ((q - j - 1) & 3); c < n; c += 4) T[c * XTP + r] = dsub_mul(T[c * XTP + r], l, T[c * XTP + j]);
     }
     __syncthreads();
-    const double u = urow[b + j];
-    double mx = 0.0;
-    if (tx == jb) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = 4 * ty + i;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (q == jr && r > j && r < n) {
-            const double d = R.a[i][q];
-            mx = fmax(mx, fabs(d));
-            const double l = __ddiv_rn(d, u);
-            R.a[i][q] = l;
-            lcol[b + r] = l;
-          }
-      }
-    }
-    mx = halfwarp_max(mx);  // whole warp participates; only the owners' half is nonzero
-    if (tx == jb && ty == 0 && mx > 0.0) atomic_max_nonneg(&bmax[j], mx);
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = 4 * ty + i;
-      if (r <= j || r >= n) continue;
-      const double l = lcol[b + r];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = 4 * tx + q;
-        if (c > j && c < n) R.a[i][q] = dsub_mul(R.a[i][q], l, urow[b + c]);
-      }
-    }
   }
-  __syncthreads();
-}
-
-// X (register tile nr x nc) <- X U^{-1}, U upper (smem, XTP stride, diag included).
-// bmax != nullptr: record max |x_qj| before the division for every column j.
-__device__ void reg_right_upper(Reg& R, int nr, int nc, const double* U, unsigned long long* bmax,
-                                double* scratch) {
-  const int ty = reg_ty(), tx = reg_tx();
-  double* lcol = scratch;  // [2][XT]
-  for (int j = 0; j < nc; ++j) {
-    const int b = (j & 1) * XT;
-    const int jb = j >> 2, jr = j & 3;
-    double mx = 0.0;
-    if (tx == jb) {
-      const double u = U[j * XTP + j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = 4 * ty + i;
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (q == jr && r < nr) {
-            const double d = R.a[i][q];
-            mx = fmax(mx, fabs(d));
-            const double x = __ddiv_rn(d, u);
-            R.a[i][q] = x;
-            lcol[b + r] = x;
-          }
-      }
-    }
-    if (bmax) {
-      mx = halfwarp_max(mx);
-      if (tx == jb && ty == 0 && mx > 0.0) atomic_max_nonneg(&bmax[j], mx);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = 4 * ty + i;
-      if (r >= nr) continue;
-      const double x = lcol[b + r];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = 4 * tx + q;
-        if (c > j && c < nc) R.a[i][q] = dsub_mul(R.a[i][q], x, U[c * XTP + j]);
-      }
-    }
-  }
-  __syncthreads();
-}
-
-// X (register tile nr x nc) <- L^{-1} X, L unit lower (smem, XTP stride).
-__device__ void reg_left_unit_lower(Reg& R, int nr, int nc, const double* L, double* scratch) {
-  const int ty = reg_ty(), tx = reg_tx();
-  double* xrow = scratch;  // [2][XT]
-  for (int k = 0; k < nr; ++k) {
-    const int b = (k & 1) * XT;
-    const int kb = k >> 2, kr = k & 3;
-    if (ty == kb) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-          if (i == kr) xrow[b + 4 * tx + q] = R.a[i][q];
-    }
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = 4 * ty + i;
-      if (r <= k || r >= nr) continue;
-      const double l = L[k * XTP + r];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int c = 4 * tx + q;
-        if (c < nc) R.a[i][q] = dsub_mul(R.a[i][q], l, xrow[b + c]);
-      }
-    }
-  }
-  __syncthreads();
 }
 
 // ---- smem staging -------------------------------------------------------------
@@ -319,13 +262,30 @@ __device__ void tile_mma_sub(double* Cs, const double* As, const double* Bs) {
   __syncthreads();
 }
 
+// C (smem, XTP stride) -> global, masked
+__device__ __forceinline__ void store_tile(double* G, int ld, const double* T, int nr, int nc) {
+  for (int idx = threadIdx.x; idx < XT * XT; idx += blockDim.x) {
+    const int r = idx & (XT - 1), c = idx >> 6;
+    if (r < nr && c < nc) G[static_cast<size_t>(c) * ld + r] = T[c * XTP + r];
+  }
+}
+
+// rinv[j] = 1 / U(j,j) of an smem tile; cm[] cleared (bmax staging)
+__device__ __forceinline__ void prep_right(const double* U, int n, double* rinv, unsigned long long* cm) {
+  for (int j = threadIdx.x; j < XT; j += blockDim.x) {
+    rinv[j] = j < n ? 1.0 / U[j * XTP + j] : 0.0;
+    cm[j] = 0ull;
+  }
+}
+
 __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double pivot_tol) {
   double* T0 = sm;                  // target tile (XTP stride)
   double* T1 = sm + XREG;           // operand tile (XTP stride) / DMMA A (XS stride)
   double* T2 = sm + 2 * XREG;       // DMMA B (XS stride)
-  double* scratch = sm + 3 * XREG;  // 4*XT doubles
+  double* rinv = sm + 3 * XREG;     // XT doubles
+  unsigned long long* cm = reinterpret_cast<unsigned long long*>(sm + 3 * XREG + XT);  // XT
   const BlockDev A = P.blk[tk.a];
-  Reg R;
+  Line X;
   switch (tk.type) {
     case X_COLMAX: {
       const int m = A.nrows, c0 = tk.c * XT, nc = min(XT, m - c0);
@@ -333,14 +293,16 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
       for (int c = c0 + warp; c < c0 + nc; c += nw) {
         const double* col = G + static_cast<size_t>(c) * m;
-        double mx0 = 0.0, mx1 = 0.0;
+        double mx0 = 0.0, mx1 = 0.0, mx2 = 0.0, mx3 = 0.0;
         int r = lane;
-        for (; r + 32 < m; r += 64) {
+        for (; r + 96 < m; r += 128) {
           mx0 = fmax(mx0, fabs(ldcg(col + r)));
           mx1 = fmax(mx1, fabs(ldcg(col + r + 32)));
+          mx2 = fmax(mx2, fabs(ldcg(col + r + 64)));
+          mx3 = fmax(mx3, fabs(ldcg(col + r + 96)));
         }
-        if (r < m) mx0 = fmax(mx0, fabs(ldcg(col + r)));
-        double mx = fmax(mx0, mx1);
+        for (; r < m; r += 32) mx0 = fmax(mx0, fabs(ldcg(col + r)));
+        double mx = fmax(fmax(mx0, mx1), fmax(mx2, mx3));
         for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
         if (lane == 0) {
           P.colmax[A.dg + c] = mx;
@@ -353,29 +315,35 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
     case X_GETRF: {
       const int m = A.nrows, k0 = tk.k * XT, n = min(XT, m - k0);
       double* G = P.vals + A.ent + static_cast<size_t>(k0) * m + k0;
-      reg_load(R, G, m, n, n);
-      reg_lu(R, n, P.bmax + A.dg + k0, scratch);
-      reg_store(G, m, R, n, n);
+      load_tile(T0, G, m, n, n);
+      __syncthreads();
+      smem_lu(T0, n, P.bmax + A.dg + k0);
+      store_tile(G, m, T0, n, n);
       break;
     }
-    case X_TRSM_L: {
+    case X_TRSM_L: {  // rows of tile (r,k) in registers, U_kk in smem
       const int m = A.nrows, k0 = tk.k * XT, r0 = tk.r * XT, nk = min(XT, m - k0), nr = min(XT, m - r0);
       double* G = P.vals + A.ent + static_cast<size_t>(k0) * m + r0;
       load_tile(T1, P.vals + A.ent + static_cast<size_t>(k0) * m + k0, m, nk, nk);
-      reg_load(R, G, m, nr, nk);
+      row_load(X, G, m, nr, nk);
       __syncthreads();
-      reg_right_upper(R, nr, nk, T1, P.bmax + A.dg + k0, scratch);
-      reg_store(G, m, R, nr, nk);
+      prep_right(T1, nk, rinv, cm);
+      __syncthreads();
+      line_right_upper<true>(X, nk, T1, rinv, cm);
+      row_store(G, m, X, nr, nk);
+      __syncthreads();
+      for (int c = threadIdx.x; c < nk; c += blockDim.x)
+        if (cm[c]) atomicMax(P.bmax + A.dg + k0 + c, cm[c]);
       break;
     }
-    case X_TRSM_U: {
+    case X_TRSM_U: {  // columns of tile (k,c) in registers, L_kk in smem
       const int m = A.nrows, k0 = tk.k * XT, c0 = tk.c * XT, nk = min(XT, m - k0), nc = min(XT, m - c0);
       double* G = P.vals + A.ent + static_cast<size_t>(c0) * m + k0;
       load_tile(T1, P.vals + A.ent + static_cast<size_t>(k0) * m + k0, m, nk, nk);
-      reg_load(R, G, m, nk, nc);
+      col_load(X, G, m, nk, nc);
       __syncthreads();
-      reg_left_unit_lower(R, nk, nc, T1, scratch);
-      reg_store(G, m, R, nk, nc);
+      line_left_unit_lower(X, nk, T1);
+      col_store(G, m, X, nk, nc);
       break;
     }
     case X_GEMM: {
@@ -388,8 +356,7 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       load_opB(T2, base + static_cast<size_t>(c0) * m + k0, m, nk, nc);
       __syncthreads();
       tile_mma_sub(T0, T1, T2);
-      reg_from_smem(R, T0);
-      reg_store(G, m, R, nr, nc);
+      store_tile(G, m, T0, nr, nc);
       break;
     }
     case X_FINAL: {
@@ -417,9 +384,10 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       if (tk.type == X_PG_DIAG) {
         if (Rl) load_tile(T1, Dv, m, nr, nr, Rl + r0, Rl + r0);
         else load_tile(T1, Dv + static_cast<size_t>(r0) * m + r0, m, nr, nr);
-        reg_load(R, G, ld, nr, nc);
+        col_load(X, G, ld, nr, nc);
         __syncthreads();
-        reg_left_unit_lower(R, nr, nc, T1, scratch);
+        line_left_unit_lower(X, nr, T1);
+        col_store(G, ld, X, nr, nc);
       } else {
         const int k0 = tk.k * XT, nk = min(XT, A.nR - k0);
         load_tile(T0, G, ld, nr, nc);
@@ -428,9 +396,8 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
         load_opB(T2, P.vals + A.ent + static_cast<size_t>(c0) * ld + k0, ld, nk, nc);
         __syncthreads();
         tile_mma_sub(T0, T1, T2);
-        reg_from_smem(R, T0);
+        store_tile(G, ld, T0, nr, nc);
       }
-      reg_store(G, ld, R, nr, nc);
       break;
     }
     case X_PT_DIAG:
@@ -445,9 +412,12 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       if (tk.type == X_PT_DIAG) {
         if (Cl) load_tile(T1, Dv, m, nc, nc, Cl + c0, Cl + c0);
         else load_tile(T1, Dv + static_cast<size_t>(c0) * m + c0, m, nc, nc);
-        reg_load(R, G, ld, nr, nc);
+        row_load(X, G, ld, nr, nc);
         __syncthreads();
-        reg_right_upper(R, nr, nc, T1, nullptr, scratch);
+        prep_right(T1, nc, rinv, cm);
+        __syncthreads();
+        line_right_upper<false>(X, nc, T1, rinv, cm);
+        row_store(G, ld, X, nr, nc);
       } else {
         const int k0 = tk.k * XT, nk = min(XT, A.nC - k0);
         load_tile(T0, G, ld, nr, nc);
@@ -456,9 +426,8 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
         else load_opB(T2, Dv + static_cast<size_t>(c0) * m + k0, m, nk, nc);
         __syncthreads();
         tile_mma_sub(T0, T1, T2);
-        reg_from_smem(R, T0);
+        store_tile(G, ld, T0, nr, nc);
       }
-      reg_store(G, ld, R, nr, nc);
       break;
     }
     default:
