@@ -171,6 +171,7 @@ struct lbk_ctx {
   DevBuf<XTask> xtasks;
   DevBuf<int32_t> xsptr, xsucc, xdeps0;
   DevBuf<int> xdeps, xheads;
+  DevBuf<int32_t> perm0;  // identity permutation per diagonal row
   int64_t n_exec = 0;
   bool use_exec = true;
   DevBuf<unsigned long long> xtrace;  // executor task timeline (instrumented replays only)
@@ -760,37 +761,46 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           const int64_t b = tgetrf[lv][q];
           const int m = hb[b].nrows, nt = (m + XT - 1) / XT;
           const int32_t stp = static_cast<int32_t>(T_bi[b]);
-          // column maxima at GETRF entry, one task per column tile; every first
-          // write into column tile c waits for colmax(c)
-          std::vector<int> last(static_cast<size_t>(nt) * nt), lt(nt, -1), ut(nt, -1), fin_deps;
-          for (int cc = 0; cc < nt; ++cc) {
-            const int col = X.add(X_COLMAX, b, b, 0, cc, 0, stp, -1, {});
-            for (int r = 0; r < nt; ++r) last[static_cast<size_t>(cc) * nt + r] = col;
-            fin_deps.push_back(col);
-          }
+          // column maxima at GETRF entry: tasks over (column tile, row chunk of
+          // COLMAX_ROWS); every first write into column tile c waits for all of
+          // column c's colmax tasks
+          std::vector<int> last(static_cast<size_t>(nt) * nt, -1), lt(nt, -1), ut(nt, -1), fin_deps;
+          std::vector<std::vector<int>> colj(nt);
+          for (int cc = 0; cc < nt; ++cc)
+            for (int rc = 0; rc * COLMAX_ROWS < m; ++rc) {
+              const int col = X.add(X_COLMAX, b, b, rc, cc, 0, stp, -1, {});
+              colj[cc].push_back(col);
+              fin_deps.push_back(col);
+            }
           auto L_ = [&](int r, int cc) -> int& { return last[static_cast<size_t>(cc) * nt + r]; };
+          auto prev = [&](int r, int cc, std::vector<int> extra) {
+            const int l = L_(r, cc);
+            if (l >= 0) extra.push_back(l);
+            else extra.insert(extra.end(), colj[cc].begin(), colj[cc].end());
+            return extra;
+          };
           for (int kb = 0; kb < nt; ++kb) {
-            const int g = X.add(X_GETRF, b, b, kb, kb, kb, stp, kb * 4, {L_(kb, kb)});
+            const int g = X.add(X_GETRF, b, b, kb, kb, kb, stp, kb * 4, prev(kb, kb, {}));
             L_(kb, kb) = g;
             fin_deps.push_back(g);
             for (int r = kb + 1; r < nt; ++r) {
               lt[r] = -1;
               if (!occ[q][static_cast<size_t>(kb) * nt + r]) continue;
-              lt[r] = X.add(X_TRSM_L, b, b, r, kb, kb, stp, kb * 4 + 1, {g, L_(r, kb)});
+              lt[r] = X.add(X_TRSM_L, b, b, r, kb, kb, stp, kb * 4 + 1, prev(r, kb, {g}));
               L_(r, kb) = lt[r];
               fin_deps.push_back(lt[r]);
             }
             for (int cc = kb + 1; cc < nt; ++cc) {
               ut[cc] = -1;
               if (!occ[q][static_cast<size_t>(cc) * nt + kb]) continue;
-              ut[cc] = X.add(X_TRSM_U, b, b, kb, cc, kb, stp, kb * 4 + 1, {g, L_(kb, cc)});
+              ut[cc] = X.add(X_TRSM_U, b, b, kb, cc, kb, stp, kb * 4 + 1, prev(kb, cc, {g}));
               L_(kb, cc) = ut[cc];
             }
             for (int cc = kb + 1; cc < nt; ++cc) {
               if (ut[cc] < 0) continue;
               for (int r = kb + 1; r < nt; ++r) {
                 if (lt[r] < 0) continue;
-                const int t2 = X.add(X_GEMM, b, b, r, cc, kb, stp, kb * 4 + 2, {lt[r], ut[cc], L_(r, cc)});
+                const int t2 = X.add(X_GEMM, b, b, r, cc, kb, stp, kb * 4 + 2, prev(r, cc, {lt[r], ut[cc]}));
                 L_(r, cc) = t2;
               }
             }
@@ -868,6 +878,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       if (T_bi[b] == T_bj[b])
         for (int r = 0; r < hb[b].nrows; ++r) idp[hb[b].dg + r] = r;
     LBK_CUDA(cudaMemcpy(c->perm.p, idp.data(), idp.size() * sizeof(int32_t), cudaMemcpyHostToDevice), st);
+    LBK_CUDA(c->perm0.upload(idp), st);
   } catch (const std::bad_alloc&) {
     return fail(st, LBK_ERR_OOM, "host allocation in lbk_plan");
   }
@@ -905,6 +916,11 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
   if (use_exec && c->n_exec) {
     cudaMemcpyAsync(c->xdeps.p, c->xdeps0.p, c->n_exec * sizeof(int), cudaMemcpyDeviceToDevice, s0);
     cudaMemsetAsync(c->xheads.p, 0, c->levels.size() * sizeof(int), s0);
+    if (c->ndiag_rows) {  // colmax/bmax accumulate with atomic max; perms start as identity
+      cudaMemsetAsync(c->colmax.p, 0, c->ndiag_rows * sizeof(double), s0);
+      cudaMemsetAsync(c->bmax.p, 0, c->ndiag_rows * sizeof(unsigned long long), s0);
+      cudaMemcpyAsync(c->perm.p, c->perm0.p, c->ndiag_rows * sizeof(int32_t), cudaMemcpyDeviceToDevice, s0);
+    }
   }
   if (evs) cudaEventRecordWithFlags((*evs)[0], s0, cudaEventRecordExternal);
   for (size_t l = 0; l < c->levels.size(); ++l) {

@@ -36,6 +36,7 @@ constexpr int XTP = XT + 1;     // padded smem column stride
 constexpr int XS = XT + 4;      // DMMA operand stride
 constexpr int XREG = XT * XS;   // one smem tile region (fits either stride)
 constexpr int EXEC_SMEM = (3 * XREG + 4 * XT) * 8;
+constexpr int COLMAX_ROWS = 512;  // rows per colmax task
 
 enum XType : int8_t {
   X_COLMAX = 0,  // colmax / bmax / perm reset of column tile c of diagonal block a
@@ -130,71 +131,117 @@ __device__ __forceinline__ void col_store(double* G, int ld, const Line& L, int 
 }
 
 // X (rows in registers, nc columns) <- X U^{-1}; U upper in smem (XTP stride).
-// rinv[j] = 1/u_jj precomputed (smem).  bmax: per column max |x_rj| before
-// scaling, accumulated in smem cm[] then flushed by the caller.
+// rinv[j] = 1/u_jj precomputed (smem).  kCheck: per column max |x_rj| before
+// scaling, staged in smem cm[] (flushed by the caller).  The outer loop over
+// groups of 4 columns stays rolled (i-cache friendly); after each group the
+// registers shift down by one so the owner's value is always x[0].
 template <bool kCheck>
 __device__ __forceinline__ void line_right_upper(Line& L, int nc, const double* U, const double* rinv,
                                                  unsigned long long* cm) {
   const int q = line_q(), lane = threadIdx.x & 31, base = lane & ~3;
+  const int ngroups = (nc + 3) >> 2;
+#pragma unroll 1
+  for (int jb = 0; jb < ngroups; ++jb) {
 #pragma unroll
-  for (int j = 0; j < XT; ++j) {
-    if (j >= nc) break;
-    const int jq = j & 3, ji = j >> 2;
-    double v = 0.0;
-    if (q == jq) {
-      const double d = L.x[ji];
-      if (kCheck && d != 0.0)
-        atomicMax(&cm[j], static_cast<unsigned long long>(__double_as_longlong(fabs(d))));
-      v = d * rinv[j];
-      L.x[ji] = v;
-    }
-    const double xj = __shfl_sync(0xffffffffu, v, base | jq);
+    for (int jr = 0; jr < 4; ++jr) {
+      const int j = 4 * jb + jr;
+      if (j >= nc) break;
+      double v = 0.0;
+      if (q == jr) {
+        const double d = L.x[0];
+        if (kCheck && d != 0.0)
+          atomicMax(&cm[j], static_cast<unsigned long long>(__double_as_longlong(fabs(d))));
+        v = d * rinv[j];
+        L.x[0] = v;
+      }
+      const double xj = __shfl_sync(0xffffffffu, v, base | jr);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int c = 4 * i + q;
-      if (c > j && c < nc) L.x[i] = dsub_mul(L.x[i], xj, U[c * XTP + j]);
+      for (int i = 0; i < 16; ++i) {
+        const int c = 4 * (jb + i) + q;  // column held in x[i] after jb shifts
+        if (c > j && c < nc) L.x[i] = dsub_mul(L.x[i], xj, U[c * XTP + j]);
+      }
     }
+    // retire x[0] (column 4*jb+q is final): park it at the end, shift the rest
+    const double done = L.x[0];
+#pragma unroll
+    for (int i = 0; i < 15; ++i) L.x[i] = L.x[i + 1];
+    L.x[15] = done;
+  }
+  // undo the rotation: x[15-t] holds column 4*(jb_done - 1 - t)+q ... restore natural order
+  // after ngroups rotations the array is rotated left by ngroups
+#pragma unroll 1
+  for (int t = ngroups; t < 16; ++t) {
+    const double w = L.x[0];
+#pragma unroll
+    for (int i = 0; i < 15; ++i) L.x[i] = L.x[i + 1];
+    L.x[15] = w;
   }
 }
 
 // X (columns in registers, nr rows) <- L^{-1} X; L unit lower in smem (XTP stride).
+// Same rolled-group / register-rotation scheme as line_right_upper.
 __device__ __forceinline__ void line_left_unit_lower(Line& X, int nr, const double* Lm) {
   const int q = line_q(), lane = threadIdx.x & 31, base = lane & ~3;
+  const int ngroups = (nr + 3) >> 2;
+#pragma unroll 1
+  for (int kb = 0; kb < ngroups; ++kb) {
 #pragma unroll
-  for (int k = 0; k < XT; ++k) {
-    if (k >= nr) break;
-    const int kq = k & 3, ki = k >> 2;
-    const double xk = __shfl_sync(0xffffffffu, X.x[ki], base | kq);
+    for (int kr = 0; kr < 4; ++kr) {
+      const int k = 4 * kb + kr;
+      if (k >= nr) break;
+      const double xk = __shfl_sync(0xffffffffu, X.x[0], base | kr);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int r = 4 * i + q;
-      if (r > k && r < nr) X.x[i] = dsub_mul(X.x[i], Lm[k * XTP + r], xk);
+      for (int i = 0; i < 16; ++i) {
+        const int r = 4 * (kb + i) + q;
+        if (r > k && r < nr) X.x[i] = dsub_mul(X.x[i], Lm[k * XTP + r], xk);
+      }
     }
+    const double done = X.x[0];
+#pragma unroll
+    for (int i = 0; i < 15; ++i) X.x[i] = X.x[i + 1];
+    X.x[15] = done;
+  }
+#pragma unroll 1
+  for (int t = ngroups; t < 16; ++t) {
+    const double w = X.x[0];
+#pragma unroll
+    for (int i = 0; i < 15; ++i) X.x[i] = X.x[i + 1];
+    X.x[15] = w;
   }
 }
 
 // LU without row exchange of the n x n tile in smem (XTP stride), one
 // barrier per elimination step.  Thread (r, q) updates row r, columns 4i+q;
 // the 4 lanes of a row compute l_rj redundantly (true division), the owner of
-// column j writes it back after a __syncwarp.  bmax[j] gets max |d_rj| over
-// rows r > j before scaling.
-__device__ void smem_lu(double* T, int n, unsigned long long* bmax) {
-  const int r = line_id(), q = line_q(), lane = threadIdx.x & 31;
+// column j writes it back after a __syncwarp.  The pre-scaling values d_rj are
+// staged in Dd (smem) and reduced to bmax[j] = max_{r>j} |d_rj| after the loop.
+__device__ void smem_lu(double* T, int n, unsigned long long* bmax, double* Dd) {
+  const int r = line_id(), q = line_q();
+#pragma unroll 1
   for (int j = 0; j < n; ++j) {
     const double u = T[j * XTP + j];
-    const bool act = r > j && r < n;
-    const double d = act ? T[j * XTP + r] : 0.0;
-    const double l = act ? __ddiv_rn(d, u) : 0.0;
-    double mx = (q == 0) ? fabs(d) : 0.0;
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0 && mx > 0.0) atomic_max_nonneg(&bmax[j], mx);
-    __syncwarp();
-    if (act) {
-      if (q == (j & 3)) T[j * XTP + r] = l;
+    if (r > j && r < n) {
+      const double d = T[j * XTP + r];
+      const double l = __ddiv_rn(d, u);
+      __syncwarp(0xfu << (threadIdx.x & 28));
+      if (q == (j & 3)) {
+        T[j * XTP + r] = l;
+        Dd[j * XTP + r] = fabs(d);
+      }
+#pragma unroll 1
       for (int c = j + 1 + ((q - j - 1) & 3); c < n; c += 4) T[c * XTP + r] = dsub_mul(T[c * XTP + r], l, T[c * XTP + j]);
     }
     __syncthreads();
   }
+  // bmax[j] = max over rows r > j of |d_rj|: warp w reduces columns w, w+8, ...
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = warp; j < n; j += 8) {
+    double mx = 0.0;
+    for (int rr = j + 1 + lane; rr < n; rr += 32) mx = fmax(mx, Dd[j * XTP + rr]);
+    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0 && mx > 0.0) atomic_max_nonneg(&bmax[j], mx);
+  }
+  __syncthreads();
 }
 
 // ---- smem staging -------------------------------------------------------------
@@ -287,28 +334,26 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
   const BlockDev A = P.blk[tk.a];
   Line X;
   switch (tk.type) {
-    case X_COLMAX: {
+    case X_COLMAX: {  // rows [r*COLMAX_ROWS, ...) of column tile c: atomic max into colmax
       const int m = A.nrows, c0 = tk.c * XT, nc = min(XT, m - c0);
+      const int rb = tk.r * COLMAX_ROWS, re = min(m, rb + COLMAX_ROWS);
       const double* G = P.vals + A.ent;
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+      unsigned long long* cmax = reinterpret_cast<unsigned long long*>(P.colmax) + A.dg;
       for (int c = c0 + warp; c < c0 + nc; c += nw) {
         const double* col = G + static_cast<size_t>(c) * m;
         double mx0 = 0.0, mx1 = 0.0, mx2 = 0.0, mx3 = 0.0;
-        int r = lane;
-        for (; r + 96 < m; r += 128) {
+        int r = rb + lane;
+        for (; r + 96 < re; r += 128) {
           mx0 = fmax(mx0, fabs(ldcg(col + r)));
           mx1 = fmax(mx1, fabs(ldcg(col + r + 32)));
           mx2 = fmax(mx2, fabs(ldcg(col + r + 64)));
           mx3 = fmax(mx3, fabs(ldcg(col + r + 96)));
         }
-        for (; r < m; r += 32) mx0 = fmax(mx0, fabs(ldcg(col + r)));
+        for (; r < re; r += 32) mx0 = fmax(mx0, fabs(ldcg(col + r)));
         double mx = fmax(fmax(mx0, mx1), fmax(mx2, mx3));
         for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        if (lane == 0) {
-          P.colmax[A.dg + c] = mx;
-          P.bmax[A.dg + c] = 0ull;
-          P.perm[A.dg + c] = c;
-        }
+        if (lane == 0 && mx > 0.0) atomic_max_nonneg(cmax + c, mx);
       }
       break;
     }
@@ -317,7 +362,7 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       double* G = P.vals + A.ent + static_cast<size_t>(k0) * m + k0;
       load_tile(T0, G, m, n, n);
       __syncthreads();
-      smem_lu(T0, n, P.bmax + A.dg + k0);
+      smem_lu(T0, n, P.bmax + A.dg + k0, T1);
       store_tile(G, m, T0, n, n);
       break;
     }
