@@ -130,15 +130,25 @@ __device__ __forceinline__ void col_store(double* G, int ld, const Line& L, int 
   }
 }
 
-// X (rows in registers, nc columns) <- X U^{-1}; U upper in smem (XTP stride).
-// rinv[j] = 1/u_jj precomputed (smem).  kCheck: per column max |x_rj| before
-// scaling, staged in smem cm[] (flushed by the caller).  The outer loop over
-// groups of 4 columns stays rolled (i-cache friendly); after each group the
-// registers shift down by one so the owner's value is always x[0].
+// The solves below keep a line's 16 entries in registers and loop over
+// elimination steps in rolled groups of 4 (i-cache friendly); after each group
+// the registers rotate down by one so the current step's entry is always x[0]
+// (static register indexing).  Every update loads its 16 operands first and
+// then issues 16 independent FMAs (ILP), masking with a select.
+__device__ __forceinline__ void line_rotate(Line& L) {
+  const double w = L.x[0];
+#pragma unroll
+  for (int i = 0; i < 15; ++i) L.x[i] = L.x[i + 1];
+  L.x[15] = w;
+}
+
+// X (rows in registers, nc columns) <- X U^{-1}; U upper in smem (XTP stride),
+// rinv[j] = 1/u_jj (smem).  kCheck: stage |x_rj| before scaling in Dd[j*XTP+r]
+// (reduced to the pivot check by the caller).
 template <bool kCheck>
-__device__ __forceinline__ void line_right_upper(Line& L, int nc, const double* U, const double* rinv,
-                                                 unsigned long long* cm) {
-  const int q = line_q(), lane = threadIdx.x & 31, base = lane & ~3;
+__device__ __forceinline__ void line_right_upper(Line& L, int nr, int nc, const double* U, const double* rinv,
+                                                 double* Dd) {
+  const int r = line_id(), q = line_q(), lane = threadIdx.x & 31, base = lane & ~3;
   const int ngroups = (nc + 3) >> 2;
 #pragma unroll 1
   for (int jb = 0; jb < ngroups; ++jb) {
@@ -149,37 +159,28 @@ __device__ __forceinline__ void line_right_upper(Line& L, int nc, const double* 
       double v = 0.0;
       if (q == jr) {
         const double d = L.x[0];
-        if (kCheck && d != 0.0)
-          atomicMax(&cm[j], static_cast<unsigned long long>(__double_as_longlong(fabs(d))));
+        if (kCheck) Dd[j * XTP + r] = r < nr ? fabs(d) : 0.0;
         v = d * rinv[j];
         L.x[0] = v;
       }
       const double xj = __shfl_sync(0xffffffffu, v, base | jr);
+      double u[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) u[i] = U[min(4 * (jb + i) + q, XT - 1) * XTP + j];
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        const int c = 4 * (jb + i) + q;  // column held in x[i] after jb shifts
-        if (c > j && c < nc) L.x[i] = dsub_mul(L.x[i], xj, U[c * XTP + j]);
+        const int c = 4 * (jb + i) + q;
+        const double nv = fma(-xj, u[i], L.x[i]);
+        L.x[i] = (c > j && c < nc) ? nv : L.x[i];
       }
     }
-    // retire x[0] (column 4*jb+q is final): park it at the end, shift the rest
-    const double done = L.x[0];
-#pragma unroll
-    for (int i = 0; i < 15; ++i) L.x[i] = L.x[i + 1];
-    L.x[15] = done;
+    line_rotate(L);
   }
-  // undo the rotation: x[15-t] holds column 4*(jb_done - 1 - t)+q ... restore natural order
-  // after ngroups rotations the array is rotated left by ngroups
 #pragma unroll 1
-  for (int t = ngroups; t < 16; ++t) {
-    const double w = L.x[0];
-#pragma unroll
-    for (int i = 0; i < 15; ++i) L.x[i] = L.x[i + 1];
-    L.x[15] = w;
-  }
+  for (int t = ngroups; t < 16; ++t) line_rotate(L);
 }
 
 // X (columns in registers, nr rows) <- L^{-1} X; L unit lower in smem (XTP stride).
-// Same rolled-group / register-rotation scheme as line_right_upper.
 __device__ __forceinline__ void line_left_unit_lower(Line& X, int nr, const double* Lm) {
   const int q = line_q(), lane = threadIdx.x & 31, base = lane & ~3;
   const int ngroups = (nr + 3) >> 2;
@@ -190,58 +191,83 @@ __device__ __forceinline__ void line_left_unit_lower(Line& X, int nr, const doub
       const int k = 4 * kb + kr;
       if (k >= nr) break;
       const double xk = __shfl_sync(0xffffffffu, X.x[0], base | kr);
+      double l[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) l[i] = Lm[k * XTP + min(4 * (kb + i) + q, XT - 1)];
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        const int r = 4 * (kb + i) + q;
-        if (r > k && r < nr) X.x[i] = dsub_mul(X.x[i], Lm[k * XTP + r], xk);
+        const int rr = 4 * (kb + i) + q;
+        const double nv = fma(-l[i], xk, X.x[i]);
+        X.x[i] = (rr > k && rr < nr) ? nv : X.x[i];
       }
     }
-    const double done = X.x[0];
-#pragma unroll
-    for (int i = 0; i < 15; ++i) X.x[i] = X.x[i + 1];
-    X.x[15] = done;
+    line_rotate(X);
   }
 #pragma unroll 1
-  for (int t = ngroups; t < 16; ++t) {
-    const double w = X.x[0];
-#pragma unroll
-    for (int i = 0; i < 15; ++i) X.x[i] = X.x[i + 1];
-    X.x[15] = w;
-  }
+  for (int t = ngroups; t < 16; ++t) line_rotate(X);
 }
 
-// LU without row exchange of the n x n tile in smem (XTP stride), one
-// barrier per elimination step.  Thread (r, q) updates row r, columns 4i+q;
-// the 4 lanes of a row compute l_rj redundantly (true division), the owner of
-// column j writes it back after a __syncwarp.  The pre-scaling values d_rj are
-// staged in Dd (smem) and reduced to bmax[j] = max_{r>j} |d_rj| after the loop.
-__device__ void smem_lu(double* T, int n, unsigned long long* bmax, double* Dd) {
-  const int r = line_id(), q = line_q();
+// LU without row exchange of an n x n tile held as rows in registers.  Step j:
+// the 4 threads of row j publish it (smem, double-buffered), one barrier, every
+// row r > j forms l_rj = d_rj * (1/u_jj) (owner lane, shuffled to its 3 peers)
+// and updates its 16 entries with independent FMAs.  |d_rj| before scaling is
+// staged in Dd for the pivot check.
+__device__ void line_lu(Line& R, int n, double* urow, double* Dd) {
+  const int r = line_id(), q = line_q(), lane = threadIdx.x & 31, base = lane & ~3;
+  const int ngroups = (n + 3) >> 2;
 #pragma unroll 1
-  for (int j = 0; j < n; ++j) {
-    const double u = T[j * XTP + j];
-    if (r > j && r < n) {
-      const double d = T[j * XTP + r];
-      const double l = __ddiv_rn(d, u);
-      __syncwarp(0xfu << (threadIdx.x & 28));
-      if (q == (j & 3)) {
-        T[j * XTP + r] = l;
-        Dd[j * XTP + r] = fabs(d);
+  for (int jb = 0; jb < ngroups; ++jb) {
+#pragma unroll
+    for (int jr = 0; jr < 4; ++jr) {
+      const int j = 4 * jb + jr;
+      if (j >= n) break;
+      double* ub = urow + (j & 1) * XT;
+      if (r == j) {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int c = 4 * (jb + i) + q;
+          if (c < XT) ub[c] = R.x[i];
+        }
       }
-#pragma unroll 1
-      for (int c = j + 1 + ((q - j - 1) & 3); c < n; c += 4) T[c * XTP + r] = dsub_mul(T[c * XTP + r], l, T[c * XTP + j]);
+      __syncthreads();
+      const double rinv = 1.0 / ub[j];
+      double v = 0.0;
+      const bool act = r > j && r < n;
+      if (q == jr && act) {
+        const double d = R.x[0];
+        Dd[j * XTP + r] = fabs(d);
+        v = d * rinv;
+        R.x[0] = v;
+      }
+      const double l = __shfl_sync(0xffffffffu, v, base | jr);
+      double u[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) u[i] = ub[min(4 * (jb + i) + q, XT - 1)];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int c = 4 * (jb + i) + q;
+        const double nv = fma(-l, u[i], R.x[i]);
+        R.x[i] = (act && c > j && c < n) ? nv : R.x[i];
+      }
     }
-    __syncthreads();
+    line_rotate(R);
   }
-  // bmax[j] = max over rows r > j of |d_rj|: warp w reduces columns w, w+8, ...
+#pragma unroll 1
+  for (int t = ngroups; t < 16; ++t) line_rotate(R);
+  __syncthreads();
+}
+
+// bmax[j] (global, bits) = max over rows r > j (r < nr) of the staged |d_rj|;
+// rows_all: the whole column is "below" (TRSM_L tiles).
+__device__ __forceinline__ void flush_colmax(const double* Dd, int nr, int nc, bool rows_all,
+                                             unsigned long long* bmax) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = warp; j < n; j += 8) {
+  for (int j = warp; j < nc; j += 8) {
     double mx = 0.0;
-    for (int rr = j + 1 + lane; rr < n; rr += 32) mx = fmax(mx, Dd[j * XTP + rr]);
+    for (int rr = (rows_all ? 0 : j + 1) + lane; rr < nr; rr += 32) mx = fmax(mx, Dd[j * XTP + rr]);
     for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if (lane == 0 && mx > 0.0) atomic_max_nonneg(&bmax[j], mx);
   }
-  __syncthreads();
 }
 
 // ---- smem staging -------------------------------------------------------------
@@ -360,10 +386,10 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
     case X_GETRF: {
       const int m = A.nrows, k0 = tk.k * XT, n = min(XT, m - k0);
       double* G = P.vals + A.ent + static_cast<size_t>(k0) * m + k0;
-      load_tile(T0, G, m, n, n);
-      __syncthreads();
-      smem_lu(T0, n, P.bmax + A.dg + k0, T1);
-      store_tile(G, m, T0, n, n);
+      row_load(X, G, m, n, n);
+      line_lu(X, n, rinv, T1);
+      row_store(G, m, X, n, n);
+      flush_colmax(T1, n, n, false, P.bmax + A.dg + k0);
       break;
     }
     case X_TRSM_L: {  // rows of tile (r,k) in registers, U_kk in smem
@@ -374,11 +400,10 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       __syncthreads();
       prep_right(T1, nk, rinv, cm);
       __syncthreads();
-      line_right_upper<true>(X, nk, T1, rinv, cm);
+      line_right_upper<true>(X, nr, nk, T1, rinv, T2);
       row_store(G, m, X, nr, nk);
       __syncthreads();
-      for (int c = threadIdx.x; c < nk; c += blockDim.x)
-        if (cm[c]) atomicMax(P.bmax + A.dg + k0 + c, cm[c]);
+      flush_colmax(T2, nr, nk, true, P.bmax + A.dg + k0);
       break;
     }
     case X_TRSM_U: {  // columns of tile (k,c) in registers, L_kk in smem
@@ -461,7 +486,7 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
         __syncthreads();
         prep_right(T1, nc, rinv, cm);
         __syncthreads();
-        line_right_upper<false>(X, nc, T1, rinv, cm);
+        line_right_upper<false>(X, nr, nc, T1, rinv, T2);
         row_store(G, ld, X, nr, nc);
       } else {
         const int k0 = tk.k * XT, nk = min(XT, A.nC - k0);
