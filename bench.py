@@ -197,7 +197,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--levels-out", default=None, help="write per-level device times + work to this .npz")
-    ap.add_argument("--dense-threshold", type=float, default=0.25,
+    ap.add_argument("--dense-threshold", type=float, default=0.1,
                     help="compressed-tile density tag for the FP64 DMMA kernels; <0 = CSC kernels only")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -35,7 +35,7 @@ DEFAULT_CHUNK = 8
 # compressed-tile tag: a block whose nonempty-rows x nonempty-columns rectangle
 # holds >= this fraction of entries runs on the DMMA kernels (the reference's
 # own dense tag is 0.5 of the FULL block, factorize.py:274)
-DEFAULT_DENSE_THRESHOLD = 0.25
+DEFAULT_DENSE_THRESHOLD = 0.1
 
 P = _native.ptr
 i64p, i32p, i8p, f64p = _native.c_i64p, _native.c_i32p, _native.c_i8p, _native.c_f64p
