@@ -812,21 +812,59 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           const int tr = (hb[xb].nR + XT - 1) / XT, tc = (hb[xb].nC + XT - 1) / XT;
           std::vector<int> last(static_cast<size_t>(tr) * tc, -1);
           auto L_ = [&](int r, int cc) -> int& { return last[static_cast<size_t>(cc) * tr + r]; };
+          // Tile occupancy from the filled patterns (tiled mode: no swaps, so the
+          // patterns are exact): occX = tiles of the panel that hold entries; occD
+          // = tiles of the diagonal factor gathered onto the panel's rows (GESSM:
+          // strict L over R_X x R_X) or columns (TSTRF: strict U over C_X x C_X).
+          // A panel tile outside the pattern stays zero through the solve (fill
+          // closure), and a zero factor tile contributes nothing.
+          const int nd = pt[0] == 1 ? tr : tc;
+          std::vector<char> occX(static_cast<size_t>(tr) * tc, all_full ? 1 : 0);
+          std::vector<char> occD(static_cast<size_t>(nd) * nd, all_full ? 1 : 0);
+          if (!all_full) {
+            const std::vector<int32_t> Rx = rows_of(xb), Cx = cols_of(xb);
+            std::vector<int32_t> rpos(hb[xb].nrows, -1), cpos(hb[xb].ncols, -1);
+            for (size_t a = 0; a < Rx.size(); ++a) rpos[Rx[a]] = static_cast<int32_t>(a);
+            for (size_t a = 0; a < Cx.size(); ++a) cpos[Cx[a]] = static_cast<int32_t>(a);
+            const int64_t* xcp = colptr + T_cp[xb];
+            const int64_t* xri = rowidx + T_ent[xb];
+            for (int col = 0; col < hb[xb].ncols; ++col)
+              for (int64_t e = xcp[col]; e < xcp[col + 1]; ++e)
+                occX[static_cast<size_t>(cpos[col] / XT) * tr + rpos[xri[e]] / XT] = 1;
+            const std::vector<int32_t>& pos = pt[0] == 1 ? rpos : cpos;
+            const int64_t* dcp = colptr + T_cp[dblk];
+            const int64_t* dri = rowidx + T_ent[dblk];
+            for (int col = 0; col < hb[dblk].ncols; ++col) {
+              const int pc = pos[col];
+              if (pc < 0) continue;
+              for (int64_t e = dcp[col]; e < dcp[col + 1]; ++e) {
+                const int64_t row = dri[e];
+                const bool keep = pt[0] == 1 ? row > col : row < col;
+                if (keep && pos[row] >= 0) occD[static_cast<size_t>(pc / XT) * nd + pos[row] / XT] = 1;
+              }
+            }
+          }
+          auto X_ = [&](int r, int cc) { return occX[static_cast<size_t>(cc) * tr + r] != 0; };
+          auto D_ = [&](int r, int cc) { return occD[static_cast<size_t>(cc) * nd + r] != 0; };
           if (pt[0] == 1) {  // GESSM: forward substitution down the row blocks
             for (int kb = 0; kb < tr; ++kb)
               for (int cc = 0; cc < tc; ++cc) {
+                if (!X_(kb, cc)) continue;
                 const int d = X.add(X_PG_DIAG, xb, dblk, kb, cc, kb, stp, kb * 4 + 1, {L_(kb, cc)});
                 L_(kb, cc) = d;
                 for (int r = kb + 1; r < tr; ++r)
-                  L_(r, cc) = X.add(X_PG_UPD, xb, dblk, r, cc, kb, stp, kb * 4 + 2, {d, L_(r, cc)});
+                  if (X_(r, cc) && D_(r, kb))  // L tile (r, kb)
+                    L_(r, cc) = X.add(X_PG_UPD, xb, dblk, r, cc, kb, stp, kb * 4 + 2, {d, L_(r, cc)});
               }
           } else {  // TSTRF: substitution along the column blocks
             for (int kb = 0; kb < tc; ++kb)
               for (int r = 0; r < tr; ++r) {
+                if (!X_(r, kb)) continue;
                 const int d = X.add(X_PT_DIAG, xb, dblk, r, kb, kb, stp, kb * 4 + 1, {L_(r, kb)});
                 L_(r, kb) = d;
                 for (int cc = kb + 1; cc < tc; ++cc)
-                  L_(r, cc) = X.add(X_PT_UPD, xb, dblk, r, cc, kb, stp, kb * 4 + 2, {d, L_(r, cc)});
+                  if (X_(r, cc) && D_(kb, cc))  // U tile (kb, cc)
+                    L_(r, cc) = X.add(X_PT_UPD, xb, dblk, r, cc, kb, stp, kb * 4 + 2, {d, L_(r, cc)});
               }
           }
         }

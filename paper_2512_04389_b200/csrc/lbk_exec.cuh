@@ -524,7 +524,6 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
   double* T1 = sm + XREG;           // operand tile (XTP stride) / DMMA A (XS stride)
   double* T2 = sm + 2 * XREG;       // DMMA B (XS stride)
   double* rinv = sm + 3 * XREG;     // XT doubles
-  unsigned long long* cm = reinterpret_cast<unsigned long long*>(sm + 3 * XREG + XT);  // XT
   const BlockDev A = P.blk[tk.a];
   Line X;
   switch (tk.type) {
