@@ -439,36 +439,46 @@ __device__ __forceinline__ void flush_colmax(const double* Dd, int nr, int nc, b
 }
 
 // ---- smem staging -------------------------------------------------------------
+// 64x64 tiles, 256 threads: thread owns row r = tid & 63 and columns (tid >> 6) + 4i,
+// i < 16.  All 16 loads are issued before the first smem store (one L2 round trip
+// per tile instead of one per element).
+constexpr int XTHREADS = 256;
+constexpr int XPER = XT * XT / XTHREADS;  // 16
+
+template <int STRIDE>
+__device__ __forceinline__ void stage_tile(double* T, const double* G, int ld, int nr, int nc,
+                                           const int32_t* rg, const int32_t* cg) {
+  const int r = threadIdx.x & (XT - 1), c0 = threadIdx.x >> 6;
+  const bool rok = r < nr;
+  const size_t roff = rok ? static_cast<size_t>(rg ? rg[r] : r) : 0;
+  int cix[XPER];
+#pragma unroll
+  for (int i = 0; i < XPER; ++i) {
+    const int c = c0 + 4 * i;
+    cix[i] = (c < nc) ? (cg ? cg[c] : c) : -1;
+  }
+  double v[XPER];
+#pragma unroll
+  for (int i = 0; i < XPER; ++i) v[i] = (rok && cix[i] >= 0) ? ldcg(G + static_cast<size_t>(cix[i]) * ld + roff) : 0.0;
+#pragma unroll
+  for (int i = 0; i < XPER; ++i) T[(c0 + 4 * i) * STRIDE + r] = v[i];
+}
+
 // (nr x nc) tile, column-major global (ld), optional row/column gathers -> smem T[c*XTP + r]
 __device__ __forceinline__ void load_tile(double* T, const double* G, int ld, int nr, int nc,
                                           const int32_t* rg = nullptr, const int32_t* cg = nullptr) {
-  for (int idx = threadIdx.x; idx < XT * XT; idx += blockDim.x) {
-    const int r = idx & (XT - 1), c = idx >> 6;
-    double v = 0.0;
-    if (r < nr && c < nc) v = ldcg(G + static_cast<size_t>(cg ? cg[c] : c) * ld + (rg ? rg[r] : r));
-    T[c * XTP + r] = v;
-  }
+  stage_tile<XTP>(T, G, ld, nr, nc, rg, cg);
 }
 
 // DMMA A operand ([k][r], stride XS) / B operand ([c][k], stride XS)
 __device__ __forceinline__ void load_opA(double* As, const double* G, int ld, int nr, int nk,
                                          const int32_t* rg = nullptr, const int32_t* kg = nullptr) {
-  for (int idx = threadIdx.x; idx < XT * XT; idx += blockDim.x) {
-    const int r = idx & (XT - 1), k = idx >> 6;
-    double v = 0.0;
-    if (r < nr && k < nk) v = ldcg(G + static_cast<size_t>(kg ? kg[k] : k) * ld + (rg ? rg[r] : r));
-    As[k * XS + r] = v;
-  }
+  stage_tile<XS>(As, G, ld, nr, nk, rg, kg);
 }
 
 __device__ __forceinline__ void load_opB(double* Bs, const double* G, int ld, int nk, int nc,
                                          const int32_t* kg = nullptr, const int32_t* cg = nullptr) {
-  for (int idx = threadIdx.x; idx < XT * XT; idx += blockDim.x) {
-    const int k = idx & (XT - 1), c = idx >> 6;
-    double v = 0.0;
-    if (k < nk && c < nc) v = ldcg(G + static_cast<size_t>(cg ? cg[c] : c) * ld + (kg ? kg[k] : k));
-    Bs[c * XS + k] = v;
-  }
+  stage_tile<XS>(Bs, G, ld, nk, nc, kg, cg);
 }
 
 // target tile (registers via smem T0) -= A * B on DMMA, 64x64x64, 8 warps of 32x16
@@ -505,9 +515,12 @@ __device__ void tile_mma_sub(double* Cs, const double* As, const double* Bs) {
 
 // C (smem, XTP stride) -> global, masked
 __device__ __forceinline__ void store_tile(double* G, int ld, const double* T, int nr, int nc) {
-  for (int idx = threadIdx.x; idx < XT * XT; idx += blockDim.x) {
-    const int r = idx & (XT - 1), c = idx >> 6;
-    if (r < nr && c < nc) G[static_cast<size_t>(c) * ld + r] = T[c * XTP + r];
+  const int r = threadIdx.x & (XT - 1), c0 = threadIdx.x >> 6;
+  if (r >= nr) return;
+#pragma unroll
+  for (int i = 0; i < XPER; ++i) {
+    const int c = c0 + 4 * i;
+    if (c < nc) G[static_cast<size_t>(c) * ld + r] = T[c * XTP + r];
   }
 }
 
