@@ -10,9 +10,13 @@ after geometric nested dissection, irregular blocking (p=174, 20,544 tasks,
 and every step starts by restoring A's values with a device copy, so no step
 sees a warm L2 from the previous one.
 
-Multi-GPU (--gpus N under torchrun): N independent replicas of the same
-factorization ("replicas only" in DESIGN.md — the 2D block-cyclic NCCL path
-is not part of this bench yet); timing = max over ranks.
+Multi-GPU (--gpus N under torchrun, NCCL): ONE factorization of the same
+matrix distributed 2D block-cyclically over the N GPUs (process grid 1x2 /
+2x2 / 2x4, owner-computes, finished diagonal and panel blocks exchanged
+between dependency levels with grouped NCCL point-to-point over NVLink;
+paper_2512_04389_b200/parallel.py DistEngine) — strong scaling, timing =
+max over ranks of the device time.  --replicas runs N independent copies
+instead (weak scaling).
 """
 
 from __future__ import annotations
@@ -120,14 +124,19 @@ def peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def dist_init():
+def dist_init(backend=None):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
+        import torch
         import torch.distributed as dist
 
-        dist.init_process_group("gloo")
+        if backend is None:
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
     return world, rank, local
 
 
@@ -145,6 +154,8 @@ def max_over_ranks(x: float, world: int) -> float:
     import torch.distributed as dist
 
     t = torch.tensor([x], dtype=torch.float64)
+    if dist.get_backend() == "nccl":
+        t = t.cuda()
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -157,7 +168,7 @@ def cpu_baseline_sample(g, t, flops_t, budget_s):
 
 
 def run_reference(args):
-    world, rank, _ = dist_init()
+    world, rank, _ = dist_init("gloo")
     if rank != 0:
         return 0
     a, f, g, t = build_case(args.config)
@@ -177,7 +188,7 @@ def run_reference(args):
               f"{r['tasks']}/{r['total_tasks']} tasks, {r['flops'] / 1e9:.3f} GFLOP in {r['seconds']:.1f}s per step")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "plan": "irregular", "n": a.n, "nnz_filled": f.nnz_filled},
             "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cores, "blas_threads": blas,
                              "cpu": model, "kind": "port", "sample": sample},
@@ -199,11 +210,17 @@ def main():
     ap.add_argument("--levels-out", default=None, help="write per-level device times + work to this .npz")
     ap.add_argument("--dense-threshold", type=float, default=0.1,
                     help="compressed-tile density tag for the FP64 DMMA kernels; <0 = CSC kernels only")
+    ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of 2D block-cyclic")
+    ap.add_argument("--dist-backend", default=None, help="nccl (default with CUDA) | gloo (host-staged, 1-GPU tests)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
 
-    world, rank, local = dist_init()
+    world, rank, local = dist_init(args.dist_backend)
+    import torch
+
+    if torch.cuda.is_available():
+        local = local % torch.cuda.device_count()  # several ranks may share a GPU in gloo tests
     import paper_2512_04389_b200 as M  # noqa: F401
     from paper_2512_04389_b200.numeric import Engine, pinned_empty
     from paper_2512_04389_b200.workmodel import task_work
@@ -213,7 +230,28 @@ def main():
     total_flops = float(flops_t.sum())
     t0 = time.perf_counter()
     dt = None if args.dense_threshold < 0 else args.dense_threshold
-    eng = Engine(g, t, device=local, dense_threshold=dt, dense_kernels=dt is not None)
+    distributed = world > 1 and not args.replicas
+    if distributed:
+        from paper_2512_04389_b200.parallel import DistEngine
+
+        de = DistEngine(g, t, device=local, dense_threshold=dt)
+        eng = de.eng
+
+        def run_dev():
+            ms_, st_ = de.run()
+            if st_.code:
+                raise SystemExit(f"distributed factorization failed: {st_.code}")
+            return ms_
+
+        def run_host(vi, vo, pv):
+            return de.run_host(vi, vo, pv)
+
+        log(f"[bench] rank {rank}: grid {de.pg.pr}x{de.pg.pc}, {eng.n_segments} segments, {de.messages} messages, "
+            f"{de.bytes_out / 1e9:.2f} GB sent per factorization")
+    else:
+        eng = Engine(g, t, device=local, dense_threshold=dt, dense_kernels=dt is not None)
+        run_dev = eng.run_device
+        run_host = eng.run_host
     eng.upload()
     log(f"[bench] plan: {eng.n_launch_levels} levels, {eng.n_launches} launches, {eng.n_items} CSC items, "
         f"{eng.n_gemm_tiles} DMMA tiles, {eng.n_dense_items} panel items, {eng.n_tile_items} tiled-GETRF items; "
@@ -221,13 +259,14 @@ def main():
         f"working entries {eng.nnz_work / 1e6:.1f}M vs {eng.nnz / 1e6:.1f}M; {time.perf_counter() - t0:.1f}s")
 
     for _ in range(max(args.warmup, 0)):
-        eng.run_device()
+        run_dev()
     barrier(world)
     with ClockSampler(local) as clk:
-        ms = [eng.run_device() for _ in range(args.steps)]
+        ms = [run_dev() for _ in range(args.steps)]
     barrier(world)
     t_step = max_over_ranks(sum(ms) / len(ms), world)
-    value = world * total_flops / (t_step / 1e3) / 1e9
+    jobs = 1 if distributed else world  # factorizations per step over the whole job
+    value = jobs * total_flops / (t_step / 1e3) / 1e9
 
     # end to end: pinned host values in, host factor values out, through the C-ABI
     vin = pinned_empty(eng.nnz)
@@ -235,18 +274,19 @@ def main():
     vout = pinned_empty(eng.nnz)
     perms = np.empty(max(eng.n_diag_rows, 1), np.int32)
     ke = args.e2e_steps or max(1, min(args.steps, 3))
-    eng.run_host(vin, vout, perms)
+    run_host(vin, vout, perms)
     barrier(world)
     t0 = time.perf_counter()
     for _ in range(ke):
-        st = eng.run_host(vin, vout, perms)
+        st = run_host(vin, vout, perms)
         if st.code:
             raise SystemExit(f"e2e factorization failed: {st.code}")
     e2e_s = max_over_ranks((time.perf_counter() - t0) / ke, world)
-    e2e_value = world * total_flops / e2e_s / 1e9
+    e2e_value = jobs * total_flops / e2e_s / 1e9
 
     # per-level / per-kernel-family device times (instrumented replay) -> roofline
-    lvl = eng.level_times()  # [levels x 5]: level, DMMA SSSSM, panel, tiled GETRF, CSC kernel
+    # (distributed: this rank's own tasks, replayed without the exchanges: timing only)
+    lvl = eng.level_times(check=not distributed)  # [levels x 5]: level, DMMA SSSSM, panel, tiled GETRF, CSC
     routes = eng.task_routes()
     fam_names = {1: "gemm_map_kernel (DMMA SSSSM)", 2: "panel_kernel (DMMA GESSM/TSTRF)",
                  3: "tiled GETRF (tile_getrf/trsm/gemm)", 0: "level_kernel (CSC SSSSM/GESSM/TSTRF)"}
@@ -313,12 +353,14 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": t_step, "higher_is_better": True,
+            "scaling": "strong" if distributed else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "matrix": "3D 7-point Poisson 64^3, geometric ND" if args.config == "C2"
                        else args.config, "plan": "irregular", "n": a.n, "nnz_A": a.nnz, "nnz_filled": f.nnz_filled,
                        "p": g.p, "tasks": t.task_count, "levels": t.n_levels, "gflop": total_flops / 1e9,
-                       "parallelism": f"replicas{world}" if world > 1 else "single",
+                       "parallelism": (f"2d-block-cyclic {de.pg.pr}x{de.pg.pc} (NCCL p2p)" if distributed
+                                       else f"replicas{world}" if world > 1 else "single"),
                        "l2": "inputs (factor values, %.2f GB) larger than L2; values restored by a device copy "
                              "before every step" % (8 * eng.nnz / 1e9)},
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "seconds_per_step": e2e_s,
@@ -332,6 +374,9 @@ def main():
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": int(args.steps * eng.n_launches),
+            "exchange": ({"segments": eng.n_segments, "messages_rank0": de.messages,
+                          "bytes_sent_rank0": de.bytes_out,
+                          "roofline_scope": "rank 0's own tasks"} if distributed else None),
         }
         print(json.dumps(line), flush=True)
     eng.close()

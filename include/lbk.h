@@ -174,6 +174,32 @@ int lbk_level_times(lbk_ctx* ctx, double pivot_tol, double static_eps, float* ou
 int lbk_exec_trace(lbk_ctx* ctx, double pivot_tol, double static_eps, uint64_t* trace, int32_t* info,
                    int64_t* n, lbk_status* st);
 
+/* ---- 2D block-cyclic distribution (north-star subsystem 5; no reference
+ * counterpart: SPEC.md:14 scopes multi-process mapping out).  Owner-computes:
+ * each rank plans only the tasks whose written block it owns
+ * (paper_2512_04389_b200/parallel.py task_owners) and the graph is cut into
+ * segments after the tree levels whose finished blocks other ranks read; the
+ * host moves those blocks between segments (NCCL point-to-point on the
+ * ctx stream) and then launches the next segment.  Both calls precede lbk_plan. */
+int lbk_set_task_mask(lbk_ctx* ctx, int64_t ntasks, const int8_t* mask, lbk_status* st);
+int lbk_set_cuts(lbk_ctx* ctx, int64_t nlevels, const int8_t* cut_after, lbk_status* st);
+int lbk_num_segments(lbk_ctx* ctx);
+/* Enqueue segment `seg` on the ctx stream (asynchronous; seg 0 also zeroes and
+ * scatters, the last one gathers into the output pool). */
+int lbk_run_segment(lbk_ctx* ctx, int32_t seg, double pivot_tol, double static_eps, lbk_status* st);
+/* Synchronize; *ms = device time from segment 0 to the last segment;
+ * err2 = the raw (block << 32 | col) words of a zero pivot / needed row swap
+ * (~0 = none), to be min-reduced across ranks and decoded by lbk_status_from_err. */
+int lbk_finish_raw(lbk_ctx* ctx, float* ms, uint64_t* err2, lbk_status* st);
+int lbk_status_from_err(const uint64_t* err2, lbk_status* st);
+/* The ctx stream (cudaStream_t) and device pointers of the working pool, the
+ * per-diagonal-row permutations and the output pool, for the block exchange. */
+void* lbk_stream(lbk_ctx* ctx);
+int lbk_work_ptrs(lbk_ctx* ctx, void** vals, void** perm, void** vout);
+/* layout[3 x nblocks]: working-pool offset, working entries, diagonal-row
+ * offset (-1 for off-diagonal blocks), in pool block order. */
+int lbk_block_layout(lbk_ctx* ctx, int64_t* layout);
+
 /* Launched-level table (4 x nlevels: item offset, items, warps, acc length)
  * and, if items != NULL, the work items (6 x total: kind, a, b, c, begin, end). */
 int lbk_plan_levels(lbk_ctx* ctx, int64_t* levels, int32_t* items);

@@ -83,6 +83,7 @@ struct Level {
   int32_t ntfin;
   int64_t exec_off, sptr_off, succ_off;  // persistent tile-DAG executor (tiled mode)
   int32_t nexec;
+  int32_t tree_level;  // ASAP level of the task DAG this launch level runs
 };
 
 constexpr int NBRANCH = 3;
@@ -145,7 +146,7 @@ struct lbk_ctx {
   cudaStream_t aux[NBRANCH] = {nullptr, nullptr, nullptr};
   cudaEvent_t fork = nullptr, join[NBRANCH] = {nullptr, nullptr, nullptr};
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  cudaGraphExec_t graph = nullptr;
+  std::vector<cudaGraphExec_t> graphs;  // one per segment (see lbk_set_cuts)
   double g_tol = NAN, g_eps = NAN;
   int32_t flags = 0;
   // plan
@@ -174,6 +175,12 @@ struct lbk_ctx {
   DevBuf<int32_t> perm0;  // identity permutation per diagonal row
   int64_t n_exec = 0;
   bool use_exec = true;
+  // distribution (lbk_set_task_mask / lbk_set_cuts): tasks this rank runs, and
+  // the tree levels after which the graph is cut for a block exchange
+  std::vector<int8_t> mask, cut_after;
+  std::vector<int32_t> seg_begin;  // launch-level index where each segment starts (+ end sentinel)
+  std::vector<int64_t> wlen;       // working entries per block
+  std::vector<char> isdiag;
   DevBuf<unsigned long long> xtrace;  // executor task timeline (instrumented replays only)
 };
 
@@ -233,6 +240,12 @@ DevPools pools(lbk_ctx* c) {
   return P;
 }
 
+void drop_graphs(lbk_ctx* c) {
+  for (auto g : c->graphs)
+    if (g) cudaGraphExecDestroy(g);
+  c->graphs.clear();
+}
+
 int choose_warps(int acc_len) { return std::max(1, std::min(4, MAX_SMEM / (acc_len * 8))); }
 
 // positions of `sub` inside sorted `sup` (-1 if absent); identity flag
@@ -288,7 +301,8 @@ int lbk_create(lbk_ctx** out, int device, lbk_status* st) {
 void lbk_destroy(lbk_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  if (c->graph) cudaGraphExecDestroy(c->graph);
+  for (auto g : c->graphs)
+    if (g) cudaGraphExecDestroy(g);
   if (c->ev0) cudaEventDestroy(c->ev0);
   if (c->ev1) cudaEventDestroy(c->ev1);
   for (int k = 0; k < NBRANCH; ++k) {
@@ -327,6 +341,11 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
   try {
     // ---- storage kind, R / C lists ------------------------------------------------
     std::vector<BlockDev> hb(nb);
+    c->wlen.assign(nb, 0);
+    c->isdiag.assign(nb, 0);
+    for (int64_t b = 0; b < nb; ++b) c->isdiag[b] = T_bi[b] == T_bj[b];
+    if (!c->mask.empty() && static_cast<int64_t>(c->mask.size()) != ntasks)
+      return fail(st, LBK_ERR_DIM_MISMATCH, "task mask length differs from the task count");
     std::vector<std::vector<int32_t>> Rl(nb), Cl(nb);
     int64_t nnz = 0, nnz_w = 0, ncp = 0;
     for (int64_t b = 0; b < nb; ++b) {
@@ -373,6 +392,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       }
       d.cp = ncp;
       d.ent = nnz_w;
+      c->wlen[b] = store == STORE_SPARSE ? nzb : static_cast<int64_t>(d.nR) * d.nC;
       ncp += d.ncols + 1;
       nnz_w += store == STORE_SPARSE ? nzb : static_cast<int64_t>(d.nR) * d.nC;
       c->store_count[store]++;
@@ -528,6 +548,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     };
     auto tile_like = [&](int64_t b) { return hb[b].store != STORE_SPARSE; };
     for (int64_t t = 0; t < ntasks; ++t) {
+      if (!c->mask.empty() && !c->mask[t]) continue;  // another rank's task (owner-computes)
       const int kind = kinds[t];
       const int64_t i = steps[t], r = trows[t], cc = tcols[t];
       const int32_t lv = tlevels[t];
@@ -666,6 +687,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       if (static_cast<int64_t>(acc_len[lv]) * 8 > MAX_SMEM || pan_smem[lv] > MAX_SMEM || exa_smem[lv] > MAX_SMEM)
         return fail(st, LBK_ERR_BAD_ARG, "block span too large for the shared-memory accumulator");
       Level L{};
+      L.tree_level = lv;
       L.item_off = static_cast<int64_t>(gall.size());
       L.nitems = static_cast<int32_t>(gen[lv].size());
       L.acc_len = acc_len[lv];
@@ -920,10 +942,19 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
   } catch (const std::bad_alloc&) {
     return fail(st, LBK_ERR_OOM, "host allocation in lbk_plan");
   }
-  if (c->graph) {
-    cudaGraphExecDestroy(c->graph);
-    c->graph = nullptr;
+  // graph segments: segment s runs the launch levels whose tree level lies in
+  // (cut_{s-1}, cut_s]; a rank exchanges blocks between segments
+  c->seg_begin.assign(1, 0);
+  {
+    size_t l = 0;
+    for (size_t tl = 0; tl < c->cut_after.size(); ++tl) {
+      if (!c->cut_after[tl]) continue;
+      while (l < c->levels.size() && c->levels[l].tree_level <= static_cast<int32_t>(tl)) ++l;
+      c->seg_begin.push_back(static_cast<int32_t>(l));
+    }
+    c->seg_begin.push_back(static_cast<int32_t>(c->levels.size()));
   }
+  drop_graphs(c);
   ok(st);
   return 0;
 }
@@ -943,14 +974,18 @@ namespace {
 
 // Capture one full factorization into the current capture of c->stream.
 // With `evs`, an external (timing-capable) event record node closes each level.
-void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std::vector<cudaEvent_t>* evs) {
+// Launch levels [lo, hi) only; the prologue (zero, scatter, counter reset)
+// belongs to the first segment and the gather to the last one.
+void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std::vector<cudaEvent_t>* evs,
+                           size_t lo, size_t hi, bool first, bool last) {
   DevPools P = pools(c);
   cudaStream_t s0 = c->stream;
   const bool exact = (c->flags & 2) != 0 || !std::isnan(static_eps);
+  const bool use_exec = !exact && c->use_exec;
+  if (first) {
   cudaMemsetAsync(c->err.p, 0xff, 2 * sizeof(unsigned long long), s0);
   cudaMemsetAsync(c->vals.p, 0, c->nnz_work * sizeof(double), s0);
   scatter_kernel<<<148 * 8, 256, 0, s0>>>(c->vin.p, c->map.p, c->vals.p, c->nnz);
-  const bool use_exec = !exact && c->use_exec;
   if (use_exec && c->n_exec) {
     cudaMemcpyAsync(c->xdeps.p, c->xdeps0.p, c->n_exec * sizeof(int), cudaMemcpyDeviceToDevice, s0);
     cudaMemsetAsync(c->xheads.p, 0, c->levels.size() * sizeof(int), s0);
@@ -960,8 +995,9 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
       cudaMemcpyAsync(c->perm.p, c->perm0.p, c->ndiag_rows * sizeof(int32_t), cudaMemcpyDeviceToDevice, s0);
     }
   }
-  if (evs) cudaEventRecordWithFlags((*evs)[0], s0, cudaEventRecordExternal);
-  for (size_t l = 0; l < c->levels.size(); ++l) {
+  }
+  if (evs && first) cudaEventRecordWithFlags((*evs)[0], s0, cudaEventRecordExternal);
+  for (size_t l = lo; l < hi; ++l) {
     const Level& L = c->levels[l];
     const bool has_t = !exact && (use_exec ? L.nexec > 0 : L.ntcol > 0);
     const bool br[NBRANCH] = {L.ngemm > 0, (!use_exec && L.npanel > 0) || (exact && L.nexact > 0), has_t};
@@ -1028,40 +1064,55 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
       if (br[k]) cudaStreamWaitEvent(s0, c->join[k], 0);
     rec(0, s0);
   }
-  gather_kernel<<<148 * 8, 256, 0, s0>>>(c->vals.p, c->map.p, c->vout.p, c->nnz);
+  if (last) gather_kernel<<<148 * 8, 256, 0, s0>>>(c->vals.p, c->map.p, c->vout.p, c->nnz);
 }
+
+int nsegments(const lbk_ctx* c) { return static_cast<int>(c->seg_begin.size()) - 1; }
 
 bool same(double a, double b) { return a == b || (std::isnan(a) && std::isnan(b)); }
 
 int build_graph(lbk_ctx* c, double pivot_tol, double static_eps, lbk_status* st) {
-  if (c->graph && same(c->g_tol, pivot_tol) && same(c->g_eps, static_eps)) return 0;
-  if (c->graph) {
-    cudaGraphExecDestroy(c->graph);
-    c->graph = nullptr;
-  }
-  cudaGraph_t g;
-  LBK_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), st);
-  (void)cudaGetLastError();
-  capture_factorization(c, pivot_tol, static_eps, nullptr);
-  cudaError_t e = cudaStreamEndCapture(c->stream, &g);
-  if (e != cudaSuccess) return cuda_fail(st, e, "graph capture");
-  e = cudaGetLastError();  // a launch rejected during capture (bad configuration)
-  if (e != cudaSuccess) {
+  const int ns = nsegments(c);
+  if (static_cast<int>(c->graphs.size()) == ns && same(c->g_tol, pivot_tol) && same(c->g_eps, static_eps)) return 0;
+  drop_graphs(c);
+  for (int s = 0; s < ns; ++s) {
+    cudaGraph_t g;
+    LBK_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), st);
+    (void)cudaGetLastError();
+    capture_factorization(c, pivot_tol, static_eps, nullptr, c->seg_begin[s], c->seg_begin[s + 1], s == 0,
+                          s == ns - 1);
+    cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+    if (e != cudaSuccess) return cuda_fail(st, e, "graph capture");
+    e = cudaGetLastError();  // a launch rejected during capture (bad configuration)
+    if (e != cudaSuccess) {
+      cudaGraphDestroy(g);
+      return cuda_fail(st, e, "kernel launch during capture");
+    }
+    size_t nodes = 0;
+    cudaGraphGetNodes(g, nullptr, &nodes);
+    cudaGraphExec_t ge = nullptr;
+    if (nodes) e = cudaGraphInstantiate(&ge, g, 0);
     cudaGraphDestroy(g);
-    return cuda_fail(st, e, "kernel launch during capture");
+    if (e != cudaSuccess) return cuda_fail(st, e, "graph instantiate");
+    c->graphs.push_back(ge);  // nullptr: nothing for this rank in the segment
   }
-  e = cudaGraphInstantiate(&c->graph, g, 0);
-  cudaGraphDestroy(g);
-  if (e != cudaSuccess) return cuda_fail(st, e, "graph instantiate");
   c->g_tol = pivot_tol;
   c->g_eps = static_eps;
   return 0;
 }
 
-int finish(lbk_ctx* c, lbk_status* st) {
-  unsigned long long h[2];
-  LBK_CUDA(cudaMemcpyAsync(h, c->err.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream), st);
-  LBK_CUDA(cudaStreamSynchronize(c->stream), st);
+cudaError_t launch_all(lbk_ctx* c) {
+  for (auto g : c->graphs)
+    if (g) {
+      const cudaError_t e = cudaGraphLaunch(g, c->stream);
+      if (e != cudaSuccess) return e;
+    }
+  return cudaSuccess;
+}
+
+// Status from the two error words (lowest failing (block << 32 | col) of a
+// zero pivot / of a needed row swap; ~0 = none).
+int status_from_err(const unsigned long long* h, lbk_status* st) {
   const unsigned long long none = ~0ull;
   ok(st);
   if (h[0] != none && (h[1] == none || h[0] < h[1])) {
@@ -1081,6 +1132,13 @@ int finish(lbk_ctx* c, lbk_status* st) {
   return 0;
 }
 
+int finish(lbk_ctx* c, lbk_status* st) {
+  unsigned long long h[2];
+  LBK_CUDA(cudaMemcpyAsync(h, c->err.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream), st);
+  LBK_CUDA(cudaStreamSynchronize(c->stream), st);
+  return status_from_err(h, st);
+}
+
 }  // namespace
 
 extern "C" {
@@ -1091,7 +1149,7 @@ int lbk_factorize(lbk_ctx* c, double pivot_tol, double static_eps, float* ms, lb
   LBK_CUDA(cudaSetDevice(c->device), st);
   if (build_graph(c, pivot_tol, static_eps, st)) return st->code;
   LBK_CUDA(cudaEventRecord(c->ev0, c->stream), st);
-  LBK_CUDA(cudaGraphLaunch(c->graph, c->stream), st);
+  LBK_CUDA(launch_all(c), st);
   LBK_CUDA(cudaEventRecord(c->ev1, c->stream), st);
   const int rc = finish(c, st);
   if (rc == LBK_ERR_CUDA || rc == LBK_ERR_OOM) return rc;
@@ -1110,12 +1168,84 @@ int lbk_factorize_host(lbk_ctx* c, const double* a_values, double* lu_values, in
   LBK_CUDA(cudaSetDevice(c->device), st);
   if (build_graph(c, pivot_tol, static_eps, st)) return st->code;
   LBK_CUDA(cudaMemcpyAsync(c->vin.p, a_values, c->nnz * sizeof(double), cudaMemcpyHostToDevice, c->stream), st);
-  LBK_CUDA(cudaGraphLaunch(c->graph, c->stream), st);
+  LBK_CUDA(launch_all(c), st);
   LBK_CUDA(cudaMemcpyAsync(lu_values, c->vout.p, c->nnz * sizeof(double), cudaMemcpyDeviceToHost, c->stream), st);
   if (perms && c->ndiag_rows)
     LBK_CUDA(cudaMemcpyAsync(perms, c->perm.p, c->ndiag_rows * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream),
              st);
   return finish(c, st);
+}
+
+// ---- distribution hooks (2D block-cyclic owner-computes, paper_2512_04389_b200/parallel.py) ----
+
+int lbk_set_task_mask(lbk_ctx* c, int64_t ntasks, const int8_t* mask, lbk_status* st) {
+  if (!c) return fail(st, LBK_ERR_BAD_ARG, "null ctx");
+  if (mask) c->mask.assign(mask, mask + ntasks);
+  else c->mask.clear();
+  ok(st);
+  return 0;
+}
+
+int lbk_set_cuts(lbk_ctx* c, int64_t nlevels, const int8_t* cut_after, lbk_status* st) {
+  if (!c) return fail(st, LBK_ERR_BAD_ARG, "null ctx");
+  if (cut_after) c->cut_after.assign(cut_after, cut_after + nlevels);
+  else c->cut_after.clear();
+  ok(st);
+  return 0;
+}
+
+int lbk_num_segments(lbk_ctx* c) { return c ? nsegments(c) : 0; }
+
+int lbk_run_segment(lbk_ctx* c, int32_t seg, double pivot_tol, double static_eps, lbk_status* st) {
+  LBK_CUDA(cudaSetDevice(c->device), st);
+  if (seg < 0 || seg >= nsegments(c)) return fail(st, LBK_ERR_BAD_ARG, "segment out of range");
+  if (build_graph(c, pivot_tol, static_eps, st)) return st->code;
+  if (seg == 0) LBK_CUDA(cudaEventRecord(c->ev0, c->stream), st);
+  if (c->graphs[seg]) LBK_CUDA(cudaGraphLaunch(c->graphs[seg], c->stream), st);
+  if (seg == nsegments(c) - 1) LBK_CUDA(cudaEventRecord(c->ev1, c->stream), st);
+  ok(st);
+  return 0;
+}
+
+int lbk_finish_raw(lbk_ctx* c, float* ms, uint64_t* err2, lbk_status* st) {
+  LBK_CUDA(cudaSetDevice(c->device), st);
+  unsigned long long h[2];
+  LBK_CUDA(cudaMemcpyAsync(h, c->err.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream), st);
+  LBK_CUDA(cudaStreamSynchronize(c->stream), st);
+  err2[0] = h[0];
+  err2[1] = h[1];
+  if (ms) {
+    float t = 0;
+    cudaEventElapsedTime(&t, c->ev0, c->ev1);
+    *ms = t;
+  }
+  ok(st);
+  return 0;
+}
+
+int lbk_status_from_err(const uint64_t* err2, lbk_status* st) {
+  const unsigned long long h[2] = {err2[0], err2[1]};
+  return status_from_err(h, st);
+}
+
+void* lbk_stream(lbk_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+int lbk_work_ptrs(lbk_ctx* c, void** vals, void** perm, void** vout) {
+  if (vals) *vals = c->vals.p;
+  if (perm) *perm = c->perm.p;
+  if (vout) *vout = c->vout.p;
+  return 0;
+}
+
+// layout[3 x nblocks]: working-pool offset, working entries, diagonal-row offset (-1 off-diagonal)
+int lbk_block_layout(lbk_ctx* c, int64_t* layout) {
+  const int64_t nb = static_cast<int64_t>(c->hblk.size());
+  for (int64_t b = 0; b < nb; ++b) {
+    layout[b] = c->hblk[b].ent;
+    layout[nb + b] = c->wlen[b];
+    layout[2 * nb + b] = c->isdiag[b] ? c->hblk[b].dg : -1;
+  }
+  return 0;
 }
 
 int lbk_download(lbk_ctx* c, double* lu_values, int32_t* perms, lbk_status* st) {
@@ -1170,7 +1300,7 @@ int lbk_level_times(lbk_ctx* c, double pivot_tol, double static_eps, float* out_
   cudaGraph_t g;
   cudaGraphExec_t ge = nullptr;
   LBK_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), st);
-  capture_factorization(c, pivot_tol, static_eps, &ev);
+  capture_factorization(c, pivot_tol, static_eps, &ev, 0, nl, true, true);
   LBK_CUDA(cudaStreamEndCapture(c->stream, &g), st);
   cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
   cudaGraphDestroy(g);

@@ -72,6 +72,15 @@ def _dev():
     d(lib, "lbk_download_work", C.c_int, [vp, f64p, i64p, st])
     d(lib, "lbk_exec_trace", C.c_int, [vp, C.c_double, C.c_double, C.POINTER(C.c_uint64), i32p, i64p, st])
     d(lib, "lbk_plan_levels", C.c_int, [vp, i64p, i32p])
+    d(lib, "lbk_set_task_mask", C.c_int, [vp, C.c_int64, i8p, st])
+    d(lib, "lbk_set_cuts", C.c_int, [vp, C.c_int64, i8p, st])
+    d(lib, "lbk_num_segments", C.c_int, [vp])
+    d(lib, "lbk_run_segment", C.c_int, [vp, C.c_int32, C.c_double, C.c_double, st])
+    d(lib, "lbk_finish_raw", C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(C.c_uint64), st])
+    d(lib, "lbk_status_from_err", C.c_int, [C.POINTER(C.c_uint64), st])
+    d(lib, "lbk_stream", vp, [vp])
+    d(lib, "lbk_work_ptrs", C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)])
+    d(lib, "lbk_block_layout", C.c_int, [vp, i64p])
     _native._dev = lib
     return lib
 
@@ -122,10 +131,13 @@ class Engine:
 
     def __init__(self, grid, tree, *, device: int = 0, chunk: int = DEFAULT_CHUNK, pool: GridPool | None = None,
                  dense: bool = False, dense_threshold: float | None = DEFAULT_DENSE_THRESHOLD,
-                 dense_kernels: bool = True):
+                 dense_kernels: bool = True, mask: np.ndarray | None = None, cuts: np.ndarray | None = None):
         """dense=True: dense-scratch mode (every block a full tile, true row swaps).
         dense_threshold: tau of the compressed-tile tag (see include/lbk.h lbk_plan);
-        None / dense_kernels=False keeps every block CSC (sparse kernels only)."""
+        None / dense_kernels=False keeps every block CSC (sparse kernels only).
+        mask (int8 per task) / cuts (int8 per tree level): distributed plans
+        (parallel.DistEngine) — run only the masked tasks, and split the graph
+        into segments after the cut levels."""
         self.lib = _dev()
         self.grid = grid
         self.tree = tree
@@ -139,6 +151,14 @@ class Engine:
         if rc:
             _native.raise_status(st, "lbk_create")
         self.ctx = ctx
+        if mask is not None:
+            mk = np.ascontiguousarray(mask, dtype=np.int8)
+            if self.lib.lbk_set_task_mask(ctx, len(mk), P(mk, i8p), C.byref(st)):
+                _native.raise_status(st, "lbk_set_task_mask")
+        if cuts is not None:
+            ct = np.ascontiguousarray(cuts, dtype=np.int8)
+            if self.lib.lbk_set_cuts(ctx, len(ct), P(ct, i8p), C.byref(st)):
+                _native.raise_status(st, "lbk_set_cuts")
         pos = np.ascontiguousarray(grid.plan.positions, dtype=np.int64)
         pl = self.pool
         self._keep = [np.ascontiguousarray(pl.table, dtype=np.int64),
@@ -223,16 +243,62 @@ class Engine:
                                     pivot_tol, self._eps(static_pivot, self.grid.value_max), C.byref(st))
         return st
 
-    def level_times(self, pivot_tol=DEFAULT_PIVOT_TOL, static_pivot=None) -> np.ndarray:
+    def level_times(self, pivot_tol=DEFAULT_PIVOT_TOL, static_pivot=None, check=True) -> np.ndarray:
         """[levels x 5] device ms from one instrumented replay: level, DMMA SSSSM,
-        panel solves, tiled GETRF, CSC kernel."""
+        panel solves, tiled GETRF, CSC kernel.  check=False: timing only (a
+        distributed plan replayed without its exchanges computes garbage)."""
         if not self._resident:
             self.upload()
         out = np.zeros((self.n_launch_levels, 5), np.float32)
         st = _native.LbkStatus()
         self.lib.lbk_level_times(self.ctx, pivot_tol, self._eps(static_pivot, self.grid.value_max),
                                  out.ctypes.data_as(C.POINTER(C.c_float)), C.byref(st))
-        _native.raise_status(st, "lbk_level_times")
+        if check or st.code in (_native.LBK_ERR_CUDA, _native.LBK_ERR_OOM):
+            _native.raise_status(st, "lbk_level_times")
+        return out
+
+    # ---- segment-wise execution (distributed plans) ----
+
+    @property
+    def n_segments(self) -> int:
+        return int(self.lib.lbk_num_segments(self.ctx))
+
+    def run_segment(self, seg: int, pivot_tol=DEFAULT_PIVOT_TOL, static_pivot=None) -> None:
+        """Enqueue graph segment `seg` on the engine stream (asynchronous)."""
+        st = _native.LbkStatus()
+        if self.lib.lbk_run_segment(self.ctx, int(seg), pivot_tol, self._eps(static_pivot, self.grid.value_max),
+                                    C.byref(st)):
+            _native.raise_status(st, "lbk_run_segment")
+
+    def finish_raw(self):
+        """Synchronize; (device ms of segments 0..last, raw error words uint64[2])."""
+        ms = C.c_float()
+        err = (C.c_uint64 * 2)()
+        st = _native.LbkStatus()
+        if self.lib.lbk_finish_raw(self.ctx, C.byref(ms), err, C.byref(st)):
+            _native.raise_status(st, "lbk_finish_raw")
+        return float(ms.value), np.array([err[0], err[1]], np.uint64)
+
+    def status_from_err(self, err) -> "_native.LbkStatus":
+        e = (C.c_uint64 * 2)(int(err[0]), int(err[1]))
+        st = _native.LbkStatus()
+        self.lib.lbk_status_from_err(e, C.byref(st))
+        return st
+
+    @property
+    def stream_ptr(self) -> int:
+        return int(self.lib.lbk_stream(self.ctx) or 0)
+
+    def work_ptrs(self):
+        """Device addresses of (working pool f64, per-diagonal-row perms i32, output pool f64)."""
+        v, p, o = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        self.lib.lbk_work_ptrs(self.ctx, C.byref(v), C.byref(p), C.byref(o))
+        return int(v.value or 0), int(p.value or 0), int(o.value or 0)
+
+    def block_layout(self) -> np.ndarray:
+        """[3 x nblocks]: working offset, working entries, diagonal-row offset (-1 off-diagonal)."""
+        out = np.zeros((3, self.pool.nblocks), np.int64)
+        self.lib.lbk_block_layout(self.ctx, P(out, i64p))
         return out
 
     def download_work(self) -> np.ndarray:

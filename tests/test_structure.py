@@ -155,7 +155,7 @@ def test_matrix_market_roundtrip(tmp_path):
 
 def test_host_library_exports_every_declared_symbol():
     hdr = open(os.path.join(REPO, "include", "lbk.h")).read()
-    declared = set(re.findall(r"^\s*(?:int|void)\s+(lbk_\w+)\s*\(", hdr, re.M))
+    declared = set(re.findall(r"^\s*(?:int|void\s*\*?)\s*(lbk_\w+)\s*\(", hdr, re.M))
     host = ctypes.CDLL(_native.HOST_LIB)
     dev_syms = {s for s in declared if not s.startswith(("lbk_symbolic", "lbk_partition", "lbk_levels",
                                                          "lbk_check", "lbk_blockptr"))}
