@@ -60,7 +60,12 @@ def build_case(name: str, strategy: str = "irregular", block_size: int | None = 
         raise SystemExit(f"unknown config {name}")
     f = M.symbolic_factorize(M.symmetrize_pattern(a))
     curve = M.percentage_curve(M.diag_block_pointer(f))
-    plan = M.irregular_plan(curve, a.n) if strategy == "irregular" else M.regular_plan(a.n, block_size)
+    if strategy == "irregular":
+        plan = M.irregular_plan(curve, a.n)
+    elif strategy == "selector":  # PanguLU-like size selector (blocking.py:130-151)
+        plan = M.regular_plan(a.n, M.pangulu_size_select(a.n, f.nnz_filled))
+    else:
+        plan = M.regular_plan(a.n, block_size)
     g = M.partition(f, a, plan)
     t = M.dependency_levels(g)
     log(f"[bench] {name}: n={a.n} nnz(A)={a.nnz} nnz(L+U)={f.nnz_filled} p={g.p} blocks={len(g.blocks)} "
@@ -167,11 +172,21 @@ def cpu_baseline_sample(g, t, flops_t, budget_s):
     return r, CB.host_cores(), CB.blas_threads(), CB.cpu_model()
 
 
+def plan_arg(s: str):
+    """'irregular' | 'selector' | 'regular:<block size>'."""
+    if s.startswith("regular:"):
+        return "regular", int(s.split(":", 1)[1])
+    if s not in ("irregular", "selector"):
+        raise SystemExit(f"bad --plan {s}")
+    return s, None
+
+
 def run_reference(args):
     world, rank, _ = dist_init("gloo")
     if rank != 0:
         return 0
-    a, f, g, t = build_case(args.config)
+    strategy, bs = plan_arg(args.plan)
+    a, f, g, t = build_case(args.config, strategy, bs)
     from paper_2512_04389_b200.workmodel import task_work
 
     flops_t, _ = task_work(g, t)
@@ -189,7 +204,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "plan": "irregular", "n": a.n, "nnz_filled": f.nnz_filled},
+            "config": {"workload": args.config, "plan": args.plan, "n": a.n, "nnz_filled": f.nnz_filled},
             "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cores, "blas_threads": blas,
                              "cpu": model, "kind": "port", "sample": sample},
             "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -210,6 +225,7 @@ def main():
     ap.add_argument("--levels-out", default=None, help="write per-level device times + work to this .npz")
     ap.add_argument("--dense-threshold", type=float, default=0.1,
                     help="compressed-tile density tag for the FP64 DMMA kernels; <0 = CSC kernels only")
+    ap.add_argument("--plan", default="irregular", help="irregular | selector | regular:<block size>")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of 2D block-cyclic")
     ap.add_argument("--dist-backend", default=None, help="nccl (default with CUDA) | gloo (host-staged, 1-GPU tests)")
     args = ap.parse_args()
@@ -225,7 +241,8 @@ def main():
     from paper_2512_04389_b200.numeric import Engine, pinned_empty
     from paper_2512_04389_b200.workmodel import task_work
 
-    a, f, g, t = build_case(args.config)
+    strategy, bs = plan_arg(args.plan)
+    a, f, g, t = build_case(args.config, strategy, bs)
     flops_t, bytes_t = task_work(g, t)
     total_flops = float(flops_t.sum())
     t0 = time.perf_counter()
@@ -357,7 +374,7 @@ def main():
             "scaling": "strong" if distributed else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "matrix": "3D 7-point Poisson 64^3, geometric ND" if args.config == "C2"
-                       else args.config, "plan": "irregular", "n": a.n, "nnz_A": a.nnz, "nnz_filled": f.nnz_filled,
+                       else args.config, "plan": args.plan, "n": a.n, "nnz_A": a.nnz, "nnz_filled": f.nnz_filled,
                        "p": g.p, "tasks": t.task_count, "levels": t.n_levels, "gflop": total_flops / 1e9,
                        "parallelism": (f"2d-block-cyclic {de.pg.pr}x{de.pg.pc} (NCCL p2p)" if distributed
                                        else f"replicas{world}" if world > 1 else "single"),

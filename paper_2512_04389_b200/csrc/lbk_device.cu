@@ -112,12 +112,34 @@ struct ExecBuilder {
     preds.push_back(std::move(deps));
     return static_cast<int>(t.size()) - 1;
   }
+  // Dequeue order = descending upward rank (longest cost path to the end of
+  // the level's DAG; per-type costs are measured tile latencies in 0.1 us).
+  // That is a topological order (a task outranks all its successors) and it
+  // is the lookahead schedule: the next panel's GETRF/TRSM tiles and the
+  // GEMMs feeding them overtake the bulk trailing updates of the current
+  // step, which a plain step-major order would dequeue first.
+  static int cost_of(int type) {
+    static const int c[10] = {150, 360, 180, 130, 64, 60, 130, 64, 180, 64};
+    return type >= 0 && type < 10 ? c[type] : 64;
+  }
   void flush(Level* L, std::vector<XTask>* tasks, std::vector<int32_t>* sptr, std::vector<int32_t>* succ,
              std::vector<int32_t>* deps0) {
     const int n = static_cast<int>(t.size());
     std::vector<int> order(n), pos(n);
     for (int i = 0; i < n; ++i) order[i] = i;
-    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return key[x] < key[y]; });
+    {
+      // insertion order is topological (deps always name earlier tasks)
+      std::vector<std::vector<int>> fwd(n);
+      for (int i = 0; i < n; ++i)
+        for (int p : preds[i]) fwd[p].push_back(i);
+      std::vector<int64_t> rank(n, 0);
+      for (int i = n - 1; i >= 0; --i) {
+        int64_t m = 0;
+        for (int s2 : fwd[i]) m = std::max(m, rank[s2]);
+        rank[i] = m + cost_of(t[i].type);
+      }
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return rank[x] > rank[y]; });
+    }
     for (int i = 0; i < n; ++i) pos[order[i]] = i;
     std::vector<std::vector<int>> out(n);
     for (int i = 0; i < n; ++i)

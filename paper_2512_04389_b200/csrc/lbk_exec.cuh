@@ -699,12 +699,17 @@ __global__ void __launch_bounds__(256) exec_kernel(XLevel L, DevPools P, double 
     if (t >= L.ntasks) break;
     const XTask tk = L.tasks[t];
     run_task(tk, P, sm, pivot_tol);
+    // every thread fences its own tile writes before the barrier, so the
+    // successor releases after it are ordered behind all of them; the
+    // releases are spread over the CTA (a GETRF tile has ~2x(tiles per
+    // column) successors: one thread walking them costs an L2 round trip each)
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) {
-      for (int e = L.succ_ptr[t]; e < L.succ_ptr[t + 1]; ++e) atomicSub(L.deps + L.succ[e], 1);
-      if (L.trace) L.trace[3 * t + 2] = gtimer();
+    {
+      const int e0 = L.succ_ptr[t], e1 = L.succ_ptr[t + 1];
+      for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicSub(L.deps + L.succ[e], 1);
     }
+    if (threadIdx.x == 0 && L.trace) L.trace[3 * t + 2] = gtimer();
   }
 }
 
