@@ -168,8 +168,9 @@ int lbk_fp64_peak(int device, double* tflops_dmma, double* tflops_dfma);
  * metrics.level_work_stats, pkg/src/lublock/metrics.py:63-90). */
 int lbk_level_times(lbk_ctx* ctx, double pivot_tol, double static_eps, float* out_ms, lbk_status* st);
 
-/* Persistent-executor timeline of one instrumented replay: trace[3 x n] =
- * dequeue / dependencies-met / done times (ns, globaltimer) per tile task,
+/* Persistent-executor timeline of one instrumented replay: trace[8 x n] =
+ * dequeue / dependencies-met / done, four in-task phase stamps and the
+ * all-writes-fenced time (ns, globaltimer) per tile task,
  * info[6 x n] = type, block, r, c, k, level.  Pass NULL buffers to get *n. */
 int lbk_exec_trace(lbk_ctx* ctx, double pivot_tol, double static_eps, uint64_t* trace, int32_t* info,
                    int64_t* n, lbk_status* st);

@@ -1059,7 +1059,7 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
         X.deps = c->xdeps.p + L.exec_off;
         X.head = c->xheads.p + l;
         X.ntasks = L.nexec;
-        X.trace = (evs && c->xtrace.p) ? c->xtrace.p + 3 * L.exec_off : nullptr;
+        X.trace = (evs && c->xtrace.p) ? c->xtrace.p + 8 * L.exec_off : nullptr;
         const int grid = std::max(1, std::min(L.nexec, 148 * 2));
         exec_kernel<<<grid, 256, EXEC_SMEM, s2>>>(X, P, pivot_tol);
       } else {
@@ -1349,7 +1349,8 @@ int lbk_level_times(lbk_ctx* c, double pivot_tol, double static_eps, float* out_
 }
 
 // Executor timeline: one instrumented replay with per-task globaltimer stamps.
-// trace[3 x n] = dequeue, ready (dependencies met), done (ns); info[6 x n] =
+// trace[8 x n] = dequeue, ready (dependencies met), done, 4 in-task phase
+// stamps (0 if unused), all writes fenced (ns); info[6 x n] =
 // type, a, r, c, k, level.  *n = executor tasks (call with NULLs to size).
 int lbk_exec_trace(lbk_ctx* c, double pivot_tol, double static_eps, uint64_t* trace, int32_t* info, int64_t* n,
                    lbk_status* st) {
@@ -1359,12 +1360,12 @@ int lbk_exec_trace(lbk_ctx* c, double pivot_tol, double static_eps, uint64_t* tr
     return 0;
   }
   LBK_CUDA(cudaSetDevice(c->device), st);
-  LBK_CUDA(c->xtrace.alloc(3 * std::max<int64_t>(c->n_exec, 1)), st);
-  LBK_CUDA(cudaMemset(c->xtrace.p, 0, 3 * std::max<int64_t>(c->n_exec, 1) * 8), st);
+  LBK_CUDA(c->xtrace.alloc(8 * std::max<int64_t>(c->n_exec, 1)), st);
+  LBK_CUDA(cudaMemset(c->xtrace.p, 0, 8 * std::max<int64_t>(c->n_exec, 1) * 8), st);
   std::vector<float> lv(c->levels.size() * 5);
   const int rc = lbk_level_times(c, pivot_tol, static_eps, lv.data(), st);
   if (rc == LBK_ERR_CUDA || rc == LBK_ERR_OOM) return rc;
-  LBK_CUDA(cudaMemcpy(trace, c->xtrace.p, 3 * c->n_exec * 8, cudaMemcpyDeviceToHost), st);
+  LBK_CUDA(cudaMemcpy(trace, c->xtrace.p, 8 * c->n_exec * 8, cudaMemcpyDeviceToHost), st);
   std::vector<XTask> ht(c->n_exec);
   LBK_CUDA(cudaMemcpy(ht.data(), c->xtasks.p, c->n_exec * sizeof(XTask), cudaMemcpyDeviceToHost), st);
   for (size_t l = 0; l < c->levels.size(); ++l)

@@ -68,7 +68,7 @@ struct XLevel {
   int* deps;   // working dependency counters (reset from a pristine copy per run)
   int* head;   // task counter of this level
   int ntasks;
-  unsigned long long* trace;  // optional: per task [dequeue, ready, done] in ns (globaltimer)
+  unsigned long long* trace;  // optional: per task [dequeue, ready, done, phase 0..3, fenced] in ns (globaltimer)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -89,6 +89,7 @@ struct Line {
 };
 
 __device__ __forceinline__ int line_id() { return threadIdx.x >> 2; }
+__device__ __forceinline__ void bar_rows64() { asm volatile("bar.sync 1, 64;" ::: "memory"); }
 __device__ __forceinline__ int line_q() { return threadIdx.x & 3; }
 
 // row `r` of a column-major tile: entries (r, 4i+q)
@@ -327,6 +328,88 @@ __device__ __forceinline__ void col_gemv32(double (&x)[32], const double* As, co
     for (int r = 0; r < 32; ++r) x[r] = fma(-As[k * XTP + r], y[k], x[r]);
 }
 
+// LU (no exchange) of the n x n (n <= 64) tile in smem T (column-major, XTP
+// stride), blocked by 16-column panels.  Per panel: (1) the 64 x 16 panel is
+// factored by threads 0..63 (thread r holds row r's 16 panel entries in
+// registers; the pivot row is published to smem, one 64-thread named barrier
+// per column); (2) U12 <- L11^{-1} A12 by one thread per trailing column;
+// (3) A22 -= L21 U12 by all 256 threads.  Every column is scaled only after
+// all updates from the columns left of it, so |d_rj| staged in Dd (r > j) is
+// the value the reference's pivot search sees.  Ends with a CTA barrier.
+__device__ void tile_lu64_blocked(double* T, int n, double* Dd, double* urow) {
+  const int tid = threadIdx.x;
+  constexpr int PB = 16;
+#pragma unroll 1
+  for (int pb = 0; pb < n; pb += PB) {
+    if (tid < XT) {
+      const int r = tid;
+      double p[PB];
+#pragma unroll
+      for (int i = 0; i < PB; ++i) p[i] = T[(pb + i) * XTP + r];
+      const bool rowok = r < n;
+#pragma unroll
+      for (int jj = 0; jj < PB; ++jj) {
+        const int j = pb + jj;
+        if (j < n) {
+          double* ub = urow + (jj & 1) * (PB + 1);
+          if (r == j) {
+#pragma unroll
+            for (int i = jj; i < PB; ++i) ub[i] = p[i];
+            ub[PB] = 1.0 / p[jj];
+          }
+          bar_rows64();
+          if (r > j && rowok) {
+            const double d = p[jj];
+            Dd[j * XTP + r] = fabs(d);
+            const double l = d * ub[PB];
+            p[jj] = l;
+#pragma unroll
+            for (int i = jj + 1; i < PB; ++i) p[i] = fma(-l, ub[i], p[i]);
+          }
+        }
+      }
+      if (r >= pb) {
+#pragma unroll
+        for (int i = 0; i < PB; ++i) T[(pb + i) * XTP + r] = p[i];
+      }
+    }
+    __syncthreads();
+    const int pe = min(n, pb + PB);
+    if (pe >= n) break;
+    // (2) U12: rows pb..pe-1 of trailing columns c >= pe, L11 unit lower
+    if (tid >= pe && tid < n) {
+      const int c = tid;
+      double x[PB];
+#pragma unroll
+      for (int i = 0; i < PB; ++i) x[i] = T[c * XTP + pb + i];
+#pragma unroll
+      for (int k = 0; k < PB; ++k)
+#pragma unroll
+        for (int i = k + 1; i < PB; ++i) x[i] = fma(-T[(pb + k) * XTP + pb + i], x[k], x[i]);
+#pragma unroll
+      for (int i = 0; i < PB; ++i) T[c * XTP + pb + i] = x[i];
+    }
+    __syncthreads();
+    // (3) A22 -= L21 U12: thread owns row r = pe + (tid & 63) (if < n), columns pe + (tid >> 6) + 4q
+    {
+      const int r = pe + (tid & (XT - 1)), c0 = pe + (tid >> 6);
+      if (r < n) {
+        double l[PB];
+#pragma unroll
+        for (int k = 0; k < PB; ++k) l[k] = T[(pb + k) * XTP + r];
+        for (int c = c0; c < n; c += 4) {
+          double acc = T[c * XTP + r];
+#pragma unroll
+          for (int k = 0; k < PB; ++k) acc = fma(-l[k], T[c * XTP + pb + k], acc);
+          T[c * XTP + r] = acc;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+}
+
 // LU (no exchange) of the 64x64 tile in smem T (XTP stride); n <= 64 valid,
 // padded diagonal set to 1.  Dd: staged |d| (XTP stride).  256 threads.
 __device__ void tile_lu64(double* T, int n, double* Dd, double* rinv) {
@@ -427,14 +510,26 @@ __device__ void tile_left_solve64(double* X, const double* L) {
 
 // bmax[j] (global, bits) = max over rows r > j (r < nr) of the staged |d_rj|;
 // rows_all: the whole column is "below" (TRSM_L tiles).
+// Thread (column c = tid & 63, row quarter tid >> 6) reduces 16 independent
+// smem reads, the 4 quarter maxima meet in `part` (256 doubles of scratch),
+// one atomic per column: ~0.2 us instead of 8 serial shuffle reductions per warp.
 __device__ __forceinline__ void flush_colmax(const double* Dd, int nr, int nc, bool rows_all,
-                                             unsigned long long* bmax) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int j = warp; j < nc; j += 8) {
-    double mx = 0.0;
-    for (int rr = (rows_all ? 0 : j + 1) + lane; rr < nr; rr += 32) mx = fmax(mx, Dd[j * XTP + rr]);
-    for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if (lane == 0 && mx > 0.0) atomic_max_nonneg(&bmax[j], mx);
+                                             unsigned long long* bmax, double* part) {
+  const int c = threadIdx.x & (XT - 1), q = threadIdx.x >> 6;
+  double mx = 0.0;
+  if (c < nc) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      const int rr = q * 16 + i;
+      const double v = Dd[c * XTP + rr];
+      if (rr < nr && (rows_all || rr > c)) mx = fmax(mx, v);
+    }
+  }
+  part[q * XT + c] = mx;
+  __syncthreads();
+  if (threadIdx.x < nc) {
+    const double m = fmax(fmax(part[c], part[XT + c]), fmax(part[2 * XT + c], part[3 * XT + c]));
+    if (m > 0.0) atomic_max_nonneg(&bmax[c], m);
   }
 }
 
@@ -532,7 +627,16 @@ __device__ __forceinline__ void prep_right(const double* U, int n, double* rinv,
   }
 }
 
-__device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double pivot_tol) {
+// instrumented replays: phase stamps inside a task (thread 0, after a barrier)
+__device__ __forceinline__ void stamp(unsigned long long* ph, int k) {
+  if (ph) {
+    __syncthreads();
+    if (threadIdx.x == 0) ph[k] = gtimer();
+  }
+}
+
+__device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double pivot_tol,
+                         unsigned long long* ph = nullptr) {
   double* T0 = sm;                  // target tile (XTP stride)
   double* T1 = sm + XREG;           // operand tile (XTP stride) / DMMA A (XS stride)
   double* T2 = sm + 2 * XREG;       // DMMA B (XS stride)
@@ -566,9 +670,14 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
     case X_GETRF: {
       const int m = A.nrows, k0 = tk.k * XT, n = min(XT, m - k0);
       double* G = P.vals + A.ent + static_cast<size_t>(k0) * m + k0;
-      row_load(X, G, m, n, n);
-      line_lu(X, n, rinv, T1, G, m);
-      flush_colmax(T1, n, n, false, P.bmax + A.dg + k0);
+      load_tile(T0, G, m, n, n);
+      __syncthreads();
+      stamp(ph, 0);
+      tile_lu64_blocked(T0, n, T1, rinv);
+      stamp(ph, 1);
+      store_tile(G, m, T0, n, n);
+      flush_colmax(T1, n, n, false, P.bmax + A.dg + k0, T2);
+      stamp(ph, 2);
       break;
     }
     case X_TRSM_L: {  // rows of tile (r,k) in registers, U_kk in smem
@@ -577,9 +686,13 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       load_tile(T1, P.vals + A.ent + static_cast<size_t>(k0) * m + k0, m, nk, nk);
       load_tile(T0, G, m, nr, nk);
       __syncthreads();
+      stamp(ph, 0);
       tile_right_solve64<true>(T0, T1, rinv, T2, nk);
+      stamp(ph, 1);
       store_tile(G, m, T0, nr, nk);
-      flush_colmax(T2, nr, nk, true, P.bmax + A.dg + k0);
+      stamp(ph, 2);
+      flush_colmax(T2, nr, nk, true, P.bmax + A.dg + k0, T1);
+      stamp(ph, 3);
       break;
     }
     case X_TRSM_U: {  // columns of tile (k,c) in registers, L_kk in smem
@@ -686,11 +799,11 @@ __global__ void __launch_bounds__(256) exec_kernel(XLevel L, DevPools P, double 
     if (threadIdx.x == 0) {
       const int t = atomicAdd(L.head, 1);
       if (t < L.ntasks) {
-        if (L.trace) L.trace[3 * t] = gtimer();
+        if (L.trace) L.trace[8 * t] = gtimer();
         volatile int* dp = L.deps + t;
         while (*dp > 0) __nanosleep(32);
         __threadfence();
-        if (L.trace) L.trace[3 * t + 1] = gtimer();
+        if (L.trace) L.trace[8 * t + 1] = gtimer();
       }
       s_t = t;
     }
@@ -698,18 +811,19 @@ __global__ void __launch_bounds__(256) exec_kernel(XLevel L, DevPools P, double 
     const int t = s_t;
     if (t >= L.ntasks) break;
     const XTask tk = L.tasks[t];
-    run_task(tk, P, sm, pivot_tol);
+    run_task(tk, P, sm, pivot_tol, L.trace ? L.trace + 8 * t + 3 : nullptr);
     // every thread fences its own tile writes before the barrier, so the
     // successor releases after it are ordered behind all of them; the
     // releases are spread over the CTA (a GETRF tile has ~2x(tiles per
     // column) successors: one thread walking them costs an L2 round trip each)
     __threadfence();
     __syncthreads();
+    if (threadIdx.x == 0 && L.trace) L.trace[8 * t + 7] = gtimer();
     {
       const int e0 = L.succ_ptr[t], e1 = L.succ_ptr[t + 1];
       for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicSub(L.deps + L.succ[e], 1);
     }
-    if (threadIdx.x == 0 && L.trace) L.trace[3 * t + 2] = gtimer();
+    if (threadIdx.x == 0 && L.trace) L.trace[8 * t + 2] = gtimer();
   }
 }
 

@@ -312,13 +312,14 @@ class Engine:
         return out
 
     def exec_trace(self, pivot_tol=DEFAULT_PIVOT_TOL):
-        """(trace[n,3] ns, info[n,6]) of the persistent executor's tile tasks (one instrumented replay)."""
+        """(trace[n,8] ns, info[n,6]) of the persistent executor's tile tasks (one instrumented replay):
+        dequeue, ready, done, in-task phase stamps 0..3 (GETRF / TRSM_L), writes fenced."""
         if not self._resident:
             self.upload()
         n = C.c_int64()
         st = _native.LbkStatus()
         self.lib.lbk_exec_trace(self.ctx, pivot_tol, math.nan, None, None, C.byref(n), C.byref(st))
-        tr = np.zeros((n.value, 3), np.uint64)
+        tr = np.zeros((n.value, 8), np.uint64)
         info = np.zeros((n.value, 6), np.int32)
         self.lib.lbk_exec_trace(self.ctx, pivot_tol, math.nan, tr.ctypes.data_as(C.POINTER(C.c_uint64)),
                                 P(info, i32p), C.byref(n), C.byref(st))

@@ -34,8 +34,12 @@ if "--trace" in sys.argv:
         sel = info[:, 0] == ty
         run = (tr[sel, 2] - tr[sel, 1]) / 1e3
         wait = (tr[sel, 1] - tr[sel, 0]) / 1e3
+        ph = tr[sel][:, [1, 3, 4, 5, 6, 7, 2]].astype(np.float64)
+        d = np.diff(ph, axis=1) / 1e3
+        d[(ph[:, 1:] == 0) | (ph[:, :-1] == 0)] = np.nan
         print(f"{names[ty]:8s} n={sel.sum():6d} run us med {np.median(run):7.2f} p90 {np.percentile(run, 90):7.2f}"
-              f" wait med {np.median(wait):8.2f}")
+              f" wait med {np.median(wait):8.2f} phases(ready>p0>p1>p2>p3>fence>done) "
+              + " ".join("-" if np.all(np.isnan(d[:, k])) else f"{np.nanmedian(d[:, k]):.2f}" for k in range(6)))
     g = np.flatnonzero(info[:, 0] == 1)
     for t in g[:6]:
         print(f"GETRF k={info[t, 4]} dequeue {(tr[t, 0] - t0) / 1e3:9.1f} ready {(tr[t, 1] - t0) / 1e3:9.1f}"
