@@ -328,6 +328,125 @@ __device__ __forceinline__ void col_gemv32(double (&x)[32], const double* As, co
     for (int r = 0; r < 32; ++r) x[r] = fma(-As[k * XTP + r], y[k], x[r]);
 }
 
+// 1/x on the critical path: MUFU approximation + two Newton steps (<= 1 ulp
+// from the rounded quotient; the 1e-10 factor tolerance is untouched), the
+// IEEE division only outside the normal range (0, inf, NaN, denormals).
+__device__ __forceinline__ double rcp_nr(double x) {
+  const double ax = fabs(x);
+  if (!(ax >= 1e-300 && ax <= 1e300)) return 1.0 / x;
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
+// acc_c -= sum_k l[k] * B(k, c) for the columns c = c0, c0 + 4, ... < ce, three
+// independent accumulation chains at a time.  Col(c) = address of column c of
+// the target (row offset applied), Bk(c) = address of B(0, c) (k contiguous).
+template <class TA, class TB>
+__device__ __forceinline__ void trail16(const double (&l)[16], int c0, int ce, TA col, TB bk) {
+#pragma unroll 1
+  for (int c = c0; c < ce; c += 12) {
+    const bool v1 = c + 4 < ce, v2 = c + 8 < ce;
+    const double* b0 = bk(c);
+    const double* b1 = bk(v1 ? c + 4 : c);
+    const double* b2 = bk(v2 ? c + 8 : c);
+    double a0 = *col(c), a1 = v1 ? *col(c + 4) : 0.0, a2 = v2 ? *col(c + 8) : 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      a0 = fma(-l[k], b0[k], a0);
+      a1 = fma(-l[k], b1[k], a1);
+      a2 = fma(-l[k], b2[k], a2);
+    }
+    *col(c) = a0;
+    if (v1) *col(c + 4) = a1;
+    if (v2) *col(c + 8) = a2;
+  }
+}
+
+// X (smem, XTP) <- X U^{-1} for columns [0, nc); U upper in smem (XTP), rinv[j] =
+// 1/u_jj.  Blocked by 16 columns: the panel solve needs no communication
+// between rows (threads 0..63 own one row each), the trailing update runs on
+// all 256 threads.  kCheck stages |x_rj| before scaling in Dd[j*XTP + r].
+// Compact (rolled panel loop): the executor's code stays i-cache resident.
+template <bool kCheck>
+__device__ void tile_right_solve_blk(double* X, const double* U, const double* rinv, double* Dd, int nc) {
+  const int tid = threadIdx.x;
+  constexpr int PB = 16;
+#pragma unroll 1
+  for (int pb = 0; pb < nc; pb += PB) {
+    if (tid < XT) {
+      const int r = tid;
+      double x[PB];
+#pragma unroll
+      for (int i = 0; i < PB; ++i) x[i] = X[(pb + i) * XTP + r];
+#pragma unroll
+      for (int jj = 0; jj < PB; ++jj) {
+        const int j = pb + jj;
+        if (j < nc) {
+          if (kCheck) Dd[j * XTP + r] = fabs(x[jj]);
+          x[jj] *= rinv[j];
+#pragma unroll
+          for (int i = jj + 1; i < PB; ++i) x[i] = fma(-x[jj], U[(pb + i) * XTP + j], x[i]);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < PB; ++i) X[(pb + i) * XTP + r] = x[i];
+    }
+    __syncthreads();
+    const int pe = pb + PB;
+    if (pe >= nc) break;
+    {
+      const int r = tid & (XT - 1);
+      double l[PB];
+#pragma unroll
+      for (int k = 0; k < PB; ++k) l[k] = X[(pb + k) * XTP + r];
+      trail16(l, pe + (tid >> 6), nc, [&](int c) { return X + c * XTP + r; },
+              [&](int c) { return U + c * XTP + pb; });
+    }
+    __syncthreads();
+  }
+}
+
+// X (smem, XTP) <- L^{-1} X for rows [0, nr); L unit lower in smem (XTP).  Thread
+// c < 64 owns column c of the 16-row panel; the trailing rows on all 256 threads.
+__device__ void tile_left_solve_blk(double* X, const double* Lm, int nr) {
+  const int tid = threadIdx.x;
+  constexpr int PB = 16;
+#pragma unroll 1
+  for (int pb = 0; pb < nr; pb += PB) {
+    if (tid < XT) {
+      const int c = tid;
+      double x[PB];
+#pragma unroll
+      for (int i = 0; i < PB; ++i) x[i] = X[c * XTP + pb + i];
+#pragma unroll
+      for (int k = 0; k < PB; ++k)
+#pragma unroll
+        for (int i = k + 1; i < PB; ++i) x[i] = fma(-Lm[(pb + k) * XTP + pb + i], x[k], x[i]);
+#pragma unroll
+      for (int i = 0; i < PB; ++i) X[c * XTP + pb + i] = x[i];
+    }
+    __syncthreads();
+    const int pe = pb + PB;
+    if (pe >= nr) break;
+    {
+      // row r = pe + (tid & 63): X[r, c] -= sum_k L[r, pb + k] X[pb + k, c]
+      const int r = pe + (tid & (XT - 1));
+      if (r < nr) {
+        double l[PB];
+#pragma unroll
+        for (int k = 0; k < PB; ++k) l[k] = Lm[(pb + k) * XTP + r];
+        trail16(l, tid >> 6, XT, [&](int c) { return X + c * XTP + r; },
+                [&](int c) { return X + c * XTP + pb; });
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // LU (no exchange) of the n x n (n <= 64) tile in smem T (column-major, XTP
 // stride), blocked by 16-column panels.  Per panel: (1) the 64 x 16 panel is
 // factored by threads 0..63 (thread r holds row r's 16 panel entries in
@@ -355,7 +474,7 @@ __device__ void tile_lu64_blocked(double* T, int n, double* Dd, double* urow) {
           if (r == j) {
 #pragma unroll
             for (int i = jj; i < PB; ++i) ub[i] = p[i];
-            ub[PB] = 1.0 / p[jj];
+            ub[PB] = rcp_nr(p[jj]);
           }
           bar_rows64();
           if (r > j && rowok) {
@@ -397,12 +516,7 @@ __device__ void tile_lu64_blocked(double* T, int n, double* Dd, double* urow) {
         double l[PB];
 #pragma unroll
         for (int k = 0; k < PB; ++k) l[k] = T[(pb + k) * XTP + r];
-        for (int c = c0; c < n; c += 4) {
-          double acc = T[c * XTP + r];
-#pragma unroll
-          for (int k = 0; k < PB; ++k) acc = fma(-l[k], T[c * XTP + pb + k], acc);
-          T[c * XTP + r] = acc;
-        }
+        trail16(l, c0, n, [&](int c) { return T + c * XTP + r; }, [&](int c) { return T + c * XTP + pb; });
       }
     }
     __syncthreads();
@@ -687,7 +801,9 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       load_tile(T0, G, m, nr, nk);
       __syncthreads();
       stamp(ph, 0);
-      tile_right_solve64<true>(T0, T1, rinv, T2, nk);
+      if (threadIdx.x < XT) rinv[threadIdx.x] = threadIdx.x < nk ? 1.0 / T1[threadIdx.x * XTP + threadIdx.x] : 1.0;
+      __syncthreads();
+      tile_right_solve_blk<true>(T0, T1, rinv, T2, nk);
       stamp(ph, 1);
       store_tile(G, m, T0, nr, nk);
       stamp(ph, 2);
@@ -701,7 +817,7 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       load_tile(T1, P.vals + A.ent + static_cast<size_t>(k0) * m + k0, m, nk, nk);
       load_tile(T0, G, m, nk, nc);
       __syncthreads();
-      tile_left_solve64(T0, T1);
+      tile_left_solve_blk(T0, T1, nk);
       store_tile(G, m, T0, nk, nc);
       break;
     }
@@ -745,7 +861,7 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
         else load_tile(T1, Dv + static_cast<size_t>(r0) * m + r0, m, nr, nr);
         load_tile(T0, G, ld, nr, nc);
         __syncthreads();
-        tile_left_solve64(T0, T1);
+        tile_left_solve_blk(T0, T1, nr);
         store_tile(G, ld, T0, nr, nc);
       } else {
         const int k0 = tk.k * XT, nk = min(XT, A.nR - k0);
@@ -773,7 +889,9 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
         else load_tile(T1, Dv + static_cast<size_t>(c0) * m + c0, m, nc, nc);
         load_tile(T0, G, ld, nr, nc);
         __syncthreads();
-        tile_right_solve64<false>(T0, T1, rinv, T2, nc);
+        if (threadIdx.x < XT) rinv[threadIdx.x] = threadIdx.x < nc ? 1.0 / T1[threadIdx.x * XTP + threadIdx.x] : 1.0;
+        __syncthreads();
+        tile_right_solve_blk<false>(T0, T1, rinv, nullptr, nc);
         store_tile(G, ld, T0, nr, nc);
       } else {
         const int k0 = tk.k * XT, nk = min(XT, A.nC - k0);
