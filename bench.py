@@ -335,6 +335,13 @@ def main():
         fv["gbs"] = fv["gbytes"] / s
         fv["frac_fp64_tensor"] = fv["tflops"] / dmma_peak if dmma_peak == dmma_peak else None
         fv["frac_hbm"] = fv["gbs"] / hbm_peak
+    # executed (tile-shaped, structural zeros included) flop rates: tensor-pipe utilisation
+    for r, ex in ((1, eng.dmma_flops_executed), (3, eng.exec_flops_executed)):
+        if r in fams and ex > 0:
+            s = max(fams[r]["ms"], 1e-9) / 1e3
+            fams[r]["executed_gflop"] = ex / 1e9
+            fams[r]["executed_tflops"] = ex / s / 1e12
+            fams[r]["executed_frac_fp64_tensor"] = ex / s / 1e12 / dmma_peak if dmma_peak == dmma_peak else None
     D = fams[dom]
     if dom in (1, 2, 3):
         roof = {"bound": "tensor", "achieved": D["tflops"], "peak": dmma_peak, "unit": "TFLOP/s",

@@ -146,10 +146,12 @@ int lbk_set_perms(lbk_ctx* ctx, const int32_t* perms, lbk_status* st);
 int lbk_host_alloc(void** ptr, int64_t bytes);
 void lbk_host_free(void* ptr);
 
-/* info[12]: [0] launched levels, [1] CSC work items, [2] diagonal rows,
+/* info[14]: [0] launched levels, [1] CSC work items, [2] diagonal rows,
  * [3] reference entries, [4] DMMA SSSSM tiles, [5] panel/exact items,
  * [6] kernel launches per factorization, [7] working entries, [8..10]
- * SPARSE/RECT/FULL blocks, [11] tiled-GETRF items. */
+ * SPARSE/RECT/FULL blocks, [11] tiled-GETRF items, [12] executed DMMA
+ * SSSSM flops (tile rectangles, structural zeros included), [13] executed
+ * flops of the tile-DAG executor (64^3-tile equivalents). */
 int lbk_plan_info(lbk_ctx* ctx, int64_t* info);
 
 /* Per task of the DependencyTree: the kernel family that executes it
@@ -200,6 +202,13 @@ int lbk_work_ptrs(lbk_ctx* ctx, void** vals, void** perm, void** vout);
 /* layout[3 x nblocks]: working-pool offset, working entries, diagonal-row
  * offset (-1 for off-diagonal blocks), in pool block order. */
 int lbk_block_layout(lbk_ctx* ctx, int64_t* layout);
+
+/* Cross-level lookahead: defer[t] = 1 marks a task whose successors all sit
+ * >= 2 ASAP levels later (computed from DependencyTree.pred_ptr/pred_idx,
+ * grid.py:172-181).  Its DMMA SSSSM tiles run on a side branch concurrently
+ * with the next level; the level two later waits for them.  Call before
+ * lbk_plan; NULL clears. */
+int lbk_set_task_defer(lbk_ctx* ctx, int64_t ntasks, const int8_t* defer, lbk_status* st);
 
 /* Launched-level table (4 x nlevels: item offset, items, warps, acc length)
  * and, if items != NULL, the work items (6 x total: kind, a, b, c, begin, end). */

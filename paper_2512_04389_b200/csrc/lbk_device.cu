@@ -69,6 +69,8 @@ struct Level {
   int32_t nitems, warps, acc_len;
   int64_t gemm_off;  // SSSSM DMMA tiles
   int32_t ngemm;
+  int64_t gemmD_off;  // deferred SSSSM DMMA tiles (every successor >= 2 tree levels later)
+  int32_t ngemmD;
   int64_t panel_off;  // dense GESSM/TSTRF strips
   int32_t npanel;
   int32_t panel_smem;
@@ -167,6 +169,10 @@ struct lbk_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t aux[NBRANCH] = {nullptr, nullptr, nullptr};
   cudaEvent_t fork = nullptr, join[NBRANCH] = {nullptr, nullptr, nullptr};
+  cudaStream_t dstream = nullptr;     // deferred SSSSM branch
+  std::vector<cudaEvent_t> dev;       // per launch level: deferred work done
+  std::vector<int8_t> defer;          // per task: may run concurrently with the next level
+  int exec_per_sm = 2;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<cudaGraphExec_t> graphs;  // one per segment (see lbk_set_cuts)
   double g_tol = NAN, g_eps = NAN;
@@ -196,6 +202,7 @@ struct lbk_ctx {
   DevBuf<int> xdeps, xheads;
   DevBuf<int32_t> perm0;  // identity permutation per diagonal row
   int64_t n_exec = 0;
+  double dmma_flops = 0, exec_flops = 0;  // executed (tile-shaped) flops per factorization
   bool use_exec = true;
   // distribution (lbk_set_task_mask / lbk_set_cuts): tasks this rank runs, and
   // the tree levels after which the graph is cut for a block exchange
@@ -311,6 +318,8 @@ int lbk_create(lbk_ctx** out, int device, lbk_status* st) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->join[k], cudaEventDisableTiming);
   }
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->dstream, cudaStreamNonBlocking);
+  if (const char* x = std::getenv("LBK_EXEC_PER_SM")) c->exec_per_sm = std::max(1, std::atoi(x));
   if (e != cudaSuccess) {
     delete c;
     return cuda_fail(st, e, "lbk_create");
@@ -332,6 +341,8 @@ void lbk_destroy(lbk_ctx* c) {
     if (c->join[k]) cudaEventDestroy(c->join[k]);
   }
   if (c->fork) cudaEventDestroy(c->fork);
+  for (auto ev : c->dev) cudaEventDestroy(ev);
+  if (c->dstream) cudaStreamDestroy(c->dstream);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -352,6 +363,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
                 *T_nz = table + 4 * nb, *T_cp = table + 5 * nb, *T_ent = table + 6 * nb;
   const bool dense_on = (flags & 1) != 0, all_full = (flags & 2) != 0;
   c->flags = flags;
+  c->dmma_flops = c->exec_flops = 0;
   c->n = n;
   c->p = p;
   c->nblocks = nb;
@@ -552,7 +564,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     for (int64_t t = 0; t < ntasks; ++t) nlevels = std::max(nlevels, tlevels[t] + 1);
     std::vector<std::vector<Item>> gen(nlevels);
     std::vector<int32_t> acc_len(nlevels, 1);
-    std::vector<std::vector<GemmItem>> gem(nlevels);
+    std::vector<std::vector<GemmItem>> gem(nlevels), gemD(nlevels);
     std::vector<GemmTask> gtasks;
     std::vector<int32_t> hmaps;
     std::vector<std::vector<DenseItem>> pan(nlevels), exa(nlevels);
@@ -685,9 +697,11 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           }
           const int32_t task = static_cast<int32_t>(gtasks.size());
           c->route[t] = 1;
+          c->dmma_flops += 2.0 * hb[lb].nR * static_cast<double>(gt.K) * hb[ub].nC;
           gtasks.push_back(gt);
+          auto& dst = (!c->defer.empty() && c->defer[t]) ? gemD[lv] : gem[lv];
           for (int32_t n0 = 0; n0 < hb[ub].nC; n0 += GBN)
-            for (int32_t m0 = 0; m0 < hb[lb].nR; m0 += GBM) gem[lv].push_back(GemmItem{task, m0, n0});
+            for (int32_t m0 = 0; m0 < hb[lb].nR; m0 += GBM) dst.push_back(GemmItem{task, m0, n0});
           continue;
         }
         acc_len[lv] = std::max(acc_len[lv], hb[tgt].nrows);
@@ -705,7 +719,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     c->levels.clear();
     c->subs.clear();
     for (int32_t lv = 0; lv < nlevels; ++lv) {
-      if (gen[lv].empty() && gem[lv].empty() && pan[lv].empty() && exa[lv].empty()) continue;
+      if (gen[lv].empty() && gem[lv].empty() && gemD[lv].empty() && pan[lv].empty() && exa[lv].empty()) continue;
       if (static_cast<int64_t>(acc_len[lv]) * 8 > MAX_SMEM || pan_smem[lv] > MAX_SMEM || exa_smem[lv] > MAX_SMEM)
         return fail(st, LBK_ERR_BAD_ARG, "block span too large for the shared-memory accumulator");
       Level L{};
@@ -718,6 +732,9 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       L.gemm_off = static_cast<int64_t>(mall.size());
       L.ngemm = static_cast<int32_t>(gem[lv].size());
       mall.insert(mall.end(), gem[lv].begin(), gem[lv].end());
+      L.gemmD_off = static_cast<int64_t>(mall.size());
+      L.ngemmD = static_cast<int32_t>(gemD[lv].size());
+      mall.insert(mall.end(), gemD[lv].begin(), gemD[lv].end());
       L.panel_off = static_cast<int64_t>(dall.size());
       L.npanel = static_cast<int32_t>(pan[lv].size());
       L.panel_smem = pan_smem[lv];
@@ -912,6 +929,13 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
               }
           }
         }
+        for (const XTask& x : X.t) {  // executed flops of the tile tasks (full 64-tiles)
+          const double t3 = 64.0 * 64.0 * 64.0;
+          c->exec_flops += x.type == X_GEMM || x.type == X_PG_UPD || x.type == X_PT_UPD ? 2 * t3
+                           : x.type == X_GETRF                                       ? 2 * t3 / 3
+                           : x.type == X_COLMAX || x.type == X_FINAL                 ? 0
+                                                                                     : t3;
+        }
         X.flush(&L, &xtasks, &xsucc_ptr, &xsucc, &xdeps0);
       }
       c->levels.push_back(L);
@@ -977,6 +1001,9 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     c->seg_begin.push_back(static_cast<int32_t>(c->levels.size()));
   }
   drop_graphs(c);
+  for (auto ev : c->dev) cudaEventDestroy(ev);
+  c->dev.assign(c->levels.size(), nullptr);
+  for (auto& ev : c->dev) LBK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), st);
   ok(st);
   return 0;
 }
@@ -1019,15 +1046,34 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
   }
   }
   if (evs && first) cudaEventRecordWithFlags((*evs)[0], s0, cudaEventRecordExternal);
+  // deferred SSSSM work of launch level l runs beside the next tree level; a
+  // level at tree level T waits for the deferred work of tree levels <= T - 2
+  std::vector<size_t> pending;
   for (size_t l = lo; l < hi; ++l) {
     const Level& L = c->levels[l];
+    for (size_t q = 0; q < pending.size();) {
+      if (c->levels[pending[q]].tree_level <= L.tree_level - 2) {
+        cudaStreamWaitEvent(s0, c->dev[pending[q]], 0);
+        pending.erase(pending.begin() + q);
+      } else {
+        ++q;
+      }
+    }
     const bool has_t = !exact && (use_exec ? L.nexec > 0 : L.ntcol > 0);
     const bool br[NBRANCH] = {L.ngemm > 0, (!use_exec && L.npanel > 0) || (exact && L.nexact > 0), has_t};
     // instrumented replays: per level [end, gemm b/e, panel b/e, getrf b/e, csc b/e]
     auto rec = [&](int k, cudaStream_t s) {
-      if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 9 + k], s, cudaEventRecordExternal);
+      if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 11 + k], s, cudaEventRecordExternal);
     };
-    if (br[0] || br[1] || br[2]) cudaEventRecord(c->fork, s0);
+    if (br[0] || br[1] || br[2] || L.ngemmD) cudaEventRecord(c->fork, s0);
+    if (L.ngemmD) {
+      cudaStreamWaitEvent(c->dstream, c->fork, 0);
+      if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 11 + 9], c->dstream, cudaEventRecordExternal);
+      gemm_map_kernel<<<L.ngemmD, 256, GEMM_SMEM, c->dstream>>>(c->gitems.p + L.gemmD_off, c->gtasks.p, P);
+      if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 11 + 10], c->dstream, cudaEventRecordExternal);
+      cudaEventRecord(c->dev[l], c->dstream);
+      pending.push_back(l);
+    }
     if (br[0]) {
       cudaStreamWaitEvent(c->aux[0], c->fork, 0);
       rec(1, c->aux[0]);
@@ -1060,7 +1106,7 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
         X.head = c->xheads.p + l;
         X.ntasks = L.nexec;
         X.trace = (evs && c->xtrace.p) ? c->xtrace.p + 8 * L.exec_off : nullptr;
-        const int grid = std::max(1, std::min(L.nexec, 148 * 2));
+        const int grid = std::max(1, std::min(L.nexec, 148 * c->exec_per_sm));
         exec_kernel<<<grid, 256, EXEC_SMEM, s2>>>(X, P, pivot_tol);
       } else {
         getrf_colmax_kernel<<<L.ntcol, 256, 0, s2>>>(c->titems.p + L.tcol_off, P);
@@ -1086,6 +1132,7 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
       if (br[k]) cudaStreamWaitEvent(s0, c->join[k], 0);
     rec(0, s0);
   }
+  for (size_t q : pending) cudaStreamWaitEvent(s0, c->dev[q], 0);
   if (last) gather_kernel<<<148 * 8, 256, 0, s0>>>(c->vals.p, c->map.p, c->vout.p, c->nnz);
 }
 
@@ -1218,6 +1265,14 @@ int lbk_set_cuts(lbk_ctx* c, int64_t nlevels, const int8_t* cut_after, lbk_statu
 
 int lbk_num_segments(lbk_ctx* c) { return c ? nsegments(c) : 0; }
 
+int lbk_set_task_defer(lbk_ctx* c, int64_t ntasks, const int8_t* defer, lbk_status* st) {
+  if (!c) return fail(st, LBK_ERR_BAD_ARG, "null ctx");
+  if (defer) c->defer.assign(defer, defer + ntasks);
+  else c->defer.clear();
+  ok(st);
+  return 0;
+}
+
 int lbk_run_segment(lbk_ctx* c, int32_t seg, double pivot_tol, double static_eps, lbk_status* st) {
   LBK_CUDA(cudaSetDevice(c->device), st);
   if (seg < 0 || seg >= nsegments(c)) return fail(st, LBK_ERR_BAD_ARG, "segment out of range");
@@ -1317,7 +1372,7 @@ void lbk_host_free(void* ptr) {
 int lbk_level_times(lbk_ctx* c, double pivot_tol, double static_eps, float* out_ms, lbk_status* st) {
   LBK_CUDA(cudaSetDevice(c->device), st);
   const size_t nl = c->levels.size();
-  std::vector<cudaEvent_t> ev(1 + nl * 9);
+  std::vector<cudaEvent_t> ev(1 + nl * 11);
   for (auto& e : ev) LBK_CUDA(cudaEventCreate(&e), st);
   cudaGraph_t g;
   cudaGraphExec_t ge = nullptr;
@@ -1333,11 +1388,16 @@ int lbk_level_times(lbk_ctx* c, double pivot_tol, double static_eps, float* out_
   if (e == cudaSuccess)
     for (size_t l = 0; l < nl; ++l) {
       const Level& L = c->levels[l];
-      const size_t b = 1 + l * 9, prev = l ? 1 + (l - 1) * 9 : 0;
+      const size_t b = 1 + l * 11, prev = l ? 1 + (l - 1) * 11 : 0;
       float* o = out_ms + l * 5;
       for (int k = 0; k < 5; ++k) o[k] = 0.f;
       cudaEventElapsedTime(&o[0], ev[prev], ev[b]);
       if (L.ngemm) cudaEventElapsedTime(&o[1], ev[b + 1], ev[b + 2]);
+      if (L.ngemmD) {  // deferred DMMA SSSSM: counted with the family (it overlaps the next level)
+        float d = 0.f;
+        cudaEventElapsedTime(&d, ev[b + 9], ev[b + 10]);
+        o[1] += d;
+      }
       if (L.npanel || (exact && L.nexact)) cudaEventElapsedTime(&o[2], ev[b + 3], ev[b + 4]);
       if (!exact && L.ntcol) cudaEventElapsedTime(&o[3], ev[b + 5], ev[b + 6]);
       if (L.nitems) cudaEventElapsedTime(&o[4], ev[b + 7], ev[b + 8]);
@@ -1416,7 +1476,7 @@ int lbk_plan_info(lbk_ctx* c, int64_t* info) {
   info[5] = c->n_panel;
   int64_t launches = 2;  // scatter + gather
   for (const Level& L : c->levels) {
-    launches += (L.nitems > 0) + (L.ngemm > 0);
+    launches += (L.nitems > 0) + (L.ngemm > 0) + (L.ngemmD > 0);
     if (c->use_exec) {
       launches += L.nexec > 0;
       continue;
@@ -1436,6 +1496,8 @@ int lbk_plan_info(lbk_ctx* c, int64_t* info) {
   info[9] = c->store_count[1];
   info[10] = c->store_count[2];
   info[11] = c->n_tile;
+  info[12] = static_cast<int64_t>(c->dmma_flops);
+  info[13] = static_cast<int64_t>(c->exec_flops);
   return 0;
 }
 

@@ -455,47 +455,63 @@ __device__ void tile_left_solve_blk(double* X, const double* Lm, int nr) {
 // (3) A22 -= L21 U12 by all 256 threads.  Every column is scaled only after
 // all updates from the columns left of it, so |d_rj| staged in Dd (r > j) is
 // the value the reference's pivot search sees.  Ends with a CTA barrier.
-__device__ void tile_lu64_blocked(double* T, int n, double* Dd, double* urow) {
+__device__ void tile_lu64_blocked(double* T, int n, double* Dd, double* urow, long long* prof = nullptr) {
   const int tid = threadIdx.x;
   constexpr int PB = 16;
+  (void)urow;
+  long long t0 = prof ? clock64() : 0;
 #pragma unroll 1
   for (int pb = 0; pb < n; pb += PB) {
-    if (tid < XT) {
-      const int r = tid;
-      double p[PB];
+    if (tid < 32) {
+      // warp 0 holds rows lane and lane + 32 of the panel; the pivot row is
+      // broadcast with shuffles (no barrier), every lane forms 1/u_jj itself
+      const int lane = tid, ra = lane, rb = lane + 32;
+      double pa[PB], pc[PB];
 #pragma unroll
-      for (int i = 0; i < PB; ++i) p[i] = T[(pb + i) * XTP + r];
-      const bool rowok = r < n;
+      for (int i = 0; i < PB; ++i) {
+        pa[i] = T[(pb + i) * XTP + ra];
+        pc[i] = T[(pb + i) * XTP + rb];
+      }
 #pragma unroll
       for (int jj = 0; jj < PB; ++jj) {
         const int j = pb + jj;
         if (j < n) {
-          double* ub = urow + (jj & 1) * (PB + 1);
-          if (r == j) {
+          const int src = j & 31;
+          const bool hi = j >= 32;
+          double u[PB];
 #pragma unroll
-            for (int i = jj; i < PB; ++i) ub[i] = p[i];
-            ub[PB] = rcp_nr(p[jj]);
+          for (int i = jj; i < PB; ++i) u[i] = __shfl_sync(0xffffffffu, hi ? pc[i] : pa[i], src);
+          const double rinv = rcp_nr(u[jj]);
+          if (ra > j && ra < n) {
+            const double d = pa[jj];
+            Dd[j * XTP + ra] = fabs(d);
+            const double l = d * rinv;
+            pa[jj] = l;
+#pragma unroll
+            for (int i = jj + 1; i < PB; ++i) pa[i] = fma(-l, u[i], pa[i]);
           }
-          bar_rows64();
-          if (r > j && rowok) {
-            const double d = p[jj];
-            Dd[j * XTP + r] = fabs(d);
-            const double l = d * ub[PB];
-            p[jj] = l;
+          if (rb > j && rb < n) {
+            const double d = pc[jj];
+            Dd[j * XTP + rb] = fabs(d);
+            const double l = d * rinv;
+            pc[jj] = l;
 #pragma unroll
-            for (int i = jj + 1; i < PB; ++i) p[i] = fma(-l, ub[i], p[i]);
+            for (int i = jj + 1; i < PB; ++i) pc[i] = fma(-l, u[i], pc[i]);
           }
         }
       }
-      if (r >= pb) {
 #pragma unroll
-        for (int i = 0; i < PB; ++i) T[(pb + i) * XTP + r] = p[i];
+      for (int i = 0; i < PB; ++i) {
+        if (ra >= pb) T[(pb + i) * XTP + ra] = pa[i];
+        if (rb >= pb) T[(pb + i) * XTP + rb] = pc[i];
       }
     }
+    if (prof) { __syncthreads(); const long long t1 = clock64(); if (tid == 0) prof[0] += t1 - t0; t0 = t1; }
     __syncthreads();
     const int pe = min(n, pb + PB);
     if (pe >= n) break;
     // (2) U12: rows pb..pe-1 of trailing columns c >= pe, L11 unit lower
+    if (prof) { __syncthreads(); const long long t1 = clock64(); if (tid == 0) prof[3] += t1 - t0; t0 = t1; }
     if (tid >= pe && tid < n) {
       const int c = tid;
       double x[PB];
@@ -509,6 +525,7 @@ __device__ void tile_lu64_blocked(double* T, int n, double* Dd, double* urow) {
       for (int i = 0; i < PB; ++i) T[c * XTP + pb + i] = x[i];
     }
     __syncthreads();
+    if (prof) { const long long t1 = clock64(); if (tid == 0) prof[1] += t1 - t0; t0 = t1; }
     // (3) A22 -= L21 U12: thread owns row r = pe + (tid & 63) (if < n), columns pe + (tid >> 6) + 4q
     {
       const int r = pe + (tid & (XT - 1)), c0 = pe + (tid >> 6);
@@ -520,6 +537,7 @@ __device__ void tile_lu64_blocked(double* T, int n, double* Dd, double* urow) {
       }
     }
     __syncthreads();
+    if (prof) { const long long t1 = clock64(); if (tid == 0) prof[2] += t1 - t0; t0 = t1; }
   }
   __syncthreads();
 }
@@ -654,8 +672,10 @@ __device__ __forceinline__ void flush_colmax(const double* Dd, int nr, int nc, b
 constexpr int XTHREADS = 256;
 constexpr int XPER = XT * XT / XTHREADS;  // 16
 
+// not inlined: ~20 call sites would otherwise put ~60 KB of address arithmetic
+// into the executor (i-cache), for a routine that runs a few times per task
 template <int STRIDE>
-__device__ __forceinline__ void stage_tile(double* T, const double* G, int ld, int nr, int nc,
+__device__ __noinline__ void stage_tile(double* T, const double* G, int ld, int nr, int nc,
                                            const int32_t* rg, const int32_t* cg) {
   const int r = threadIdx.x & (XT - 1), c0 = threadIdx.x >> 6;
   const bool rok = r < nr;
@@ -723,7 +743,7 @@ __device__ void tile_mma_sub(double* Cs, const double* As, const double* Bs) {
 }
 
 // C (smem, XTP stride) -> global, masked
-__device__ __forceinline__ void store_tile(double* G, int ld, const double* T, int nr, int nc) {
+__device__ __noinline__ void store_tile(double* G, int ld, const double* T, int nr, int nc) {
   const int r = threadIdx.x & (XT - 1), c0 = threadIdx.x >> 6;
   if (r >= nr) return;
 #pragma unroll

@@ -74,6 +74,7 @@ def _dev():
     d(lib, "lbk_plan_levels", C.c_int, [vp, i64p, i32p])
     d(lib, "lbk_set_task_mask", C.c_int, [vp, C.c_int64, i8p, st])
     d(lib, "lbk_set_cuts", C.c_int, [vp, C.c_int64, i8p, st])
+    d(lib, "lbk_set_task_defer", C.c_int, [vp, C.c_int64, i8p, st])
     d(lib, "lbk_num_segments", C.c_int, [vp])
     d(lib, "lbk_run_segment", C.c_int, [vp, C.c_int32, C.c_double, C.c_double, st])
     d(lib, "lbk_finish_raw", C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(C.c_uint64), st])
@@ -83,6 +84,22 @@ def _dev():
     d(lib, "lbk_block_layout", C.c_int, [vp, i64p])
     _native._dev = lib
     return lib
+
+
+def defer_flags(tree) -> np.ndarray | None:
+    """int8 per task: 1 if every successor sits >= 2 ASAP levels later, so the
+    task may run concurrently with the next level (the engine defers such DMMA
+    SSSSM updates onto a side branch: lookahead across levels).  Needs the
+    tree's predecessor lists (grid.py:172-181); None without them."""
+    pp = getattr(tree, "pred_ptr", None)
+    pi = getattr(tree, "pred_idx", None)
+    if pp is None or pi is None:
+        return None
+    lv = np.asarray(tree.levels_of, np.int64)
+    nt = len(lv)
+    minsucc = np.full(nt, np.iinfo(np.int64).max, np.int64)
+    np.minimum.at(minsucc, np.asarray(pi, np.int64), np.repeat(lv, np.diff(np.asarray(pp, np.int64))))
+    return (minsucc >= lv + 2).astype(np.int8)
 
 
 def fp64_peak(device: int = 0) -> tuple[float, float]:
@@ -131,7 +148,8 @@ class Engine:
 
     def __init__(self, grid, tree, *, device: int = 0, chunk: int = DEFAULT_CHUNK, pool: GridPool | None = None,
                  dense: bool = False, dense_threshold: float | None = DEFAULT_DENSE_THRESHOLD,
-                 dense_kernels: bool = True, mask: np.ndarray | None = None, cuts: np.ndarray | None = None):
+                 dense_kernels: bool = True, mask: np.ndarray | None = None, cuts: np.ndarray | None = None,
+                 lookahead: bool = True):
         """dense=True: dense-scratch mode (every block a full tile, true row swaps).
         dense_threshold: tau of the compressed-tile tag (see include/lbk.h lbk_plan);
         None / dense_kernels=False keeps every block CSC (sparse kernels only).
@@ -155,6 +173,11 @@ class Engine:
             mk = np.ascontiguousarray(mask, dtype=np.int8)
             if self.lib.lbk_set_task_mask(ctx, len(mk), P(mk, i8p), C.byref(st)):
                 _native.raise_status(st, "lbk_set_task_mask")
+        df = defer_flags(tree) if lookahead else None
+        if df is not None:
+            self._defer = df
+            if self.lib.lbk_set_task_defer(ctx, len(df), P(df, i8p), C.byref(st)):
+                _native.raise_status(st, "lbk_set_task_defer")
         if cuts is not None:
             ct = np.ascontiguousarray(cuts, dtype=np.int8)
             if self.lib.lbk_set_cuts(ctx, len(ct), P(ct, i8p), C.byref(st)):
@@ -190,7 +213,7 @@ class Engine:
         if rc:
             _native.raise_status(st, "lbk_plan")
         self.nnz = int(pl.values.shape[0])
-        info = np.zeros(12, np.int64)
+        info = np.zeros(14, np.int64)
         self.lib.lbk_plan_info(ctx, P(info, i64p))
         self.info = info
         self.n_launch_levels, self.n_items, self.n_diag_rows = int(info[0]), int(info[1]), int(info[2])
@@ -198,6 +221,7 @@ class Engine:
         self.nnz_work = int(info[7])
         self.n_sparse_blocks, self.n_rect_blocks, self.n_full_blocks = int(info[8]), int(info[9]), int(info[10])
         self.n_tile_items = int(info[11])
+        self.dmma_flops_executed, self.exec_flops_executed = float(info[12]), float(info[13])
         self._resident = False
 
     def close(self):

@@ -113,6 +113,59 @@ __global__ void k_left64(double* out, int iters, long long* cyc) {
   if (threadIdx.x == 0) cyc[blockIdx.x] = tot / iters;
 }
 
+__global__ void k_lub(double* out, int iters, long long* cyc) {
+  extern __shared__ double sm[];
+  double* T = sm; double* Dd = sm + XREG; double* rinv = sm + 2 * XREG;
+  long long tot = 0;
+  __shared__ long long prof[4];
+  if (threadIdx.x < 4) prof[threadIdx.x] = 0;
+  for (int it = 0; it < iters; ++it) {
+    for (int i = threadIdx.x; i < XT * XTP; i += blockDim.x) T[i] = (i % 65 == i / 65) ? 100.0 : 1e-3 * ((i * 7) % 13);
+    __syncthreads();
+    long long t0 = clock64();
+    tile_lu64_blocked(T, 64, Dd, rinv, blockIdx.x == 0 ? prof : nullptr);
+    tot += clock64() - t0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0)
+    printf("lu64_blocked phases per call: panel %lld  U12 %lld  A22 %lld  sync %lld cycles\n", prof[0] / iters,
+           prof[1] / iters, prof[2] / iters, prof[3] / iters);
+  out[blockIdx.x * 4096 + threadIdx.x] = T[threadIdx.x];
+  if (threadIdx.x == 0) cyc[blockIdx.x] = tot / iters;
+}
+
+__global__ void k_rblk(double* out, int iters, long long* cyc) {
+  extern __shared__ double sm[];
+  double* X = sm; double* U = sm + XREG; double* rinv = sm + 3 * XREG; double* Dd = sm + 2 * XREG;
+  for (int i = threadIdx.x; i < XT * XTP; i += blockDim.x) U[i] = 1.0 + 1e-3 * ((i * 7) % 13);
+  if (threadIdx.x < 64) rinv[threadIdx.x] = 0.9;
+  long long tot = 0;
+  for (int it = 0; it < iters; ++it) {
+    for (int i = threadIdx.x; i < XT * XTP; i += blockDim.x) X[i] = 1e-3 * (i % 11);
+    __syncthreads();
+    long long t0 = clock64();
+    tile_right_solve_blk<true>(X, U, rinv, Dd, 64);
+    tot += clock64() - t0;
+  }
+  out[blockIdx.x * 4096 + threadIdx.x] = X[threadIdx.x];
+  if (threadIdx.x == 0) cyc[blockIdx.x] = tot / iters;
+}
+
+__global__ void k_lblk(double* out, int iters, long long* cyc) {
+  extern __shared__ double sm[];
+  double* X = sm; double* L = sm + XREG;
+  for (int i = threadIdx.x; i < XT * XTP; i += blockDim.x) L[i] = 1e-3 * ((i * 7) % 13);
+  long long tot = 0;
+  for (int it = 0; it < iters; ++it) {
+    for (int i = threadIdx.x; i < XT * XTP; i += blockDim.x) X[i] = 1e-3 * (i % 11);
+    __syncthreads();
+    long long t0 = clock64();
+    tile_left_solve_blk(X, L, 64);
+    tot += clock64() - t0;
+  }
+  out[blockIdx.x * 4096 + threadIdx.x] = X[threadIdx.x];
+  if (threadIdx.x == 0) cyc[blockIdx.x] = tot / iters;
+}
+
 int main() {
   double* out; long long* cyc; long long h[148];
   cudaMalloc(&out, 148 * 4096 * 8); cudaMalloc(&cyc, 148 * 8);
@@ -124,8 +177,11 @@ int main() {
   cudaFuncSetAttribute(k_lu64, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_right64, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_left64, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const char* names[7] = {"line_left_unit_lower", "line_right_upper", "line_lu", "tile_mma_sub", "tile_lu64", "tile_right_solve64", "tile_left_solve64"};
-  for (int k = 0; k < 7; ++k) {
+  cudaFuncSetAttribute(k_lub, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_rblk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_lblk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const char* names[10] = {"line_left_unit_lower", "line_right_upper", "line_lu", "tile_mma_sub", "tile_lu64", "tile_right_solve64", "tile_left_solve64", "tile_lu64_blocked", "tile_right_solve_blk", "tile_left_solve_blk"};
+  for (int k = 0; k < 10; ++k) {
     for (int rep = 0; rep < 2; ++rep) {
       if (k == 0) k_left<<<148, 256, smem>>>(out, 50, cyc);
       if (k == 1) k_right<<<148, 256, smem>>>(out, 50, cyc);
@@ -134,6 +190,9 @@ int main() {
       if (k == 4) k_lu64<<<148, 256, smem>>>(out, 20, cyc);
       if (k == 5) k_right64<<<148, 256, smem>>>(out, 20, cyc);
       if (k == 6) k_left64<<<148, 256, smem>>>(out, 20, cyc);
+      if (k == 7) k_lub<<<148, 256, smem>>>(out, 20, cyc);
+      if (k == 8) k_rblk<<<148, 256, smem>>>(out, 20, cyc);
+      if (k == 9) k_lblk<<<148, 256, smem>>>(out, 20, cyc);
       cudaDeviceSynchronize();
     }
     cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
