@@ -210,6 +210,13 @@ int lbk_block_layout(lbk_ctx* ctx, int64_t* layout);
  * lbk_plan; NULL clears. */
 int lbk_set_task_defer(lbk_ctx* ctx, int64_t ntasks, const int8_t* defer, lbk_status* st);
 
+/* Device triangular solve on the factors of the last lbk_factorize /
+ * lbk_factorize_host of this ctx: x = U^-1 L^-1 b[perm_global]
+ * (factorize.py:451-457; L, U = the blocks LUFactors exports, :370-384).
+ * Blocked column-oriented substitution (one launch per diagonal block and
+ * one per block column of updates, graph-captured); b, x: host, length n. */
+int lbk_solve(lbk_ctx* ctx, const double* b, double* x, lbk_status* st);
+
 /* Launched-level table (4 x nlevels: item offset, items, warps, acc length)
  * and, if items != NULL, the work items (6 x total: kind, a, b, c, begin, end). */
 int lbk_plan_levels(lbk_ctx* ctx, int64_t* levels, int32_t* items);

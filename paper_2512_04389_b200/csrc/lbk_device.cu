@@ -27,6 +27,7 @@
 #include "lbk_common.cuh"
 #include "lbk_dense.cuh"
 #include "lbk_exec.cuh"
+#include "lbk_solve.cuh"
 #include "lbk_sparse.cuh"
 
 #include <array>
@@ -210,6 +211,14 @@ struct lbk_ctx {
   std::vector<int32_t> seg_begin;  // launch-level index where each segment starts (+ end sentinel)
   std::vector<int64_t> wlen;       // working entries per block
   std::vector<char> isdiag;
+  // device triangular solve (lbk_solve): block grid + lazily built graph
+  std::vector<int64_t> pos, hbi, hbj;
+  DevBuf<SolveStep> sfw, sbw;
+  DevBuf<SolveUpd> ufw, ubw;
+  DevBuf<int32_t> sbstart;
+  DevBuf<int64_t> sdgrow;
+  DevBuf<double> sb, sv;
+  cudaGraphExec_t solve_graph = nullptr;
   DevBuf<unsigned long long> xtrace;  // executor task timeline (instrumented replays only)
 };
 
@@ -312,6 +321,10 @@ int lbk_create(lbk_ctx** out, int device, lbk_status* st) {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(tile_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TGEMM_SMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, EXEC_SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(solve_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(solve_upd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_SMEM);
   c->use_exec = std::getenv("LBK_NO_EXEC") == nullptr;
   for (int k = 0; k < NBRANCH && e == cudaSuccess; ++k) {
     e = cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking);
@@ -343,6 +356,7 @@ void lbk_destroy(lbk_ctx* c) {
   if (c->fork) cudaEventDestroy(c->fork);
   for (auto ev : c->dev) cudaEventDestroy(ev);
   if (c->dstream) cudaStreamDestroy(c->dstream);
+  if (c->solve_graph) cudaGraphExecDestroy(c->solve_graph);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -356,8 +370,14 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
              const int32_t* steps, const int32_t* trows, const int32_t* tcols, const int32_t* tlevels,
              const int64_t* costs, int32_t chunk, int32_t flags, double tau, lbk_status* st) {
   if (!c) return fail(st, LBK_ERR_BAD_ARG, "null ctx");
-  (void)positions;
   LBK_CUDA(cudaSetDevice(c->device), st);
+  c->pos.assign(positions, positions + p + 1);
+  c->hbi.assign(table, table + nblocks);
+  c->hbj.assign(table + nblocks, table + 2 * nblocks);
+  if (c->solve_graph) {
+    cudaGraphExecDestroy(c->solve_graph);
+    c->solve_graph = nullptr;
+  }
   const int64_t nb = nblocks;
   const int64_t *T_bi = table, *T_bj = table + nb, *T_nr = table + 2 * nb, *T_nc = table + 3 * nb,
                 *T_nz = table + 4 * nb, *T_cp = table + 5 * nb, *T_ent = table + 6 * nb;
@@ -1352,6 +1372,109 @@ int lbk_set_perms(lbk_ctx* c, const int32_t* perms, lbk_status* st) {
   LBK_CUDA(cudaSetDevice(c->device), st);
   if (c->ndiag_rows)
     LBK_CUDA(cudaMemcpy(c->perm.p, perms, c->ndiag_rows * sizeof(int32_t), cudaMemcpyHostToDevice), st);
+  ok(st);
+  return 0;
+}
+
+}  // extern "C"
+
+namespace {
+
+// Steps + update items of the forward (L, block rows ascending) and backward
+// (U, descending) substitutions, and the graph that runs both.
+int build_solve(lbk_ctx* c, lbk_status* st) {
+  if (c->solve_graph) return 0;
+  const int64_t p = c->p, nb = c->nblocks;
+  std::vector<int64_t> bid(static_cast<size_t>(p * p), -1);
+  for (int64_t b = 0; b < nb; ++b) bid[c->hbi[b] * p + c->hbj[b]] = b;
+  std::vector<std::vector<int64_t>> bycol(p);
+  for (int64_t b = 0; b < nb; ++b) bycol[c->hbj[b]].push_back(b);
+  std::vector<SolveStep> fw, bw;
+  std::vector<SolveUpd> uf, ub;
+  int64_t maxspan = 1;
+  auto items = [&](int64_t i, bool lower, std::vector<SolveUpd>* out) {
+    for (int64_t b : bycol[i]) {
+      const int64_t k = c->hbi[b];
+      if (lower ? k <= i : k >= i) continue;
+      const BlockDev& B = c->hblk[b];
+      const int rows = B.store == STORE_SPARSE ? B.nrows : B.nR;
+      for (int r0 = 0; r0 < rows; r0 += UPD_ROWS)
+        out->push_back(SolveUpd{static_cast<int32_t>(b), static_cast<int32_t>(c->pos[k]),
+                                static_cast<int32_t>(c->pos[i]), r0});
+    }
+  };
+  for (int64_t q = 0; q < p; ++q) {
+    for (int dir = 0; dir < 2; ++dir) {
+      const int64_t i = dir == 0 ? q : p - 1 - q;
+      SolveStep S{};
+      S.diag = static_cast<int32_t>(bid[i * p + i]);
+      S.off = static_cast<int32_t>(c->pos[i]);
+      S.span = static_cast<int32_t>(c->pos[i + 1] - c->pos[i]);
+      maxspan = std::max<int64_t>(maxspan, S.span);
+      std::vector<SolveUpd>* out = dir == 0 ? &uf : &ub;
+      S.upd_off = static_cast<int64_t>(out->size());
+      items(i, dir == 0, out);
+      S.nupd = static_cast<int32_t>(out->size() - S.upd_off);
+      (dir == 0 ? fw : bw).push_back(S);
+    }
+  }
+  const size_t diag_smem = (static_cast<size_t>((maxspan + 1) & ~1LL) + SOLVE_CHUNK * 65) * sizeof(double);
+  if (diag_smem > static_cast<size_t>(MAX_SMEM)) return fail(st, LBK_ERR_BAD_ARG, "block span too large for the solve");
+  std::vector<int32_t> bstart(c->n);
+  std::vector<int64_t> dgrow(c->n);
+  for (int64_t i = 0; i < p; ++i) {
+    const BlockDev& D = c->hblk[bid[i * p + i]];
+    for (int64_t g = c->pos[i]; g < c->pos[i + 1]; ++g) {
+      bstart[g] = static_cast<int32_t>(c->pos[i]);
+      dgrow[g] = D.dg + (g - c->pos[i]);
+    }
+  }
+  LBK_CUDA(c->sfw.upload(fw), st);
+  LBK_CUDA(c->sbw.upload(bw), st);
+  LBK_CUDA(c->ufw.upload(uf), st);
+  LBK_CUDA(c->ubw.upload(ub), st);
+  LBK_CUDA(c->sbstart.upload(bstart), st);
+  LBK_CUDA(c->sdgrow.upload(dgrow), st);
+  LBK_CUDA(c->sb.alloc(c->n), st);
+  LBK_CUDA(c->sv.alloc(c->n), st);
+  DevPools P = pools(c);
+  cudaStream_t s0 = c->stream;
+  cudaGraph_t g;
+  LBK_CUDA(cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal), st);
+  solve_perm_kernel<<<148 * 4, 256, 0, s0>>>(c->sb.p, c->sv.p, c->perm.p, c->sbstart.p, c->sdgrow.p, c->n);
+  for (int dir = 0; dir < 2; ++dir) {
+    const std::vector<SolveStep>& steps = dir == 0 ? fw : bw;
+    for (size_t q = 0; q < steps.size(); ++q) {
+      const SolveStep& S = steps[q];
+      const size_t sm = (static_cast<size_t>((S.span + 1) & ~1) + SOLVE_CHUNK * 65) * sizeof(double);
+      solve_diag_kernel<<<1, 256, sm, s0>>>(P, (dir == 0 ? c->sfw.p : c->sbw.p), static_cast<int>(q), c->sv.p, dir);
+      if (S.nupd)
+        solve_upd_kernel<<<S.nupd, 256, static_cast<size_t>(S.span) * sizeof(double), s0>>>(
+            P, (dir == 0 ? c->ufw.p : c->ubw.p) + S.upd_off, c->sv.p);
+    }
+  }
+  cudaError_t e = cudaStreamEndCapture(s0, &g);
+  if (e != cudaSuccess) return cuda_fail(st, e, "solve graph capture");
+  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&c->solve_graph, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_fail(st, e, "solve graph");
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+// x = U^-1 L^-1 b[perm_global] on the factors of the last factorization
+// (factorize.py:451-457); host vectors of length n in and out.
+int lbk_solve(lbk_ctx* c, const double* b, double* x, lbk_status* st) {
+  LBK_CUDA(cudaSetDevice(c->device), st);
+  if (build_solve(c, st)) return st->code;
+  LBK_CUDA(cudaMemcpyAsync(c->sb.p, b, c->n * sizeof(double), cudaMemcpyHostToDevice, c->stream), st);
+  LBK_CUDA(cudaGraphLaunch(c->solve_graph, c->stream), st);
+  LBK_CUDA(cudaMemcpyAsync(x, c->sv.p, c->n * sizeof(double), cudaMemcpyDeviceToHost, c->stream), st);
+  LBK_CUDA(cudaStreamSynchronize(c->stream), st);
   ok(st);
   return 0;
 }

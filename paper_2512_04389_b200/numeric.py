@@ -75,6 +75,7 @@ def _dev():
     d(lib, "lbk_set_task_mask", C.c_int, [vp, C.c_int64, i8p, st])
     d(lib, "lbk_set_cuts", C.c_int, [vp, C.c_int64, i8p, st])
     d(lib, "lbk_set_task_defer", C.c_int, [vp, C.c_int64, i8p, st])
+    d(lib, "lbk_solve", C.c_int, [vp, f64p, f64p, st])
     d(lib, "lbk_num_segments", C.c_int, [vp])
     d(lib, "lbk_run_segment", C.c_int, [vp, C.c_int32, C.c_double, C.c_double, st])
     d(lib, "lbk_finish_raw", C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(C.c_uint64), st])
@@ -223,6 +224,19 @@ class Engine:
         self.n_tile_items = int(info[11])
         self.dmma_flops_executed, self.exec_flops_executed = float(info[12]), float(info[13])
         self._resident = False
+        self.generation = 0  # bumped by every factorization: device factors of LUFactors stay valid until then
+
+    def solve(self, b) -> np.ndarray:
+        """x = U^-1 L^-1 b[perm_global] on the device-resident factors of the
+        last factorization (factorize.py:451-457)."""
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        if b.shape != (self.grid.n,):
+            raise DimensionMismatch(f"rhs must have length {self.grid.n}")
+        x = np.empty(self.grid.n, np.float64)
+        st = _native.LbkStatus()
+        if self.lib.lbk_solve(self.ctx, P(b, f64p), P(x, f64p), C.byref(st)):
+            _native.raise_status(st, "lbk_solve")
+        return x
 
     def close(self):
         if getattr(self, "ctx", None):
@@ -254,6 +268,7 @@ class Engine:
             self.upload()
         ms = C.c_float()
         st = _native.LbkStatus()
+        self.generation += 1
         self.lib.lbk_factorize(self.ctx, pivot_tol, self._eps(static_pivot, self.grid.value_max),
                                C.byref(ms), C.byref(st))
         _native.raise_status(st, "lbk_factorize")
@@ -262,6 +277,7 @@ class Engine:
     def run_host(self, a_values, out_values, out_perms, pivot_tol=DEFAULT_PIVOT_TOL, static_pivot=None):
         """End-to-end: host values in -> host factor values + perms out. Returns lbk_status."""
         st = _native.LbkStatus()
+        self.generation += 1
         self.lib.lbk_factorize_host(self.ctx, P(a_values, f64p), P(out_values, f64p),
                                     P(out_perms, i32p) if out_perms is not None else None,
                                     pivot_tol, self._eps(static_pivot, self.grid.value_max), C.byref(st))
@@ -391,6 +407,7 @@ class LUFactors:
     u_blocks: dict
     perms: list
     _assembled: dict = field(default_factory=dict, repr=False)
+    _device: tuple | None = field(default=None, repr=False)  # (Engine, generation) holding these factors
 
     def perm_global(self) -> np.ndarray:
         if "perm" not in self._assembled:
@@ -545,8 +562,11 @@ def factorize(grid, tree, workers: int = 1, pivot_tol: float = DEFAULT_PIVOT_TOL
             continue
         _native.raise_status(st, "factorize")
         if dense:
-            return build_factors_full(grid, eng.pool, eng.download_work(), perms[: eng.n_diag_rows])
-        return build_factors(grid, eng.pool, out, perms[: eng.n_diag_rows])
+            lu = build_factors_full(grid, eng.pool, eng.download_work(), perms[: eng.n_diag_rows])
+        else:
+            lu = build_factors(grid, eng.pool, out, perms[: eng.n_diag_rows])
+        lu._device = (eng, eng.generation)
+        return lu
     raise DeviceError("unreachable")  # pragma: no cover
 
 
@@ -567,10 +587,25 @@ def residual(a: CscMatrix, f: LUFactors) -> float:
 
 
 def solve(f: LUFactors, b) -> np.ndarray:
-    """x = U^-1 L^-1 b[perm] (factorize.py:451-457)."""
+    """x = U^-1 L^-1 b[perm] (factorize.py:451-457).
+
+    Factors returned by ``factorize`` are still resident on the device: the
+    solve runs there (lbk_solve, blocked substitution on the factor blocks)
+    while no later factorization has overwritten them.  Otherwise (factors
+    built on the host, or stale) it is the reference's host solve."""
     b = np.asarray(b, dtype=np.float64)
     if b.shape != (f.n,):
         raise DimensionMismatch(f"rhs must have length {f.n}")
+    if f._device is not None:
+        eng, gen = f._device
+        if eng.ctx is not None and eng.generation == gen:
+            return eng.solve(b)
+    return solve_host(f, b)
+
+
+def solve_host(f: LUFactors, b) -> np.ndarray:
+    """The reference's host solve (scipy spsolve_triangular on the assembled CSR)."""
+    b = np.asarray(b, dtype=np.float64)
     y = spsolve_triangular(f.l_matrix(), b[f.perm_global()], lower=True)
     return spsolve_triangular(f.u_matrix(), y, lower=False)
 

@@ -1,0 +1,90 @@
+"""Device triangular solve (lbk_solve) vs the reference's host solve.
+
+solve(f, b) runs on the device while the factors produced by factorize are
+still resident (factorize.py:451-457 semantics: x = U^-1 L^-1 b[perm_global]
+on the exported blocks).  Bar: same solution as the host solve within 1e-10
+relative, and ||Ax - b||/||b|| no worse than the host solve's (x10 slack for
+the different summation order, floor 1e-14).
+"""
+
+import numpy as np
+import pytest
+
+import paper_2512_04389_b200 as M
+from conftest import load_small
+from paper_2512_04389_b200 import generators as G
+from paper_2512_04389_b200.matrix_io import generate
+from paper_2512_04389_b200.numeric import solve_host
+
+pytestmark = pytest.mark.gpu
+
+
+def pipeline(a, bs=None):
+    f = M.symbolic_factorize(M.symmetrize_pattern(a))
+    pl = (M.irregular_plan(M.percentage_curve(M.diag_block_pointer(f)), a.n) if bs is None
+          else M.regular_plan(a.n, bs))
+    g = M.partition(f, a, pl)
+    return g, M.dependency_levels(g)
+
+
+CASES = {
+    "C1": (lambda: G.poisson2d(64), None, {}),
+    "C1_reg200": (lambda: G.poisson2d(64), 200, {}),
+    "p3d16": (lambda: G.poisson3d(16, "nd"), None, {}),
+    "bbd20k": (lambda: G.bbd(20000, 400, 20, seed=1), None, {}),
+    "arrow": (lambda: generate("arrowhead", 1000, b=100), None, {}),
+    "randspd": (lambda: generate("random_spd", 3000, bandwidth=20, density=0.3), None, {}),
+    "p3d12_csc": (lambda: G.poisson3d(12, "nd"), None, {"dense_threshold": None}),
+}
+
+
+def check(a, lu, b):
+    xd = M.solve(lu, b)
+    xh = solve_host(lu, b)
+    A = a.to_scipy()
+    rd = float(np.linalg.norm(A @ xd - b) / np.linalg.norm(b))
+    rh = float(np.linalg.norm(A @ xh - b) / np.linalg.norm(b))
+    assert np.linalg.norm(xd - xh) <= 1e-10 * np.linalg.norm(xh), (rd, rh)
+    assert rd <= max(10 * rh, 1e-14), (rd, rh)
+    return rd
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_device_solve_matches_host(name):
+    mk, bs, kw = CASES[name]
+    a = mk()
+    g, t = pipeline(a, bs)
+    lu = M.factorize(g, t, **kw)
+    assert lu._device is not None
+    rng = np.random.default_rng(3)
+    check(a, lu, a.to_scipy() @ np.ones(a.n))
+    check(a, lu, rng.standard_normal(a.n))
+
+
+@pytest.mark.parametrize("idx", [14, 15, 16, 18, 21])
+def test_device_solve_with_pivot_swaps(idx):
+    """Golden small cases whose diagonal blocks pivot (dense-scratch re-run):
+    the solve must apply perm_global and the unpermuted-L quirk like the host."""
+    d = load_small(idx)
+    a = M.CscMatrix(int(d["n"]), d["a_col_ptr"], d["a_row_idx"], d["a_values"])
+    f = M.symbolic_factorize(M.symmetrize_pattern(a))
+    g = M.partition(f, a, M.BlockingPlan(a.n, np.asarray(d["positions"], np.int64), "given"))
+    t = M.dependency_levels(g)
+    sp = float(d["static_pivot"][0])
+    lu = M.factorize(g, t, static_pivot=None if np.isnan(sp) else sp)
+    b = np.arange(1, a.n + 1, dtype=np.float64)
+    xd = M.solve(lu, b)
+    xh = solve_host(lu, b)
+    np.testing.assert_allclose(xd, xh, rtol=1e-9, atol=1e-12 * np.abs(xh).max())
+
+
+def test_stale_factors_fall_back_to_host():
+    a = G.poisson2d(24)
+    g, t = pipeline(a)
+    lu1 = M.factorize(g, t)
+    eng, gen = lu1._device
+    lu2 = M.factorize(g, t)  # same cached engine: lu1's device copy is overwritten
+    assert lu2._device[0] is eng and eng.generation != gen
+    b = a.to_scipy() @ np.ones(a.n)
+    np.testing.assert_allclose(M.solve(lu1, b), solve_host(lu1, b), rtol=0, atol=0)
+    check(a, lu2, b)
