@@ -122,8 +122,8 @@ struct ExecBuilder {
   // GEMMs feeding them overtake the bulk trailing updates of the current
   // step, which a plain step-major order would dequeue first.
   static int cost_of(int type) {
-    static const int c[10] = {150, 360, 180, 130, 64, 60, 130, 64, 180, 64};
-    return type >= 0 && type < 10 ? c[type] : 64;
+    static const int c[11] = {150, 360, 180, 130, 64, 60, 130, 64, 180, 64, 100000};
+    return type >= 0 && type < 11 ? c[type] : 64;
   }
   void flush(Level* L, std::vector<XTask>* tasks, std::vector<int32_t>* sptr, std::vector<int32_t>* succ,
              std::vector<int32_t>* deps0) {
@@ -842,6 +842,22 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           const int64_t b = tgetrf[lv][q];
           const int m = hb[b].nrows, nt = (m + XT - 1) / XT;
           const int32_t stp = static_cast<int32_t>(T_bi[b]);
+          if (!all_full && m > 2 * XT) {
+            // banded diagonal block: one sweeping task instead of the tile DAG
+            int bl = 0, bu = 0;
+            const int64_t* scp = colptr + T_cp[b];
+            const int64_t* sri = rowidx + T_ent[b];
+            for (int col = 0; col < m; ++col)
+              for (int64_t e = scp[col]; e < scp[col + 1]; ++e) {
+                const int r = static_cast<int>(sri[e]);
+                bl = std::max(bl, r - col);
+                bu = std::max(bu, col - r);
+              }
+            if (bl <= BAND_MAX && bu <= BAND_MAX) {
+              X.add(X_BAND, b, b, bl, bu, 0, stp, 0, {});
+              continue;
+            }
+          }
           // column maxima at GETRF entry: tasks over (column tile, row chunk of
           // COLMAX_ROWS); every first write into column tile c waits for all of
           // column c's colmax tasks

@@ -49,6 +49,7 @@ enum XType : int8_t {
   X_PG_UPD = 7,  // tile (r,c) -= L[R_r, R_k] tile(k,c)
   X_PT_DIAG = 8, // TSTRF panel a (cols C_X): tile (r,c) <- tile U[C_c,C_c]^{-1}
   X_PT_UPD = 9,  // tile (r,c) -= tile(r,k) U[C_k, C_c]
+  X_BAND = 10,   // whole LU of a banded FULL diagonal block a (r = lower, c = upper bandwidth <= 15)
 };
 
 struct XTask {
@@ -769,6 +770,85 @@ __device__ __forceinline__ void stamp(unsigned long long* ph, int k) {
   }
 }
 
+// ---- banded diagonal blocks -------------------------------------------------------
+// A FULL diagonal block whose filled pattern lies inside a narrow band (lower
+// bandwidth bl, upper bu <= 15: e.g. the bodies of bordered-block-diagonal
+// matrices) needs no tile DAG: its LU never leaves the band, so one CTA sweeps
+// the columns with the band staged in shared memory (diagonal storage,
+// CHUNK columns at a time + the bw-column overlap), one barrier per column:
+// thread (i, j) updates entry (k+i, k+j) of step k.  Pivot rule exactly as
+// the tile path (factorize.py:38-78): colmax at entry over the band, |d_ik|
+// before scaling staged per column, the verdict per chunk.  Rows outside the
+// band are structural zeros, so they can neither be a pivot nor change colmax.
+constexpr int BAND_MAX = 15;
+constexpr int BAND_CH = 128;
+
+static_assert(((BAND_CH + BAND_MAX) * (2 * BAND_MAX + 1) + 2 * BAND_CH * 16) * 8 <= EXEC_SMEM, "band smem");
+
+__device__ void band_getrf(const BlockDev& A, const DevPools& P, double* sm, int bl, int bu, int step,
+                           double pivot_tol) {
+  const int m = A.nrows, W = bl + bu + 1, bw = max(bl, bu), tid = threadIdx.x;
+  double* G = P.vals + A.ent;
+  double* Bs = sm;                                   // (BAND_CH + bw) x W band values
+  double* S = sm + (BAND_CH + BAND_MAX) * (2 * BAND_MAX + 1);  // BAND_CH x 16 staged |d|
+  double* Lc = S + BAND_CH * 16;                     // BAND_CH x 16 multipliers
+  double* colmax = P.colmax + A.dg;
+  for (int c = tid; c < m; c += blockDim.x) {
+    double mx = 0.0;
+    const int r1 = min(m - 1, c + bl);
+    for (int r = max(0, c - bu); r <= r1; ++r) mx = fmax(mx, fabs(ldcg(G + static_cast<size_t>(c) * m + r)));
+    colmax[c] = mx;
+  }
+  // band entry (r, c) -> Bs[(c - c0) * W + (r - c + bu)]
+  const int i = tid >> 4, j = tid & 15;
+  for (int c0 = 0; c0 < m; c0 += BAND_CH) {
+    const int ce = min(m, c0 + BAND_CH + bw), kend = min(m, c0 + BAND_CH);
+    __syncthreads();
+    for (int idx = tid; idx < (ce - c0) * W; idx += blockDim.x) {
+      const int c = c0 + idx / W, r = c - bu + idx % W;
+      Bs[idx] = (r >= 0 && r < m) ? ldcg(G + static_cast<size_t>(c) * m + r) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 1
+    for (int k = c0; k < kend; ++k) {
+      const double* colk = Bs + (k - c0) * W + bu;  // (k + i, k) = colk[i]
+      const double u = colk[0];
+      const bool act = i >= 1 && i <= bl && k + i < m;
+      if (act) {
+        const double d = colk[i];
+        const double l = d * rcp_nr(u);
+        if (j == 0) {
+          S[(k - c0) * 16 + i] = fabs(d);
+          Lc[(k - c0) * 16 + i] = l;
+        } else if (j <= bu && k + j < m) {
+          double* e = Bs + (k + j - c0) * W + (i - j + bu);  // (k + i, k + j)
+          const double urow = Bs[(k + j - c0) * W + (bu - j)];  // (k, k + j)
+          *e = fma(-l, urow, *e);
+        }
+      }
+      __syncthreads();
+    }
+    // multipliers into the band, pivot verdict of the chunk's columns, write-back
+    for (int idx = tid; idx < (kend - c0) * 16; idx += blockDim.x) {
+      const int kk = idx >> 4, ii = idx & 15;
+      if (ii >= 1 && ii <= bl && c0 + kk + ii < m) Bs[kk * W + bu + ii] = Lc[idx];
+    }
+    for (int k = c0 + tid; k < kend; k += blockDim.x) {
+      const double uk = Bs[(k - c0) * W + bu];
+      double below = 0.0;
+      for (int ii = 1; ii <= bl && k + ii < m; ++ii) below = fmax(below, S[(k - c0) * 16 + ii]);
+      const double piv = fmax(fabs(uk), below);
+      if (piv == 0.0 || piv < pivot_tol * colmax[k] || isnan(uk)) record(&P.err[0], step, k);
+      else if (below > fabs(uk)) record(&P.err[1], step, k);
+    }
+    __syncthreads();
+    for (int idx = tid; idx < (ce - c0) * W; idx += blockDim.x) {
+      const int c = c0 + idx / W, r = c - bu + idx % W;
+      if (r >= 0 && r < m) G[static_cast<size_t>(c) * m + r] = Bs[idx];
+    }
+  }
+}
+
 __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double pivot_tol,
                          unsigned long long* ph = nullptr) {
   double* T0 = sm;                  // target tile (XTP stride)
@@ -925,6 +1005,9 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       }
       break;
     }
+    case X_BAND:
+      band_getrf(A, P, sm, tk.r, tk.c, tk.step, pivot_tol);
+      break;
     default:
       break;
   }
