@@ -856,7 +856,6 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
   double* T2 = sm + 2 * XREG;       // DMMA B (XS stride)
   double* rinv = sm + 3 * XREG;     // XT doubles
   const BlockDev A = P.blk[tk.a];
-  Line X;
   switch (tk.type) {
     case X_COLMAX: {  // rows [r*COLMAX_ROWS, ...) of column tile c: atomic max into colmax
       const int m = A.nrows, c0 = tk.c * XT, nc = min(XT, m - c0);

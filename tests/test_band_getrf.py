@@ -69,12 +69,12 @@ def test_band_zero_pivot_location():
     rng = np.random.default_rng(7)
     n = 600
     a = banded(n, 3, 3, rng, zero_at=None)
-    # make column 417 structurally present but numerically singular at its step:
-    # zero its diagonal and every entry below it in the band
+    # decouple row and column 417 and zero its diagonal: the column is exactly
+    # zero at its elimination step (the symmetrized pattern keeps a 0.0 diagonal)
     d = a.to_scipy().tolil()
-    d[417, 417] = 0.0
-    for r in range(418, 421):
-        d[r, 417] = 0.0
+    for q in range(n):
+        d[417, q] = 0.0
+        d[q, 417] = 0.0
     d = d.tocsc()
     a = M.CscMatrix(n, d.indptr.astype(np.int64), d.indices.astype(np.int64), d.data)
     g, t, og = run_both(a, [0, 300, n])
