@@ -592,13 +592,43 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     std::vector<int32_t> pan_smem(nlevels, 0), exa_smem(nlevels, 0);
     std::vector<std::vector<int64_t>> tgetrf(nlevels);  // FULL diagonal blocks factored by the tiled GETRF
     c->route.assign(ntasks, -1);
-    auto add_range = [&](int32_t lv, Item base, int32_t count) {
-      for (int32_t s = 0; s < count; s += chunk) {
+    // items of `chunk` NONEMPTY columns/rows each (the kernels skip empty ones
+    // in a few instructions; a CTA per 8 positions of a 2000-wide, 2%-occupied
+    // panel would launch 250 CTAs with 64 KB accumulators for nothing)
+    auto add_range = [&](int32_t lv, Item base, int32_t count, const std::vector<char>& nonempty) {
+      int32_t s = 0, have = 0;
+      for (int32_t x = 0; x < count; ++x) {
+        if (!nonempty[x]) {
+          if (have == 0) s = x + 1;
+          continue;
+        }
+        if (++have == chunk) {
+          Item it = base;
+          it.begin = s;
+          it.end = x + 1;
+          gen[lv].push_back(it);
+          s = x + 1;
+          have = 0;
+        }
+      }
+      if (have) {
         Item it = base;
         it.begin = s;
-        it.end = std::min(count, s + chunk);
+        it.end = count;
         gen[lv].push_back(it);
       }
+    };
+    auto col_nonempty = [&](int64_t b) {
+      std::vector<char> v(hb[b].ncols, 0);
+      const int64_t* scp = colptr + T_cp[b];
+      for (int x = 0; x < hb[b].ncols; ++x) v[x] = scp[x + 1] > scp[x];
+      return v;
+    };
+    auto row_nonempty = [&](int64_t b) {
+      std::vector<char> v(hb[b].nrows, 0);
+      const int64_t* sri = rowidx + T_ent[b];
+      for (int64_t e = 0; e < T_nz[b]; ++e) v[sri[e]] = 1;
+      return v;
     };
     auto tile_like = [&](int64_t b) { return hb[b].store != STORE_SPARSE; };
     for (int64_t t = 0; t < ntasks; ++t) {
@@ -643,7 +673,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         }
         acc_len[lv] = std::max(acc_len[lv], hb[x].nrows);
         c->route[t] = 0;
-        add_range(lv, it, hb[x].ncols);
+        add_range(lv, it, hb[x].ncols, col_nonempty(x));
       } else if (kind == KIND_TSTRF) {
         const int64_t x = bid[r * p + i];
         it.a = static_cast<int32_t>(dblk);
@@ -660,7 +690,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           return fail(st, LBK_ERR_BAD_ARG, "TSTRF operand without a CSR index");
         acc_len[lv] = std::max(acc_len[lv], hb[x].ncols);
         c->route[t] = 0;
-        add_range(lv, it, hb[x].nrows);
+        add_range(lv, it, hb[x].nrows, row_nonempty(x));
       } else {
         const int64_t tgt = bid[r * p + cc];
         if (tgt < 0) {
@@ -726,7 +756,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         }
         acc_len[lv] = std::max(acc_len[lv], hb[tgt].nrows);
         c->route[t] = 0;
-        add_range(lv, it, hb[tgt].ncols);
+        add_range(lv, it, hb[tgt].ncols, col_nonempty(ub));
       }
     }
     // ---- flatten ---------------------------------------------------------------------
@@ -853,8 +883,27 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
                 bl = std::max(bl, r - col);
                 bu = std::max(bu, col - r);
               }
-            if (bl <= BAND_MAX && bu <= BAND_MAX) {
-              X.add(X_BAND, b, b, bl, bu, 0, stp, 0, {});
+            if (bl <= BAND_MAX && bu <= BAND_MAX && m <= 32767) {
+              // independent segments: cut before column s when no entry couples
+              // [.., s) with [s, ..) (block-diagonal bodies inside one block)
+              std::vector<int> lo(m, m);  // lowest row/col index coupled to index x from the other side
+              for (int col = 0; col < m; ++col)
+                for (int64_t e = scp[col]; e < scp[col + 1]; ++e) {
+                  const int r = static_cast<int>(sri[e]);
+                  const int a0 = std::min(r, col), a1 = std::max(r, col);
+                  lo[a1] = std::min(lo[a1], a0);
+                }
+              // segment boundary at s iff min over x >= s of lo[x] >= s
+              std::vector<int> sufmin(m + 1, m);
+              for (int x = m - 1; x >= 0; --x) sufmin[x] = std::min(sufmin[x + 1], lo[x]);
+              int s0 = 0;
+              for (int s1 = 1; s1 <= m; ++s1) {
+                const bool boundary = s1 == m || (sufmin[s1] >= s1 && s1 - s0 >= 64);
+                if (boundary) {
+                  X.add(X_BAND, b, s0, bl, bu, s1 - s0, stp, 0, {});
+                  s0 = s1;
+                }
+              }
               continue;
             }
           }

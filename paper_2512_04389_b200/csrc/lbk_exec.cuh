@@ -49,7 +49,7 @@ enum XType : int8_t {
   X_PG_UPD = 7,  // tile (r,c) -= L[R_r, R_k] tile(k,c)
   X_PT_DIAG = 8, // TSTRF panel a (cols C_X): tile (r,c) <- tile U[C_c,C_c]^{-1}
   X_PT_UPD = 9,  // tile (r,c) -= tile(r,k) U[C_k, C_c]
-  X_BAND = 10,   // whole LU of a banded FULL diagonal block a (r = lower, c = upper bandwidth <= 15)
+  X_BAND = 10,   // LU of an independent segment [d, d + k) of a banded FULL diagonal block a (r, c = bandwidths)
 };
 
 struct XTask {
@@ -785,18 +785,20 @@ constexpr int BAND_CH = 128;
 
 static_assert(((BAND_CH + BAND_MAX) * (2 * BAND_MAX + 1) + 2 * BAND_CH * 16) * 8 <= EXEC_SMEM, "band smem");
 
-__device__ void band_getrf(const BlockDev& A, const DevPools& P, double* sm, int bl, int bu, int step,
+// Segment [s0, s0 + m) of the block: independent of the rest of the block
+// (no band entry crosses its ends), so it is factored on its own.
+__device__ void band_getrf(const BlockDev& A, const DevPools& P, double* sm, int bl, int bu, int s0, int m, int step,
                            double pivot_tol) {
-  const int m = A.nrows, W = bl + bu + 1, bw = max(bl, bu), tid = threadIdx.x;
-  double* G = P.vals + A.ent;
+  const int ld = A.nrows, W = bl + bu + 1, bw = max(bl, bu), tid = threadIdx.x;
+  double* G = P.vals + A.ent + static_cast<size_t>(s0) * ld + s0;
   double* Bs = sm;                                   // (BAND_CH + bw) x W band values
   double* S = sm + (BAND_CH + BAND_MAX) * (2 * BAND_MAX + 1);  // BAND_CH x 16 staged |d|
   double* Lc = S + BAND_CH * 16;                     // BAND_CH x 16 multipliers
-  double* colmax = P.colmax + A.dg;
+  double* colmax = P.colmax + A.dg + s0;
   for (int c = tid; c < m; c += blockDim.x) {
     double mx = 0.0;
     const int r1 = min(m - 1, c + bl);
-    for (int r = max(0, c - bu); r <= r1; ++r) mx = fmax(mx, fabs(ldcg(G + static_cast<size_t>(c) * m + r)));
+    for (int r = max(0, c - bu); r <= r1; ++r) mx = fmax(mx, fabs(ldcg(G + static_cast<size_t>(c) * ld + r)));
     colmax[c] = mx;
   }
   // band entry (r, c) -> Bs[(c - c0) * W + (r - c + bu)]
@@ -806,7 +808,7 @@ __device__ void band_getrf(const BlockDev& A, const DevPools& P, double* sm, int
     __syncthreads();
     for (int idx = tid; idx < (ce - c0) * W; idx += blockDim.x) {
       const int c = c0 + idx / W, r = c - bu + idx % W;
-      Bs[idx] = (r >= 0 && r < m) ? ldcg(G + static_cast<size_t>(c) * m + r) : 0.0;
+      Bs[idx] = (r >= 0 && r < m) ? ldcg(G + static_cast<size_t>(c) * ld + r) : 0.0;
     }
     __syncthreads();
 #pragma unroll 1
@@ -838,13 +840,13 @@ __device__ void band_getrf(const BlockDev& A, const DevPools& P, double* sm, int
       double below = 0.0;
       for (int ii = 1; ii <= bl && k + ii < m; ++ii) below = fmax(below, S[(k - c0) * 16 + ii]);
       const double piv = fmax(fabs(uk), below);
-      if (piv == 0.0 || piv < pivot_tol * colmax[k] || isnan(uk)) record(&P.err[0], step, k);
-      else if (below > fabs(uk)) record(&P.err[1], step, k);
+      if (piv == 0.0 || piv < pivot_tol * colmax[k] || isnan(uk)) record(&P.err[0], step, s0 + k);
+      else if (below > fabs(uk)) record(&P.err[1], step, s0 + k);
     }
     __syncthreads();
     for (int idx = tid; idx < (ce - c0) * W; idx += blockDim.x) {
       const int c = c0 + idx / W, r = c - bu + idx % W;
-      if (r >= 0 && r < m) G[static_cast<size_t>(c) * m + r] = Bs[idx];
+      if (r >= 0 && r < m) G[static_cast<size_t>(c) * ld + r] = Bs[idx];
     }
   }
 }
@@ -1005,7 +1007,7 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       break;
     }
     case X_BAND:
-      band_getrf(A, P, sm, tk.r, tk.c, tk.step, pivot_tol);
+      band_getrf(A, P, sm, tk.r, tk.c, tk.d, tk.k, tk.step, pivot_tol);
       break;
     default:
       break;
