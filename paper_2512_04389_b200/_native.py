@@ -17,7 +17,7 @@ from . import errors
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
 HOST_LIB = os.path.join(LIB_DIR, "liblbk_host.so")
-DEV_LIB = os.path.join(LIB_DIR, "liblbk.so")
+DEV_LIB = os.environ.get("LBK_DEV_LIB") or os.path.join(LIB_DIR, "liblbk.so")  # override: experiments only
 
 LBK_OK = 0
 LBK_ERR_ZERO_PIVOT = 1

@@ -28,7 +28,13 @@
 
 namespace lbk {
 
-constexpr int GBM = 128, GBN = 64, GBK = 16, GSTAGES = 3;
+#ifndef LBK_GBK
+#define LBK_GBK 16
+#endif
+#ifndef LBK_GSTAGES
+#define LBK_GSTAGES 3
+#endif
+constexpr int GBM = 128, GBN = 64, GBK = LBK_GBK, GSTAGES = LBK_GSTAGES;
 constexpr int SA = GBM + 4;  // padded k-column stride of the A tile (conflict-free fragment loads)
 constexpr int SB = GBK + 4;  // padded n-column stride of the B tile
 constexpr int GEMM_SMEM = GSTAGES * (GBK * SA + GBN * SB) * 8;

@@ -592,17 +592,30 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     std::vector<int32_t> pan_smem(nlevels, 0), exa_smem(nlevels, 0);
     std::vector<std::vector<int64_t>> tgetrf(nlevels);  // FULL diagonal blocks factored by the tiled GETRF
     c->route.assign(ntasks, -1);
-    // items of `chunk` NONEMPTY columns/rows each (the kernels skip empty ones
+    // items of min(chunk, warps) NONEMPTY columns/rows each (the kernels skip empty ones
     // in a few instructions; a CTA per 8 positions of a 2000-wide, 2%-occupied
     // panel would launch 250 CTAs with 64 KB accumulators for nothing)
-    auto add_range = [&](int32_t lv, Item base, int32_t count, const std::vector<char>& nonempty) {
+    // materialized after the task loop, when the level's warps per CTA are
+    // known: one nonempty column/row per warp and item
+    struct PendingRange {
+      int32_t lv;
+      Item base;
+      int32_t count;
+      std::vector<char> nonempty;
+    };
+    std::vector<PendingRange> pending_ranges;
+    auto add_range = [&](int32_t lv, Item base, int32_t count, std::vector<char> nonempty) {
+      pending_ranges.push_back(PendingRange{lv, base, count, std::move(nonempty)});
+    };
+    auto emit_range = [&](int32_t lv, Item base, int32_t count, const std::vector<char>& nonempty,
+                          int32_t chunk_nz) {
       int32_t s = 0, have = 0;
       for (int32_t x = 0; x < count; ++x) {
         if (!nonempty[x]) {
           if (have == 0) s = x + 1;
           continue;
         }
-        if (++have == chunk) {
+        if (++have == chunk_nz) {
           Item it = base;
           it.begin = s;
           it.end = x + 1;
@@ -759,6 +772,9 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         add_range(lv, it, hb[tgt].ncols, col_nonempty(ub));
       }
     }
+    for (const PendingRange& pr : pending_ranges)
+      emit_range(pr.lv, pr.base, pr.count, pr.nonempty, std::min(chunk, choose_warps(acc_len[pr.lv])));
+    pending_ranges.clear();
     // ---- flatten ---------------------------------------------------------------------
     std::vector<Item> gall;
     std::vector<GemmItem> mall;
