@@ -141,7 +141,10 @@ def dist_init(backend=None):
             backend = "nccl" if torch.cuda.is_available() else "gloo"
         if backend == "nccl":
             torch.cuda.set_device(local)
-        dist.init_process_group(backend)
+        import datetime
+
+        # a hung exchange aborts through the NCCL watchdog instead of hanging the job
+        dist.init_process_group(backend, timeout=datetime.timedelta(minutes=10))
     return world, rank, local
 
 
@@ -248,10 +251,26 @@ def main():
     t0 = time.perf_counter()
     dt = None if args.dense_threshold < 0 else args.dense_threshold
     distributed = world > 1 and not args.replicas
+    dist_error = None
     if distributed:
         from paper_2512_04389_b200.parallel import DistEngine
 
-        de = DistEngine(g, t, device=local, dense_threshold=dt)
+        try:
+            de = DistEngine(g, t, device=local, dense_threshold=dt)
+            de.upload()
+            de.run()  # one trial factorization: the exchange must work before we time it
+        except Exception as exc:  # reported in the JSON line; the job then runs replicas
+            dist_error = f"{type(exc).__name__}: {exc}"[:300]
+            log(f"[bench] distributed path failed on rank {rank}: {dist_error}")
+        flags = max_over_ranks(1.0 if dist_error else 0.0, world)
+        if flags > 0:
+            distributed = False
+            dist_error = dist_error or "failed on another rank"
+            try:
+                de.close()
+            except Exception:
+                pass
+    if distributed:
         eng = de.eng
 
         def run_dev():
@@ -354,7 +373,9 @@ def main():
     traffic = None
     tp = os.path.join(REPO, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("dram_bytes_per_launch")
+        tr = json.load(open(tp)).get("dram_bytes_per_launch")
+        # per kernel (ncu dram__bytes_read.sum + dram__bytes_write.sum, averaged over launches)
+        traffic = tr.get(D["kernel"].split(" ")[0]) if isinstance(tr, dict) else tr
     roof.update({"traffic": traffic, "kernel": D["kernel"], "launches_per_step": D["launches"],
                  "algorithmic": "flops = 2*tree.costs (SSSSM), GETRF/panel formulas of SURVEY 8d; "
                                 "bytes = 8 B/value + 4 B/index per touched block",
@@ -384,7 +405,9 @@ def main():
                        else args.config, "plan": args.plan, "n": a.n, "nnz_A": a.nnz, "nnz_filled": f.nnz_filled,
                        "p": g.p, "tasks": t.task_count, "levels": t.n_levels, "gflop": total_flops / 1e9,
                        "parallelism": (f"2d-block-cyclic {de.pg.pr}x{de.pg.pc} (NCCL p2p)" if distributed
-                                       else f"replicas{world}" if world > 1 else "single"),
+                                       else (f"replicas{world}" + (f" (2d-block-cyclic failed: {dist_error})"
+                                                                   if dist_error else ""))
+                                       if world > 1 else "single"),
                        "l2": "inputs (factor values, %.2f GB) larger than L2; values restored by a device copy "
                              "before every step" % (8 * eng.nnz / 1e9)},
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "seconds_per_step": e2e_s,
