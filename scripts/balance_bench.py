@@ -7,10 +7,10 @@ Per (matrix, plan) row: p, blocks, tasks, levels, the reference's balance
 metrics (block_nnz_stats CV, level_work_stats last-level share, 4-worker
 makespan model, pkg/src/lublock/metrics.py:45-138), and the measured device
 numeric-factorization time (median), GFLOP/s, the summed per-level device
-time and the per-level imbalance of the DMMA SSSSM kernel (max/mean item
-time is not observable; we report the level-synchronous time share of the
-levels whose work is below 10% of the widest level).  Rows "pangulu_select"
-and "best_regular" repeat the matching regular rows like cmd_bench.
+time and its split over the kernel families (DMMA SSSSM, tile-DAG
+executor, CSC kernel).  Rows "pangulu_select" and "best_regular" repeat the
+matching regular rows like cmd_bench.  --taus adds irregular-plan rows for
+other density tags (sparse-kernel vs DMMA selection; "off" = CSC only).
 """
 
 from __future__ import annotations
@@ -81,6 +81,8 @@ def main():
     ap.add_argument("--tau", type=float, default=0.1)
     ap.add_argument("--check", action="store_true", help="also solve and report ||Ax-b||/||b||")
     ap.add_argument("--out", default=None, help="JSON lines output")
+    ap.add_argument("--taus", default=None,
+                    help="also sweep the density tag on the irregular plan, e.g. 0.05,0.1,0.25,0.5,off")
     args = ap.parse_args()
     out = open(args.out, "w") if args.out else None
     for name in args.matrices:
@@ -109,6 +111,20 @@ def main():
             print(line, flush=True)
             if out:
                 out.write(line + "\n")
+        if args.taus:
+            irr = M.irregular_plan(curve, a.n)
+            for tv in args.taus.split(","):
+                tau = None if tv == "off" else float(tv)
+                try:
+                    r = run_plan(a, f, irr, args.repeats, tau, False)
+                    r["status"] = "ok"
+                except Exception as exc:
+                    r = {"status": f"error:{type(exc).__name__}: {exc}"[:200]}
+                r.update({"matrix": name, "plan": f"irregular_tau_{tv}"})
+                line = json.dumps(r)
+                print(line, flush=True)
+                if out:
+                    out.write(line + "\n")
         regs = {k: v for k, v in rows.items() if k.startswith("regular_") and v["status"] == "ok"}
         extra = []
         if f"regular_{sel}" in regs:
