@@ -170,7 +170,8 @@ struct lbk_ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t aux[NBRANCH] = {nullptr, nullptr, nullptr};
   cudaEvent_t fork = nullptr, join[NBRANCH] = {nullptr, nullptr, nullptr};
-  cudaStream_t dstream = nullptr;     // deferred SSSSM branch
+  cudaStream_t dstream = nullptr;     // deferred SSSSM branch (lowest priority)
+  cudaEvent_t dfork = nullptr;
   std::vector<cudaEvent_t> dev;       // per launch level: deferred work done
   std::vector<int8_t> defer;          // per task: may run concurrently with the next level
   int exec_per_sm = 2;
@@ -284,6 +285,8 @@ void drop_graphs(lbk_ctx* c) {
   c->graphs.clear();
 }
 
+constexpr double RECT_SMALL = 64.0 * 64.0;
+
 int choose_warps(int acc_len) { return std::max(1, std::min(4, MAX_SMEM / (acc_len * 8))); }
 
 // positions of `sub` inside sorted `sup` (-1 if absent); identity flag
@@ -309,7 +312,12 @@ int lbk_create(lbk_ctx** out, int device, lbk_status* st) {
   if (!c) return fail(st, LBK_ERR_OOM, "ctx alloc");
   c->device = device;
   cudaError_t e = cudaSetDevice(device);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+  int prio_lo = 0, prio_hi = 0;
+  if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  // critical-path streams at the highest priority: graph kernel nodes inherit
+  // it (instantiated with cudaGraphInstantiateFlagUseNodePriority), so the
+  // block scheduler serves them before the deferred SSSSM branch
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, prio_hi);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
   if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_SMEM);
@@ -327,11 +335,12 @@ int lbk_create(lbk_ctx** out, int device, lbk_status* st) {
     e = cudaFuncSetAttribute(solve_upd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_SMEM);
   c->use_exec = std::getenv("LBK_NO_EXEC") == nullptr;
   for (int k = 0; k < NBRANCH && e == cudaSuccess; ++k) {
-    e = cudaStreamCreateWithFlags(&c->aux[k], cudaStreamNonBlocking);
+    e = cudaStreamCreateWithPriority(&c->aux[k], cudaStreamNonBlocking, prio_hi);
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->join[k], cudaEventDisableTiming);
   }
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->dstream, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->dstream, cudaStreamNonBlocking, prio_lo);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->dfork, cudaEventDisableTiming);
   if (const char* x = std::getenv("LBK_EXEC_PER_SM")) c->exec_per_sm = std::max(1, std::atoi(x));
   if (e != cudaSuccess) {
     delete c;
@@ -356,6 +365,7 @@ void lbk_destroy(lbk_ctx* c) {
   if (c->fork) cudaEventDestroy(c->fork);
   for (auto ev : c->dev) cudaEventDestroy(ev);
   if (c->dstream) cudaStreamDestroy(c->dstream);
+  if (c->dfork) cudaEventDestroy(c->dfork);
   if (c->solve_graph) cudaGraphExecDestroy(c->solve_graph);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -426,7 +436,10 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         for (int col = 0; col < d.ncols; ++col)
           if (scp[col + 1] > scp[col]) Cc.push_back(col);
         const double rect = static_cast<double>(R.size()) * Cc.size();
-        if (static_cast<double>(nzb) >= tau * rect) {
+        // small rectangles go dense regardless of their fill: a <= 64 x 64 tile
+        // costs at most 32 KB and turns scattered few-entry updates (BBD ports
+        // into a dense border) into one DMMA tile instead of CSC column sweeps
+        if (static_cast<double>(nzb) >= tau * rect || rect <= RECT_SMALL) {
           if (static_cast<int>(R.size()) == d.nrows && static_cast<int>(Cc.size()) == d.ncols) {
             store = STORE_FULL;
           } else {
@@ -1166,15 +1179,7 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
     auto rec = [&](int k, cudaStream_t s) {
       if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 11 + k], s, cudaEventRecordExternal);
     };
-    if (br[0] || br[1] || br[2] || L.ngemmD) cudaEventRecord(c->fork, s0);
-    if (L.ngemmD) {
-      cudaStreamWaitEvent(c->dstream, c->fork, 0);
-      if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 11 + 9], c->dstream, cudaEventRecordExternal);
-      gemm_map_kernel<<<L.ngemmD, 256, GEMM_SMEM, c->dstream>>>(c->gitems.p + L.gemmD_off, c->gtasks.p, P);
-      if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 11 + 10], c->dstream, cudaEventRecordExternal);
-      cudaEventRecord(c->dev[l], c->dstream);
-      pending.push_back(l);
-    }
+    if (br[0] || br[1] || br[2]) cudaEventRecord(c->fork, s0);
     if (br[0]) {
       cudaStreamWaitEvent(c->aux[0], c->fork, 0);
       rec(1, c->aux[0]);
@@ -1231,6 +1236,17 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
     }
     for (int k = 0; k < NBRANCH; ++k)
       if (br[k]) cudaStreamWaitEvent(s0, c->join[k], 0);
+    if (L.ngemmD) {
+      // deferred SSSSM updates start once this level's critical work is done
+      // and run (low stream priority) beside the next level
+      cudaEventRecord(c->dfork, s0);
+      cudaStreamWaitEvent(c->dstream, c->dfork, 0);
+      if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 11 + 9], c->dstream, cudaEventRecordExternal);
+      gemm_map_kernel<<<L.ngemmD, 256, GEMM_SMEM, c->dstream>>>(c->gitems.p + L.gemmD_off, c->gtasks.p, P);
+      if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 11 + 10], c->dstream, cudaEventRecordExternal);
+      cudaEventRecord(c->dev[l], c->dstream);
+      pending.push_back(l);
+    }
     rec(0, s0);
   }
   for (size_t q : pending) cudaStreamWaitEvent(s0, c->dev[q], 0);
@@ -1261,7 +1277,7 @@ int build_graph(lbk_ctx* c, double pivot_tol, double static_eps, lbk_status* st)
     size_t nodes = 0;
     cudaGraphGetNodes(g, nullptr, &nodes);
     cudaGraphExec_t ge = nullptr;
-    if (nodes) e = cudaGraphInstantiate(&ge, g, 0);
+    if (nodes) e = cudaGraphInstantiate(&ge, g, cudaGraphInstantiateFlagUseNodePriority);
     cudaGraphDestroy(g);
     if (e != cudaSuccess) return cuda_fail(st, e, "graph instantiate");
     c->graphs.push_back(ge);  // nullptr: nothing for this rank in the segment
@@ -1583,7 +1599,7 @@ int lbk_level_times(lbk_ctx* c, double pivot_tol, double static_eps, float* out_
   LBK_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), st);
   capture_factorization(c, pivot_tol, static_eps, &ev, 0, nl, true, true);
   LBK_CUDA(cudaStreamEndCapture(c->stream, &g), st);
-  cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+  cudaError_t e = cudaGraphInstantiate(&ge, g, cudaGraphInstantiateFlagUseNodePriority);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return cuda_fail(st, e, "instrumented graph");
   e = cudaGraphLaunch(ge, c->stream);
