@@ -89,10 +89,8 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // ------------------------------------------------------------- SSSSM ----
-__global__ void __launch_bounds__(256) gemm_map_kernel(const GemmItem* __restrict__ items,
-                                                       const GemmTask* __restrict__ tasks, DevPools P) {
-  extern __shared__ double sm[];
-  const GemmItem it = items[blockIdx.x];
+__device__ __forceinline__ void gemm_map_item(const GemmItem it, const GemmTask* __restrict__ tasks, const DevPools& P,
+                                              double* sm) {
   const GemmTask tk = tasks[it.task];
   const BlockDev Lb = P.blk[tk.a], Ub = P.blk[tk.b], Cb = P.blk[tk.c];
   const double* __restrict__ A = P.vals + Lb.ent;
@@ -183,6 +181,24 @@ __global__ void __launch_bounds__(256) gemm_map_kernel(const GemmItem* __restric
         Cv[static_cast<size_t>(cc) * ldc + rr] -= acc[i][j][h];
       }
     }
+  }
+}
+
+__global__ void __launch_bounds__(256) gemm_map_kernel(const GemmItem* __restrict__ items,
+                                                       const GemmTask* __restrict__ tasks, DevPools P) {
+  extern __shared__ double sm[];
+  gemm_map_item(items[blockIdx.x], tasks, P, sm);
+}
+
+// Throttled variant for the deferred (off-critical-path) SSSSM updates: a
+// fixed number of CTAs loop over the items, so the deferred work never holds
+// more than gridDim.x CTA slots while the next level's critical work runs.
+__global__ void __launch_bounds__(256) gemm_map_loop_kernel(const GemmItem* __restrict__ items, int n,
+                                                            const GemmTask* __restrict__ tasks, DevPools P) {
+  extern __shared__ double sm[];
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    gemm_map_item(items[i], tasks, P, sm);
+    __syncthreads();  // the next item's prologue overwrites the pipeline stages
   }
 }
 

@@ -175,6 +175,7 @@ struct lbk_ctx {
   std::vector<cudaEvent_t> dev;       // per launch level: deferred work done
   std::vector<int8_t> defer;          // per task: may run concurrently with the next level
   int exec_per_sm = 2;
+  int defer_ctas = 0;  // > 0: deferred SSSSM work on this many looping CTAs (LBK_DEFER_CTAS)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<cudaGraphExec_t> graphs;  // one per segment (see lbk_set_cuts)
   double g_tol = NAN, g_eps = NAN;
@@ -323,6 +324,8 @@ int lbk_create(lbk_ctx** out, int device, lbk_status* st) {
   if (e == cudaSuccess) e = cudaFuncSetAttribute(level_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_SMEM);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(gemm_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(gemm_map_loop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, GEMM_SMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_SMEM);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(tile_trsm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TRSM_SMEM);
@@ -342,6 +345,7 @@ int lbk_create(lbk_ctx** out, int device, lbk_status* st) {
   if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->dstream, cudaStreamNonBlocking, prio_lo);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->dfork, cudaEventDisableTiming);
   if (const char* x = std::getenv("LBK_EXEC_PER_SM")) c->exec_per_sm = std::max(1, std::atoi(x));
+  if (const char* x = std::getenv("LBK_DEFER_CTAS")) c->defer_ctas = std::max(0, std::atoi(x));
   if (e != cudaSuccess) {
     delete c;
     return cuda_fail(st, e, "lbk_create");
@@ -1242,7 +1246,11 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
       cudaEventRecord(c->dfork, s0);
       cudaStreamWaitEvent(c->dstream, c->dfork, 0);
       if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 11 + 9], c->dstream, cudaEventRecordExternal);
-      gemm_map_kernel<<<L.ngemmD, 256, GEMM_SMEM, c->dstream>>>(c->gitems.p + L.gemmD_off, c->gtasks.p, P);
+      if (c->defer_ctas > 0)
+        gemm_map_loop_kernel<<<std::min(L.ngemmD, c->defer_ctas), 256, GEMM_SMEM, c->dstream>>>(
+            c->gitems.p + L.gemmD_off, L.ngemmD, c->gtasks.p, P);
+      else
+        gemm_map_kernel<<<L.ngemmD, 256, GEMM_SMEM, c->dstream>>>(c->gitems.p + L.gemmD_off, c->gtasks.p, P);
       if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 11 + 10], c->dstream, cudaEventRecordExternal);
       cudaEventRecord(c->dev[l], c->dstream);
       pending.push_back(l);

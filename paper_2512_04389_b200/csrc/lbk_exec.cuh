@@ -343,6 +343,19 @@ __device__ __forceinline__ double rcp_nr(double x) {
   return fma(r, e, r);
 }
 
+// Branch-free 1/x: MUFU + two Newton steps; 0 -> +-inf, inf -> 0 like the
+// IEEE division (a zero pivot is then caught by the pivot verdict as usual).
+__device__ __forceinline__ double rcp_fast(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-x, r, 1.0);
+  r = fma(r, e, r);
+  r = fabs(x) < 1e-300 ? copysign(__longlong_as_double(0x7ff0000000000000LL), x) : r;
+  return isinf(x) ? copysign(0.0, x) : r;
+}
+
 // acc_c -= sum_k l[k] * B(k, c) for the columns c = c0, c0 + 4, ... < ce, three
 // independent accumulation chains at a time.  Col(c) = address of column c of
 // the target (row offset applied), Bk(c) = address of B(0, c) (k contiguous).
@@ -812,6 +825,32 @@ __device__ void band_getrf(const BlockDev& A, const DevPools& P, double* sm, int
     }
     __syncthreads();
 #pragma unroll 1
+    if (bl * (bu + 1) <= 32) {
+      // narrow band: the bl x (bu + 1) update pairs fit one warp (fixed lane ->
+      // (i, j) map); steps only need a __syncwarp, the other warps wait
+      if (tid < 32) {
+        const int q = tid, ii = 1 + q / (bu + 1), jj = q % (bu + 1);
+        const bool own = q < bl * (bu + 1);
+#pragma unroll 1
+        for (int k = c0; k < kend; ++k) {
+          const double* colk = Bs + (k - c0) * W + bu;
+          const double rinv = rcp_fast(colk[0]);
+          if (own && k + ii < m) {
+            const double d = colk[ii];
+            const double l = d * rinv;
+            if (jj == 0) {
+              S[(k - c0) * 16 + ii] = fabs(d);
+              Lc[(k - c0) * 16 + ii] = l;
+            } else if (k + jj < m) {
+              double* e = Bs + (k + jj - c0) * W + (ii - jj + bu);
+              *e = fma(-l, Bs[(k + jj - c0) * W + (bu - jj)], *e);
+            }
+          }
+          __syncwarp();
+        }
+      }
+      __syncthreads();
+    } else
     for (int k = c0; k < kend; ++k) {
       const double* colk = Bs + (k - c0) * W + bu;  // (k + i, k) = colk[i]
       const double u = colk[0];
