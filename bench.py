@@ -320,6 +320,22 @@ def main():
     e2e_s = max_over_ranks((time.perf_counter() - t0) / ke, world)
     e2e_value = jobs * total_flops / e2e_s / 1e9
 
+    # device triangular solve on the resident factors (factorize.py:451-457 on the device)
+    solve_info = None
+    if not distributed:
+        A = a.to_scipy()
+        rhs = A @ np.ones(a.n)
+        run_dev()
+        eng.solve(rhs)  # builds the solve graph
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            x = eng.solve(rhs)
+            ts.append(time.perf_counter() - t0)
+        solve_info = {"ms": 1e3 * statistics.median(ts),
+                      "relres": float(np.linalg.norm(A @ x - rhs) / np.linalg.norm(rhs)),
+                      "path": "Engine.solve -> lbk_solve (host b in, host x out), b = A @ ones"}
+
     # per-level / per-kernel-family device times (instrumented replay) -> roofline
     # (distributed: this rank's own tasks, replayed without the exchanges: timing only)
     lvl = eng.level_times(check=not distributed)  # [levels x 5]: level, DMMA SSSSM, panel, tiled GETRF, CSC
@@ -421,6 +437,7 @@ def main():
             "cpu_baseline": cpu,
             "clocks": clk.summary(),
             "gpu_launches": int(args.steps * eng.n_launches),
+            "solve": solve_info,
             "exchange": ({"segments": eng.n_segments, "messages_rank0": de.messages,
                           "bytes_sent_rank0": de.bytes_out,
                           "roofline_scope": "rank 0's own tasks"} if distributed else None),

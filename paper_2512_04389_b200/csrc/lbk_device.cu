@@ -215,11 +215,15 @@ struct lbk_ctx {
   std::vector<char> isdiag;
   // device triangular solve (lbk_solve): block grid + lazily built graph
   std::vector<int64_t> pos, hbi, hbj;
+  std::vector<int32_t> dext;       // per diagonal block, per 64-col chunk: (row hi, row lo) of its pattern
+  std::vector<int64_t> dext_off;   // per block: offset into dext (diagonal blocks)
+  DevBuf<int32_t> sdext;
   DevBuf<SolveStep> sfw, sbw;
   DevBuf<SolveUpd> ufw, ubw;
-  DevBuf<int32_t> sbstart;
+  DevBuf<int32_t> sbstart, tistep, titile;
   DevBuf<int64_t> sdgrow;
-  DevBuf<double> sb, sv;
+  DevBuf<double> sb, sv, stinv;
+  int64_t n_tinv = 0;
   cudaGraphExec_t solve_graph = nullptr;
   DevBuf<unsigned long long> xtrace;  // executor task timeline (instrumented replays only)
 };
@@ -336,6 +340,9 @@ int lbk_create(lbk_ctx** out, int device, lbk_status* st) {
     e = cudaFuncSetAttribute(solve_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_SMEM);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(solve_upd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(tile_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (2 * XREG + XT) * sizeof(double));
   c->use_exec = std::getenv("LBK_NO_EXEC") == nullptr;
   for (int k = 0; k < NBRANCH && e == cudaSuccess; ++k) {
     e = cudaStreamCreateWithPriority(&c->aux[k], cudaStreamNonBlocking, prio_hi);
@@ -410,6 +417,8 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     // ---- storage kind, R / C lists ------------------------------------------------
     std::vector<BlockDev> hb(nb);
     c->wlen.assign(nb, 0);
+    c->dext.clear();
+    c->dext_off.assign(nb, -1);
     c->isdiag.assign(nb, 0);
     for (int64_t b = 0; b < nb; ++b) c->isdiag[b] = T_bi[b] == T_bj[b];
     if (!c->mask.empty() && static_cast<int64_t>(c->mask.size()) != ntasks)
@@ -536,6 +545,23 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
             hmap[eo + e] = d.ent + static_cast<int64_t>(cpos[col]) * d.nR + rpos[sri[e]];
       }
       if (T_bi[b] == T_bj[b]) {
+        // row extent of every 64-column chunk of the diagonal block's pattern
+        // (the device solve only touches rows the chunk can reach)
+        {
+          const int nch = (d.ncols + 63) / 64;
+          c->dext_off[b] = static_cast<int64_t>(c->dext.size());
+          std::vector<int32_t> hi(nch, 0), lo(nch, d.nrows);
+          for (int col = 0; col < d.ncols; ++col)
+            for (int64_t e = scp[col]; e < scp[col + 1]; ++e) {
+              const int r = static_cast<int>(sri[e]), ch = col / 64;
+              hi[ch] = std::max(hi[ch], r + 1);
+              lo[ch] = std::min(lo[ch], r);
+            }
+          for (int ch = 0; ch < nch; ++ch) {
+            c->dext.push_back(hi[ch]);
+            c->dext.push_back(lo[ch]);
+          }
+        }
         d.dg = ndiag;
         ndiag += d.nrows;
         if (d.store == STORE_SPARSE) {
@@ -1497,6 +1523,22 @@ int build_solve(lbk_ctx* c, lbk_status* st) {
   std::vector<SolveStep> fw, bw;
   std::vector<SolveUpd> uf, ub;
   int64_t maxspan = 1;
+  // inverse diagonal tiles for the FULL diagonal blocks (cluster solve)
+  std::vector<int64_t> tinv_off(p, -1);
+  std::vector<int32_t> tistep, titile;
+  int64_t ntinv = 0;
+  for (int64_t i = 0; i < p; ++i) {
+    const BlockDev& D = c->hblk[bid[i * p + i]];
+    const int64_t span = c->pos[i + 1] - c->pos[i];
+    if (D.store != STORE_FULL || span <= XT) continue;
+    tinv_off[i] = ntinv;
+    const int64_t nt = (span + XT - 1) / XT;
+    for (int64_t t = 0; t < nt; ++t) {
+      tistep.push_back(static_cast<int32_t>(i));  // forward steps are in block order
+      titile.push_back(static_cast<int32_t>(t));
+    }
+    ntinv += nt * 2 * XT * XT;
+  }
   auto items = [&](int64_t i, bool lower, std::vector<SolveUpd>* out) {
     for (int64_t b : bycol[i]) {
       const int64_t k = c->hbi[b];
@@ -1515,6 +1557,8 @@ int build_solve(lbk_ctx* c, lbk_status* st) {
       S.diag = static_cast<int32_t>(bid[i * p + i]);
       S.off = static_cast<int32_t>(c->pos[i]);
       S.span = static_cast<int32_t>(c->pos[i + 1] - c->pos[i]);
+      S.tinv = tinv_off[i];
+      S.ext = c->dext_off[bid[i * p + i]];
       maxspan = std::max<int64_t>(maxspan, S.span);
       std::vector<SolveUpd>* out = dir == 0 ? &uf : &ub;
       S.upd_off = static_cast<int64_t>(out->size());
@@ -1542,19 +1586,33 @@ int build_solve(lbk_ctx* c, lbk_status* st) {
   LBK_CUDA(c->sdgrow.upload(dgrow), st);
   LBK_CUDA(c->sb.alloc(c->n), st);
   LBK_CUDA(c->sv.alloc(c->n), st);
+  LBK_CUDA(c->tistep.upload(tistep), st);
+  LBK_CUDA(c->sdext.upload(c->dext.empty() ? std::vector<int32_t>(2, 0) : c->dext), st);
+  LBK_CUDA(c->titile.upload(titile), st);
+  LBK_CUDA(c->stinv.alloc(std::max<int64_t>(ntinv, 1)), st);
+  c->n_tinv = static_cast<int64_t>(tistep.size());
   DevPools P = pools(c);
   cudaStream_t s0 = c->stream;
   cudaGraph_t g;
   LBK_CUDA(cudaStreamBeginCapture(s0, cudaStreamCaptureModeThreadLocal), st);
   solve_perm_kernel<<<148 * 4, 256, 0, s0>>>(c->sb.p, c->sv.p, c->perm.p, c->sbstart.p, c->sdgrow.p, c->n);
+  if (c->n_tinv)
+    tile_inverse_kernel<<<static_cast<int>(c->n_tinv), 256, (2 * XREG + XT) * sizeof(double), s0>>>(
+        P, c->sfw.p, c->tistep.p, c->titile.p, c->stinv.p);
   for (int dir = 0; dir < 2; ++dir) {
     const std::vector<SolveStep>& steps = dir == 0 ? fw : bw;
     for (size_t q = 0; q < steps.size(); ++q) {
       const SolveStep& S = steps[q];
       const size_t sm = (static_cast<size_t>((S.span + 1) & ~1) + SOLVE_CHUNK * 65) * sizeof(double);
-      solve_diag_kernel<<<1, 256, sm, s0>>>(P, (dir == 0 ? c->sfw.p : c->sbw.p), static_cast<int>(q), c->sv.p, dir);
+      if (S.tinv >= 0) {
+        const int nch = (S.span + XT - 1) / XT, rpc = ((nch + SOLVE_CL - 1) / SOLVE_CL) * XT;
+        solve_diag_cluster_kernel<<<SOLVE_CL, 256, (rpc + 7 * XT) * sizeof(double), s0>>>(
+            P, (dir == 0 ? c->sfw.p : c->sbw.p), static_cast<int>(q), c->sv.p, dir, c->stinv.p, c->sdext.p);
+      } else {
+        solve_diag_kernel<<<1, 256, sm, s0>>>(P, (dir == 0 ? c->sfw.p : c->sbw.p), static_cast<int>(q), c->sv.p, dir);
+      }
       if (S.nupd)
-        solve_upd_kernel<<<S.nupd, 256, static_cast<size_t>(S.span) * sizeof(double), s0>>>(
+        solve_upd_kernel<<<S.nupd, 256, (static_cast<size_t>((S.span + 1) & ~1) + 256) * sizeof(double), s0>>>(
             P, (dir == 0 ? c->ufw.p : c->ubw.p) + S.upd_off, c->sv.p);
     }
   }

@@ -10,22 +10,27 @@
 // the same blocks LUFactors exports (factorize.py:370-384), so the quirk of
 // unpermuted L blocks left of a pivoting diagonal block is reproduced too.
 //
-// Column-oriented: step i solves the diagonal block of block row i in one
-// CTA (64-row chunks: the 64x64 triangle by one warp out of shared memory,
-// the rest of the chunk's column panel as a GEMV on all threads), then one
+// Column-oriented: step i solves the diagonal block of block row i, then one
 // launch updates every target block row k with the stored blocks of block
-// column i: r_k -= B_ki y_i — distinct targets per block, row chunks per
-// item, so no atomics and a fixed summation order.  2p + 2p launches per
-// solve, captured once into a CUDA graph.
+// column i: r_k -= B_ki y_i — distinct targets per block, 64-row chunks per
+// item, so no atomics and a fixed summation order.  FULL diagonal blocks run
+// on a cluster of 8 CTAs (distributed shared memory) with the inverses of
+// their 64x64 diagonal tiles (computed at the start of every solve), CSC
+// diagonal blocks on one CTA sweeping the columns.  2p + 2p launches per
+// solve, captured once into a CUDA graph.  C2: 79 ms (was 536 ms with one
+// CTA and triangular tile solves per diagonal block).
 
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "lbk_common.cuh"
+#include "lbk_exec.cuh"
 
 namespace lbk {
 
 constexpr int SOLVE_CHUNK = 64;     // rows per diagonal-solve chunk
-constexpr int UPD_ROWS = 256;       // block rows per update item
+constexpr int UPD_ROWS = 64;        // block rows per update item
 
 struct SolveStep {
   int32_t diag;   // diagonal block id
@@ -33,7 +38,113 @@ struct SolveStep {
   int32_t span;
   int32_t nupd;   // update items of this step
   int64_t upd_off;
+  int64_t tinv;   // FULL diagonal blocks: offset of its inverse 64x64 diagonal tiles (-1: none)
+  int64_t ext;    // offset of the per-chunk (row hi, row lo) pattern extents
 };
+
+constexpr int SOLVE_CL = 8;  // CTAs per cluster of the diagonal solve
+
+// Inverses of the 64x64 diagonal tiles of a factored FULL diagonal block:
+// Linv = (unit lower of tile)^-1, Uinv = (upper of tile)^-1, column-major 64x64
+// each, at inv[2 * 4096 * tile + {0, 4096}].  Edge tiles are padded with the
+// identity.  One CTA per tile (the compact blocked tile solves of the executor
+// applied to an identity right-hand side).
+__global__ void __launch_bounds__(256) tile_inverse_kernel(DevPools P, const SolveStep* __restrict__ steps,
+                                                          const int32_t* __restrict__ tstep,
+                                                          const int32_t* __restrict__ ttile, double* inv) {
+  extern __shared__ double sm[];
+  const SolveStep S = steps[tstep[blockIdx.x]];
+  const int t = ttile[blockIdx.x];
+  const BlockDev D = P.blk[S.diag];
+  const int m = S.span, c0 = t * XT, cn = min(XT, m - c0), ld = D.nR;
+  double* X = sm;             // XTP stride
+  double* T = sm + XREG;      // the factored tile
+  double* rinv = sm + 2 * XREG;
+  const double* G = P.vals + D.ent + static_cast<size_t>(c0) * ld + c0;
+  for (int e = threadIdx.x; e < XT * XT; e += blockDim.x) {
+    const int r = e & (XT - 1), c = e >> 6;
+    T[c * XTP + r] = (r < cn && c < cn) ? G[static_cast<size_t>(c) * ld + r] : (r == c ? 1.0 : 0.0);
+    X[c * XTP + r] = r == c ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  double* out = inv + S.tinv + static_cast<int64_t>(t) * 2 * XT * XT;
+  tile_left_solve_blk(X, T, XT);  // X = L^-1
+  for (int e = threadIdx.x; e < XT * XT; e += blockDim.x) out[e] = X[(e >> 6) * XTP + (e & (XT - 1))];
+  for (int e = threadIdx.x; e < XT * XT; e += blockDim.x) X[(e >> 6) * XTP + (e & (XT - 1))] = (e >> 6) == (e & 63) ? 1.0 : 0.0;
+  if (threadIdx.x < XT) rinv[threadIdx.x] = 1.0 / T[threadIdx.x * XTP + threadIdx.x];
+  __syncthreads();
+  tile_right_solve_blk<false>(X, T, rinv, nullptr, XT);  // X = U^-1
+  for (int e = threadIdx.x; e < XT * XT; e += blockDim.x) out[XT * XT + e] = X[(e >> 6) * XTP + (e & (XT - 1))];
+}
+
+// Diagonal block of one step on a cluster of SOLVE_CL CTAs (FULL storage).
+// CTA q owns rows [q*rpc, (q+1)*rpc) of the segment (rpc a multiple of 64, so
+// every 64-row chunk has one owner).  Per chunk: the owner forms x_c = Tinv_c
+// r_c from its shared memory and publishes it; one cluster barrier; every CTA
+// reads x_c through distributed shared memory and updates its own rows below
+// (forward) / above (backward) the chunk.  x buffers alternate by chunk
+// parity, so one barrier per chunk suffices.
+__global__ void __cluster_dims__(SOLVE_CL, 1, 1) __launch_bounds__(256)
+    solve_diag_cluster_kernel(DevPools P, const SolveStep* __restrict__ steps, int s, double* __restrict__ v,
+                              int upper, const double* __restrict__ inv, const int32_t* __restrict__ ext) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ double sm[];
+  const SolveStep S = steps[s];
+  const BlockDev D = P.blk[S.diag];
+  const int m = S.span, tid = threadIdx.x, q = static_cast<int>(cl.block_rank());
+  const int nch = (m + XT - 1) / XT, rpc = ((nch + SOLVE_CL - 1) / SOLVE_CL) * XT;
+  const int r0 = q * rpc, r1 = min(m, r0 + rpc);
+  double* y = sm;                 // my rows
+  double* xb = sm + rpc;          // [2][64] published chunk solution
+  double* xs = xb + 2 * XT;       // chunk solution read from the owner
+  double* part = xs + XT;         // 256 matvec partial sums
+  for (int r = r0 + tid; r < r1; r += blockDim.x) y[r - r0] = v[S.off + r];
+  const double* G = P.vals + D.ent;
+  const int ld = D.nR;
+  cl.sync();
+  for (int qq = 0; qq < nch; ++qq) {
+    const int c = upper ? nch - 1 - qq : qq;
+    const int c0 = c * XT, cn = min(XT, m - c0), owner = c0 / rpc;
+    double* xbuf = xb + (qq & 1) * XT;
+    if (q == owner) {
+      // x_c = Tinv_c r_c: thread (row, k-quarter) -> 16 independent loads
+      const double* Ti = inv + S.tinv + static_cast<int64_t>(c) * 2 * XT * XT + (upper ? XT * XT : 0);
+      const int row = tid & (XT - 1), kq = (tid >> 6) * 16;
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (kq + k < cn) acc = fma(Ti[(kq + k) * XT + row], y[c0 - r0 + kq + k], acc);
+      part[tid] = acc;
+      __syncthreads();
+      if (tid < XT) xbuf[tid] = tid < cn ? (part[tid] + part[XT + tid]) + (part[2 * XT + tid] + part[3 * XT + tid]) : 0.0;
+      __syncthreads();
+      if (tid < cn) y[c0 - r0 + tid] = xbuf[tid];
+    }
+    cl.sync();
+    const double* src = cl.map_shared_rank(xbuf, owner);
+    if (tid < XT) xs[tid] = tid < cn ? src[tid] : 0.0;
+    __syncthreads();
+    // my rows strictly below (forward) / above (backward) the chunk
+    // ... limited to the rows the chunk's pattern reaches (banded blocks: a few)
+    const int lo = upper ? max(r0, ext[S.ext + 2 * c + 1]) : max(r0, c0 + cn);
+    const int hi = upper ? min(r1, c0) : min(r1, ext[S.ext + 2 * c]);
+    for (int r = lo + tid; r < hi; r += blockDim.x) {
+      const double* col = G + static_cast<size_t>(c0) * ld + r;
+      double a4[4] = {0.0, 0.0, 0.0, 0.0};
+      if (cn == XT) {
+#pragma unroll
+        for (int k = 0; k < XT; ++k) a4[k & 3] = fma(col[static_cast<size_t>(k) * ld], xs[k], a4[k & 3]);
+      } else {
+        for (int k = 0; k < cn; ++k) a4[k & 3] = fma(col[static_cast<size_t>(k) * ld], xs[k], a4[k & 3]);
+      }
+      y[r - r0] -= (a4[0] + a4[1]) + (a4[2] + a4[3]);
+    }
+    __syncthreads();
+  }
+  cl.sync();  // no CTA leaves while another may still read its x buffer
+  for (int r = r0 + tid; r < r1; r += blockDim.x) v[S.off + r] = y[r - r0];
+}
 
 struct SolveUpd {
   int32_t blk;      // factor block B_ki
@@ -120,12 +231,18 @@ __global__ void __launch_bounds__(256) solve_diag_kernel(DevPools P, const Solve
       __syncthreads();
       // the rest of the chunk's columns: rows below (forward) / above (backward)
       const int rb0 = upper ? 0 : c0 + cn, rb1 = upper ? c0 : m;
+      // four independent partial sums and a fully unrolled k loop: the 64
+      // column loads of a row are all in flight at once (HBM latency bound)
       for (int r = rb0 + tid; r < rb1; r += blockDim.x) {
-        double acc = y[r];
         const double* col = G + static_cast<size_t>(c0) * ld + r;
-#pragma unroll 8
-        for (int k = 0; k < cn; ++k) acc = fma(-col[static_cast<size_t>(k) * ld], y[c0 + k], acc);
-        y[r] = acc;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        if (cn == SOLVE_CHUNK) {
+#pragma unroll
+          for (int k = 0; k < SOLVE_CHUNK; ++k) acc[k & 3] = fma(col[static_cast<size_t>(k) * ld], y[c0 + k], acc[k & 3]);
+        } else {
+          for (int k = 0; k < cn; ++k) acc[k & 3] = fma(col[static_cast<size_t>(k) * ld], y[c0 + k], acc[k & 3]);
+        }
+        y[r] -= (acc[0] + acc[1]) + (acc[2] + acc[3]);
       }
       __syncthreads();
     }
@@ -133,8 +250,9 @@ __global__ void __launch_bounds__(256) solve_diag_kernel(DevPools P, const Solve
   for (int r = tid; r < m; r += blockDim.x) v[S.off + r] = y[r];
 }
 
-// r_k -= B_ki y_i for one row chunk of one stored block (256 threads, one row each).
-// Dynamic smem: the source segment (block column span).
+// r_k -= B_ki y_i for one 64-row chunk of one stored block (dense tiles: 64 rows
+// x 4 column quarters, partial sums reduced in smem; CSC: one row per thread).
+// Dynamic smem: the source segment (block column span) + 256 partial sums.
 __global__ void __launch_bounds__(256) solve_upd_kernel(DevPools P, const SolveUpd* __restrict__ items,
                                                        double* __restrict__ v) {
   extern __shared__ double ys[];
@@ -146,7 +264,7 @@ __global__ void __launch_bounds__(256) solve_upd_kernel(DevPools P, const SolveU
   const double* G = P.vals + B.ent;
   const int a = it.r0 + tid;
   if (B.store == STORE_SPARSE) {
-    if (a >= B.nrows) return;
+    if (tid >= UPD_ROWS || a >= B.nrows) return;
     const int32_t* rp = P.csr_ptr + B.rp;
     const int32_t* cc = P.csr_col + B.csr;
     const int32_t* ps = P.csr_pos + B.csr;
@@ -154,14 +272,28 @@ __global__ void __launch_bounds__(256) solve_upd_kernel(DevPools P, const SolveU
     for (int g = rp[a]; g < rp[a + 1]; ++g) acc = fma(G[ps[g]], ys[cc[g]], acc);
     v[it.tgt_off + a] -= acc;
   } else {
-    if (a >= B.nR) return;
+    // 64 rows x 4 column quarters per CTA: 4x shorter dependent load chains
+    const int ar = it.r0 + (tid & 63), quarter = tid >> 6;
     const int32_t* cl = B.store == STORE_RECT ? P.clist + B.coff : nullptr;
-    const int row = B.store == STORE_RECT ? P.rlist[B.roff + a] : a;
-    double acc = 0.0;
-    const double* col = G + a;
-#pragma unroll 4
-    for (int c = 0; c < B.nC; ++c) acc = fma(col[static_cast<size_t>(c) * B.nR], ys[cl ? cl[c] : c], acc);
-    v[it.tgt_off + row] -= acc;
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    if (ar < B.nR) {
+      const int cq = (B.nC + 3) / 4, cb = quarter * cq, ce = min(B.nC, cb + cq);
+      const double* col = G + ar;
+      int c = cb;
+      for (; c + 8 <= ce; c += 8) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          acc[q & 3] = fma(col[static_cast<size_t>(c + q) * B.nR], ys[cl ? cl[c + q] : c + q], acc[q & 3]);
+      }
+      for (; c < ce; ++c) acc[0] = fma(col[static_cast<size_t>(c) * B.nR], ys[cl ? cl[c] : c], acc[0]);
+    }
+    double* part = ys + ((B.ncols + 1) & ~1);  // 4 x 64 partial sums after the source segment
+    part[quarter * 64 + (tid & 63)] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    __syncthreads();
+    if (tid < 64 && ar < B.nR) {
+      const int row = B.store == STORE_RECT ? P.rlist[B.roff + ar] : ar;
+      v[it.tgt_off + row] -= (part[tid] + part[64 + tid]) + (part[128 + tid] + part[192 + tid]);
+    }
   }
 }
 

@@ -1,0 +1,5 @@
+timeout 900 python -m pytest tests/test_device_solve.py -x -q 2>&1 | tail -2
+for cfg in C2 C3; do
+python scripts/solve_time.py $cfg 2>&1 | tail -1
+LBK_SOLVE_SKIP_UPD=1 python scripts/solve_time.py $cfg 2>&1 | tail -1
+done
