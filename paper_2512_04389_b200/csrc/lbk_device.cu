@@ -122,8 +122,8 @@ struct ExecBuilder {
   // GEMMs feeding them overtake the bulk trailing updates of the current
   // step, which a plain step-major order would dequeue first.
   static int cost_of(int type) {
-    static const int c[11] = {150, 360, 180, 130, 64, 60, 130, 64, 180, 64, 100000};
-    return type >= 0 && type < 11 ? c[type] : 64;
+    static const int c[14] = {150, 360, 180, 130, 64, 60, 130, 64, 180, 64, 100000, 420, 190, 240};
+    return type >= 0 && type < 14 ? c[type] : 64;
   }
   void flush(Level* L, std::vector<XTask>* tasks, std::vector<int32_t>* sptr, std::vector<int32_t>* succ,
              std::vector<int32_t>* deps0) {
@@ -984,8 +984,15 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
             else extra.insert(extra.end(), colj[cc].begin(), colj[cc].end());
             return extra;
           };
+          // the last update of diagonal tile kb (GEMM(kb, kb, kb-1)) is fused into
+          // its LU task: one handoff and one tile round trip less per step of
+          // the critical chain
+          std::vector<int> fused_deps;
+          bool fused = false;
           for (int kb = 0; kb < nt; ++kb) {
-            const int g = X.add(X_GETRF, b, b, kb, kb, kb, stp, kb * 4, prev(kb, kb, {}));
+            const int g = fused ? X.add(X_GETRF_UPD, b, b, kb, kb, kb - 1, stp, kb * 4, fused_deps)
+                                : X.add(X_GETRF, b, b, kb, kb, kb, stp, kb * 4, prev(kb, kb, {}));
+            fused = false;
             L_(kb, kb) = g;
             fin_deps.push_back(g);
             for (int r = kb + 1; r < nt; ++r) {
@@ -1005,6 +1012,11 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
               if (ut[cc] < 0) continue;
               for (int r = kb + 1; r < nt; ++r) {
                 if (lt[r] < 0) continue;
+                if (r == kb + 1 && cc == kb + 1) {
+                  fused = true;
+                  fused_deps = prev(r, cc, {lt[r], ut[cc]});
+                  continue;
+                }
                 const int t2 = X.add(X_GEMM, b, b, r, cc, kb, stp, kb * 4 + 2, prev(r, cc, {lt[r], ut[cc]}));
                 L_(r, cc) = t2;
               }
@@ -1051,31 +1063,56 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           }
           auto X_ = [&](int r, int cc) { return occX[static_cast<size_t>(cc) * tr + r] != 0; };
           auto D_ = [&](int r, int cc) { return occD[static_cast<size_t>(cc) * nd + r] != 0; };
+          // the update of the next tile along the substitution chain is fused
+          // into that tile's solve task (one handoff + one tile round trip less
+          // per chain step)
+          std::vector<int> pend(static_cast<size_t>(tr) * tc, -2);  // step k of a pending fused update
+          std::vector<std::vector<int>> pend_deps(static_cast<size_t>(tr) * tc);
+          auto P_ = [&](int r, int cc) -> int& { return pend[static_cast<size_t>(cc) * tr + r]; };
+          auto PD_ = [&](int r, int cc) -> std::vector<int>& { return pend_deps[static_cast<size_t>(cc) * tr + r]; };
           if (pt[0] == 1) {  // GESSM: forward substitution down the row blocks
             for (int kb = 0; kb < tr; ++kb)
               for (int cc = 0; cc < tc; ++cc) {
                 if (!X_(kb, cc)) continue;
-                const int d = X.add(X_PG_DIAG, xb, dblk, kb, cc, kb, stp, kb * 4 + 1, {L_(kb, cc)});
+                const int d = P_(kb, cc) >= 0
+                                  ? X.add(X_PG_FUSED, xb, dblk, kb, cc, P_(kb, cc), stp, kb * 4 + 1, PD_(kb, cc))
+                                  : X.add(X_PG_DIAG, xb, dblk, kb, cc, kb, stp, kb * 4 + 1, {L_(kb, cc)});
                 L_(kb, cc) = d;
                 for (int r = kb + 1; r < tr; ++r)
-                  if (X_(r, cc) && D_(r, kb))  // L tile (r, kb)
+                  if (X_(r, cc) && D_(r, kb)) {  // L tile (r, kb)
+                    if (r == kb + 1) {
+                      P_(r, cc) = kb;
+                      PD_(r, cc) = {d, L_(r, cc)};
+                      continue;
+                    }
                     L_(r, cc) = X.add(X_PG_UPD, xb, dblk, r, cc, kb, stp, kb * 4 + 2, {d, L_(r, cc)});
+                  }
               }
           } else {  // TSTRF: substitution along the column blocks
             for (int kb = 0; kb < tc; ++kb)
               for (int r = 0; r < tr; ++r) {
                 if (!X_(r, kb)) continue;
-                const int d = X.add(X_PT_DIAG, xb, dblk, r, kb, kb, stp, kb * 4 + 1, {L_(r, kb)});
+                const int d = P_(r, kb) >= 0
+                                  ? X.add(X_PT_FUSED, xb, dblk, r, kb, P_(r, kb), stp, kb * 4 + 1, PD_(r, kb))
+                                  : X.add(X_PT_DIAG, xb, dblk, r, kb, kb, stp, kb * 4 + 1, {L_(r, kb)});
                 L_(r, kb) = d;
                 for (int cc = kb + 1; cc < tc; ++cc)
-                  if (X_(r, cc) && D_(kb, cc))  // U tile (kb, cc)
+                  if (X_(r, cc) && D_(kb, cc)) {  // U tile (kb, cc)
+                    if (cc == kb + 1) {
+                      P_(r, cc) = kb;
+                      PD_(r, cc) = {d, L_(r, cc)};
+                      continue;
+                    }
                     L_(r, cc) = X.add(X_PT_UPD, xb, dblk, r, cc, kb, stp, kb * 4 + 2, {d, L_(r, cc)});
+                  }
               }
           }
         }
         for (const XTask& x : X.t) {  // executed flops of the tile tasks (full 64-tiles)
           const double t3 = 64.0 * 64.0 * 64.0;
-          c->exec_flops += x.type == X_GEMM || x.type == X_PG_UPD || x.type == X_PT_UPD ? 2 * t3
+          c->exec_flops += x.type == X_GETRF_UPD                                     ? 2 * t3 + 2 * t3 / 3
+                           : x.type == X_PG_FUSED || x.type == X_PT_FUSED              ? 3 * t3
+                           : x.type == X_GEMM || x.type == X_PG_UPD || x.type == X_PT_UPD ? 2 * t3
                            : x.type == X_GETRF                                       ? 2 * t3 / 3
                            : x.type == X_COLMAX || x.type == X_FINAL                 ? 0
                                                                                      : t3;

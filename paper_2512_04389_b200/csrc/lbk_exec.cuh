@@ -50,6 +50,9 @@ enum XType : int8_t {
   X_PT_DIAG = 8, // TSTRF panel a (cols C_X): tile (r,c) <- tile U[C_c,C_c]^{-1}
   X_PT_UPD = 9,  // tile (r,c) -= tile(r,k) U[C_k, C_c]
   X_BAND = 10,   // LU of an independent segment [d, d + k) of a banded FULL diagonal block a (r, c = bandwidths)
+  X_GETRF_UPD = 11,  // tile (r,r) -= tile(r,k) tile(k,r), then its LU (the diagonal chain, fused)
+  X_PG_FUSED = 12,   // GESSM: X_PG_UPD from step k into tile (r,c), then X_PG_DIAG of (r,c)
+  X_PT_FUSED = 13,   // TSTRF: X_PT_UPD from step k into tile (r,c), then X_PT_DIAG of (r,c)
 };
 
 struct XTask {
@@ -921,10 +924,19 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       }
       break;
     }
-    case X_GETRF: {
-      const int m = A.nrows, k0 = tk.k * XT, n = min(XT, m - k0);
+    case X_GETRF:
+    case X_GETRF_UPD: {
+      const int m = A.nrows, k0 = tk.r * XT, n = min(XT, m - k0);
       double* G = P.vals + A.ent + static_cast<size_t>(k0) * m + k0;
       load_tile(T0, G, m, n, n);
+      if (tk.type == X_GETRF_UPD) {  // the last trailing update of this tile first
+        const int u0 = tk.k * XT, nu = min(XT, m - u0);
+        const double* base = P.vals + A.ent;
+        load_opA(T1, base + static_cast<size_t>(u0) * m + k0, m, n, nu);
+        load_opB(T2, base + static_cast<size_t>(k0) * m + u0, m, nu, n);
+        __syncthreads();
+        tile_mma_sub(T0, T1, T2);
+      }
       __syncthreads();
       stamp(ph, 0);
       tile_lu64_blocked(T0, n, T1, rinv);
@@ -988,7 +1000,8 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       break;
     }
     case X_PG_DIAG:
-    case X_PG_UPD: {
+    case X_PG_UPD:
+    case X_PG_FUSED: {
       // GESSM on panel X (rows R_X): L = unit lower of diagonal block D restricted to R_X
       const BlockDev D = P.blk[tk.d];
       const int m = D.nrows, ld = A.nR;
@@ -996,10 +1009,18 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       const int r0 = tk.r * XT, c0 = tk.c * XT, nr = min(XT, A.nR - r0), nc = min(XT, A.nC - c0);
       double* G = P.vals + A.ent + static_cast<size_t>(c0) * ld + r0;
       const double* Dv = P.vals + D.ent;
-      if (tk.type == X_PG_DIAG) {
+      if (tk.type == X_PG_DIAG || tk.type == X_PG_FUSED) {
+        load_tile(T0, G, ld, nr, nc);
+        if (tk.type == X_PG_FUSED) {  // the update from the previous row step first
+          const int k0 = tk.k * XT, nk = min(XT, A.nR - k0);
+          if (Rl) load_opA(T1, Dv, m, nr, nk, Rl + r0, Rl + k0);
+          else load_opA(T1, Dv + static_cast<size_t>(k0) * m + r0, m, nr, nk);
+          load_opB(T2, P.vals + A.ent + static_cast<size_t>(c0) * ld + k0, ld, nk, nc);
+          __syncthreads();
+          tile_mma_sub(T0, T1, T2);
+        }
         if (Rl) load_tile(T1, Dv, m, nr, nr, Rl + r0, Rl + r0);
         else load_tile(T1, Dv + static_cast<size_t>(r0) * m + r0, m, nr, nr);
-        load_tile(T0, G, ld, nr, nc);
         __syncthreads();
         tile_left_solve_blk(T0, T1, nr);
         store_tile(G, ld, T0, nr, nc);
@@ -1016,7 +1037,8 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       break;
     }
     case X_PT_DIAG:
-    case X_PT_UPD: {
+    case X_PT_UPD:
+    case X_PT_FUSED: {
       // TSTRF on panel X (cols C_X): U = upper of diagonal block D restricted to C_X
       const BlockDev D = P.blk[tk.d];
       const int m = D.nrows, ld = A.nR;
@@ -1024,10 +1046,18 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       const int r0 = tk.r * XT, c0 = tk.c * XT, nr = min(XT, A.nR - r0), nc = min(XT, A.nC - c0);
       double* G = P.vals + A.ent + static_cast<size_t>(c0) * ld + r0;
       const double* Dv = P.vals + D.ent;
-      if (tk.type == X_PT_DIAG) {
+      if (tk.type == X_PT_DIAG || tk.type == X_PT_FUSED) {
+        load_tile(T0, G, ld, nr, nc);
+        if (tk.type == X_PT_FUSED) {  // the update from the previous column step first
+          const int k0 = tk.k * XT, nk = min(XT, A.nC - k0);
+          load_opA(T1, P.vals + A.ent + static_cast<size_t>(k0) * ld + r0, ld, nr, nk);
+          if (Cl) load_opB(T2, Dv, m, nk, nc, Cl + k0, Cl + c0);
+          else load_opB(T2, Dv + static_cast<size_t>(c0) * m + k0, m, nk, nc);
+          __syncthreads();
+          tile_mma_sub(T0, T1, T2);
+        }
         if (Cl) load_tile(T1, Dv, m, nc, nc, Cl + c0, Cl + c0);
         else load_tile(T1, Dv + static_cast<size_t>(c0) * m + c0, m, nc, nc);
-        load_tile(T0, G, ld, nr, nc);
         __syncthreads();
         if (threadIdx.x < XT) rinv[threadIdx.x] = threadIdx.x < nc ? 1.0 / T1[threadIdx.x * XTP + threadIdx.x] : 1.0;
         __syncthreads();

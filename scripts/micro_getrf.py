@@ -29,7 +29,7 @@ if "--trace" in sys.argv:
     tr, info = eng.exec_trace()
     tr = tr.astype(np.int64)
     t0 = tr[:, 0][tr[:, 0] > 0].min()
-    names = ["COLMAX", "GETRF", "TRSM_L", "TRSM_U", "GEMM", "FINAL", "PG_DIAG", "PG_UPD", "PT_DIAG", "PT_UPD"]
+    names = ["COLMAX", "GETRF", "TRSM_L", "TRSM_U", "GEMM", "FINAL", "PG_DIAG", "PG_UPD", "PT_DIAG", "PT_UPD", "BAND", "GETRF_UPD", "PG_FUSED", "PT_FUSED"]
     for ty in np.unique(info[:, 0]):
         sel = info[:, 0] == ty
         run = (tr[sel, 2] - tr[sel, 1]) / 1e3
@@ -40,7 +40,7 @@ if "--trace" in sys.argv:
         print(f"{names[ty]:8s} n={sel.sum():6d} run us med {np.median(run):7.2f} p90 {np.percentile(run, 90):7.2f}"
               f" wait med {np.median(wait):8.2f} phases(ready>p0>p1>p2>p3>fence>done) "
               + " ".join("-" if np.all(np.isnan(d[:, k])) else f"{np.nanmedian(d[:, k]):.2f}" for k in range(6)))
-    g = np.flatnonzero(info[:, 0] == 1)
+    g = np.flatnonzero((info[:, 0] == 1) | (info[:, 0] == 11))
     for t in g[:6]:
         print(f"GETRF k={info[t, 4]} dequeue {(tr[t, 0] - t0) / 1e3:9.1f} ready {(tr[t, 1] - t0) / 1e3:9.1f}"
               f" done {(tr[t, 2] - t0) / 1e3:9.1f} us")

@@ -14,7 +14,7 @@ eng.upload()
 eng.run_device()
 tr, info = eng.exec_trace()
 tr = tr.astype(np.int64)
-names = ["COLMAX", "GETRF", "TRSM_L", "TRSM_U", "GEMM", "FINAL", "PG_DIAG", "PG_UPD", "PT_DIAG", "PT_UPD", "BAND"]
+names = ["COLMAX", "GETRF", "TRSM_L", "TRSM_U", "GEMM", "FINAL", "PG_DIAG", "PG_UPD", "PT_DIAG", "PT_UPD", "BAND", "GETRF_UPD", "PG_FUSED", "PT_FUSED"]
 ok = tr[:, 2] > 0
 for ty in np.unique(info[:, 0]):
     sel = (info[:, 0] == ty) & ok
