@@ -70,8 +70,10 @@ struct Level {
   int32_t nitems, warps, acc_len;
   int64_t gemm_off;  // SSSSM DMMA tiles
   int32_t ngemm;
-  int64_t gemmD_off;  // deferred SSSSM DMMA tiles (every successor >= 2 tree levels later)
+  int64_t gemmD_off;  // deferred SSSSM DMMA tiles (every successor exactly 2 tree levels later)
   int32_t ngemmD;
+  int64_t gemmE_off;  // deferred SSSSM DMMA tiles with >= 3 levels of slack
+  int32_t ngemmE;
   int64_t panel_off;  // dense GESSM/TSTRF strips
   int32_t npanel;
   int32_t panel_smem;
@@ -172,7 +174,8 @@ struct lbk_ctx {
   cudaEvent_t fork = nullptr, join[NBRANCH] = {nullptr, nullptr, nullptr};
   cudaStream_t dstream = nullptr;     // deferred SSSSM branch (lowest priority)
   cudaEvent_t dfork = nullptr;
-  std::vector<cudaEvent_t> dev;       // per launch level: deferred work done
+  std::vector<cudaEvent_t> dev, dev2; // per launch level: deferred work done (slack 2 / >= 3)
+  cudaStream_t dstream2 = nullptr;
   std::vector<int8_t> defer;          // per task: may run concurrently with the next level
   int exec_per_sm = 2;
   int defer_ctas = 0;  // > 0: deferred SSSSM work on this many looping CTAs (LBK_DEFER_CTAS)
@@ -350,6 +353,7 @@ int lbk_create(lbk_ctx** out, int device, lbk_status* st) {
   }
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->dstream, cudaStreamNonBlocking, prio_lo);
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->dstream2, cudaStreamNonBlocking, prio_lo);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->dfork, cudaEventDisableTiming);
   if (const char* x = std::getenv("LBK_EXEC_PER_SM")) c->exec_per_sm = std::max(1, std::atoi(x));
   if (const char* x = std::getenv("LBK_DEFER_CTAS")) c->defer_ctas = std::max(0, std::atoi(x));
@@ -375,7 +379,9 @@ void lbk_destroy(lbk_ctx* c) {
   }
   if (c->fork) cudaEventDestroy(c->fork);
   for (auto ev : c->dev) cudaEventDestroy(ev);
+  for (auto ev : c->dev2) cudaEventDestroy(ev);
   if (c->dstream) cudaStreamDestroy(c->dstream);
+  if (c->dstream2) cudaStreamDestroy(c->dstream2);
   if (c->dfork) cudaEventDestroy(c->dfork);
   if (c->solve_graph) cudaGraphExecDestroy(c->solve_graph);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -627,7 +633,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     for (int64_t t = 0; t < ntasks; ++t) nlevels = std::max(nlevels, tlevels[t] + 1);
     std::vector<std::vector<Item>> gen(nlevels);
     std::vector<int32_t> acc_len(nlevels, 1);
-    std::vector<std::vector<GemmItem>> gem(nlevels), gemD(nlevels);
+    std::vector<std::vector<GemmItem>> gem(nlevels), gemD(nlevels), gemE(nlevels);
     std::vector<GemmTask> gtasks;
     std::vector<int32_t> hmaps;
     std::vector<std::vector<DenseItem>> pan(nlevels), exa(nlevels);
@@ -805,7 +811,8 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           c->route[t] = 1;
           c->dmma_flops += 2.0 * hb[lb].nR * static_cast<double>(gt.K) * hb[ub].nC;
           gtasks.push_back(gt);
-          auto& dst = (!c->defer.empty() && c->defer[t]) ? gemD[lv] : gem[lv];
+          const int slack = c->defer.empty() ? 0 : c->defer[t];
+          auto& dst = slack >= 3 ? gemE[lv] : slack == 2 ? gemD[lv] : gem[lv];
           for (int32_t n0 = 0; n0 < hb[ub].nC; n0 += GBN)
             for (int32_t m0 = 0; m0 < hb[lb].nR; m0 += GBM) dst.push_back(GemmItem{task, m0, n0});
           continue;
@@ -828,7 +835,9 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     c->levels.clear();
     c->subs.clear();
     for (int32_t lv = 0; lv < nlevels; ++lv) {
-      if (gen[lv].empty() && gem[lv].empty() && gemD[lv].empty() && pan[lv].empty() && exa[lv].empty()) continue;
+      if (gen[lv].empty() && gem[lv].empty() && gemD[lv].empty() && gemE[lv].empty() && pan[lv].empty() &&
+          exa[lv].empty())
+        continue;
       if (static_cast<int64_t>(acc_len[lv]) * 8 > MAX_SMEM || pan_smem[lv] > MAX_SMEM || exa_smem[lv] > MAX_SMEM)
         return fail(st, LBK_ERR_BAD_ARG, "block span too large for the shared-memory accumulator");
       Level L{};
@@ -844,6 +853,9 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       L.gemmD_off = static_cast<int64_t>(mall.size());
       L.ngemmD = static_cast<int32_t>(gemD[lv].size());
       mall.insert(mall.end(), gemD[lv].begin(), gemD[lv].end());
+      L.gemmE_off = static_cast<int64_t>(mall.size());
+      L.ngemmE = static_cast<int32_t>(gemE[lv].size());
+      mall.insert(mall.end(), gemE[lv].begin(), gemE[lv].end());
       L.panel_off = static_cast<int64_t>(dall.size());
       L.npanel = static_cast<int32_t>(pan[lv].size());
       L.panel_smem = pan_smem[lv];
@@ -1183,8 +1195,11 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
   }
   drop_graphs(c);
   for (auto ev : c->dev) cudaEventDestroy(ev);
+  for (auto ev : c->dev2) cudaEventDestroy(ev);
   c->dev.assign(c->levels.size(), nullptr);
+  c->dev2.assign(c->levels.size(), nullptr);
   for (auto& ev : c->dev) LBK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), st);
+  for (auto& ev : c->dev2) LBK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), st);
   ok(st);
   return 0;
 }
@@ -1229,12 +1244,12 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
   if (evs && first) cudaEventRecordWithFlags((*evs)[0], s0, cudaEventRecordExternal);
   // deferred SSSSM work of launch level l runs beside the next tree level; a
   // level at tree level T waits for the deferred work of tree levels <= T - 2
-  std::vector<size_t> pending;
+  std::vector<std::pair<cudaEvent_t, int32_t>> pending;  // (done event, first tree level that needs it)
   for (size_t l = lo; l < hi; ++l) {
     const Level& L = c->levels[l];
     for (size_t q = 0; q < pending.size();) {
-      if (c->levels[pending[q]].tree_level <= L.tree_level - 2) {
-        cudaStreamWaitEvent(s0, c->dev[pending[q]], 0);
+      if (pending[q].second <= L.tree_level) {
+        cudaStreamWaitEvent(s0, pending[q].first, 0);
         pending.erase(pending.begin() + q);
       } else {
         ++q;
@@ -1244,7 +1259,7 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
     const bool br[NBRANCH] = {L.ngemm > 0, (!use_exec && L.npanel > 0) || (exact && L.nexact > 0), has_t};
     // instrumented replays: per level [end, gemm b/e, panel b/e, getrf b/e, csc b/e]
     auto rec = [&](int k, cudaStream_t s) {
-      if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 11 + k], s, cudaEventRecordExternal);
+      if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 12 + k], s, cudaEventRecordExternal);
     };
     if (br[0] || br[1] || br[2]) cudaEventRecord(c->fork, s0);
     if (br[0]) {
@@ -1303,24 +1318,31 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
     }
     for (int k = 0; k < NBRANCH; ++k)
       if (br[k]) cudaStreamWaitEvent(s0, c->join[k], 0);
-    if (L.ngemmD) {
+    if (L.ngemmD || L.ngemmE) {
       // deferred SSSSM updates start once this level's critical work is done
-      // and run (low stream priority) beside the next level
+      // and run (low stream priority) beside the next one (slack 2) or two
+      // (slack >= 3) levels
       cudaEventRecord(c->dfork, s0);
-      cudaStreamWaitEvent(c->dstream, c->dfork, 0);
-      if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 11 + 9], c->dstream, cudaEventRecordExternal);
-      if (c->defer_ctas > 0)
-        gemm_map_loop_kernel<<<std::min(L.ngemmD, c->defer_ctas), 256, GEMM_SMEM, c->dstream>>>(
-            c->gitems.p + L.gemmD_off, L.ngemmD, c->gtasks.p, P);
-      else
-        gemm_map_kernel<<<L.ngemmD, 256, GEMM_SMEM, c->dstream>>>(c->gitems.p + L.gemmD_off, c->gtasks.p, P);
-      if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 11 + 10], c->dstream, cudaEventRecordExternal);
-      cudaEventRecord(c->dev[l], c->dstream);
-      pending.push_back(l);
+      if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 12 + 9], s0, cudaEventRecordExternal);
+      for (int cls = 0; cls < 2; ++cls) {
+        const int32_t nd = cls ? L.ngemmE : L.ngemmD;
+        if (!nd) continue;
+        cudaStream_t ds = cls ? c->dstream2 : c->dstream;
+        cudaStreamWaitEvent(ds, c->dfork, 0);
+        const GemmItem* items = c->gitems.p + (cls ? L.gemmE_off : L.gemmD_off);
+        if (c->defer_ctas > 0)
+          gemm_map_loop_kernel<<<std::min(nd, c->defer_ctas), 256, GEMM_SMEM, ds>>>(items, nd, c->gtasks.p, P);
+        else
+          gemm_map_kernel<<<nd, 256, GEMM_SMEM, ds>>>(items, c->gtasks.p, P);
+        if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 12 + 10 + cls], ds, cudaEventRecordExternal);
+        cudaEvent_t ev = cls ? c->dev2[l] : c->dev[l];
+        cudaEventRecord(ev, ds);
+        pending.push_back({ev, L.tree_level + (cls ? 3 : 2)});
+      }
     }
     rec(0, s0);
   }
-  for (size_t q : pending) cudaStreamWaitEvent(s0, c->dev[q], 0);
+  for (const auto& pq : pending) cudaStreamWaitEvent(s0, pq.first, 0);
   if (last) gather_kernel<<<148 * 8, 256, 0, s0>>>(c->vals.p, c->map.p, c->vout.p, c->nnz);
 }
 
@@ -1695,7 +1717,7 @@ void lbk_host_free(void* ptr) {
 int lbk_level_times(lbk_ctx* c, double pivot_tol, double static_eps, float* out_ms, lbk_status* st) {
   LBK_CUDA(cudaSetDevice(c->device), st);
   const size_t nl = c->levels.size();
-  std::vector<cudaEvent_t> ev(1 + nl * 11);
+  std::vector<cudaEvent_t> ev(1 + nl * 12);
   for (auto& e : ev) LBK_CUDA(cudaEventCreate(&e), st);
   cudaGraph_t g;
   cudaGraphExec_t ge = nullptr;
@@ -1711,16 +1733,17 @@ int lbk_level_times(lbk_ctx* c, double pivot_tol, double static_eps, float* out_
   if (e == cudaSuccess)
     for (size_t l = 0; l < nl; ++l) {
       const Level& L = c->levels[l];
-      const size_t b = 1 + l * 11, prev = l ? 1 + (l - 1) * 11 : 0;
+      const size_t b = 1 + l * 12, prev = l ? 1 + (l - 1) * 12 : 0;
       float* o = out_ms + l * 5;
       for (int k = 0; k < 5; ++k) o[k] = 0.f;
       cudaEventElapsedTime(&o[0], ev[prev], ev[b]);
       if (L.ngemm) cudaEventElapsedTime(&o[1], ev[b + 1], ev[b + 2]);
-      if (L.ngemmD) {  // deferred DMMA SSSSM: counted with the family (it overlaps the next level)
-        float d = 0.f;
-        cudaEventElapsedTime(&d, ev[b + 9], ev[b + 10]);
-        o[1] += d;
-      }
+      for (int cls = 0; cls < 2; ++cls)  // deferred DMMA SSSSM: counted with the family (overlaps the next levels)
+        if (cls ? L.ngemmE : L.ngemmD) {
+          float d = 0.f;
+          cudaEventElapsedTime(&d, ev[b + 9], ev[b + 10 + cls]);
+          o[1] += d;
+        }
       if (L.npanel || (exact && L.nexact)) cudaEventElapsedTime(&o[2], ev[b + 3], ev[b + 4]);
       if (!exact && L.ntcol) cudaEventElapsedTime(&o[3], ev[b + 5], ev[b + 6]);
       if (L.nitems) cudaEventElapsedTime(&o[4], ev[b + 7], ev[b + 8]);
@@ -1799,7 +1822,7 @@ int lbk_plan_info(lbk_ctx* c, int64_t* info) {
   info[5] = c->n_panel;
   int64_t launches = 2;  // scatter + gather
   for (const Level& L : c->levels) {
-    launches += (L.nitems > 0) + (L.ngemm > 0) + (L.ngemmD > 0);
+    launches += (L.nitems > 0) + (L.ngemm > 0) + (L.ngemmD > 0) + (L.ngemmE > 0);
     if (c->use_exec) {
       launches += L.nexec > 0;
       continue;

@@ -88,10 +88,12 @@ def _dev():
 
 
 def defer_flags(tree) -> np.ndarray | None:
-    """int8 per task: 1 if every successor sits >= 2 ASAP levels later, so the
-    task may run concurrently with the next level (the engine defers such DMMA
-    SSSSM updates onto a side branch: lookahead across levels).  Needs the
-    tree's predecessor lists (grid.py:172-181); None without them."""
+    """int8 per task: its slack, min(successor level) - own level, capped at
+    100 (0 for tasks without successors is never produced: every update has
+    one).  Slack >= 2: the task may run concurrently with the following
+    slack - 1 levels (the engine defers such DMMA SSSSM updates onto low-
+    priority side branches: lookahead across levels).  Needs the tree's
+    predecessor lists (grid.py:172-181); None without them."""
     pp = getattr(tree, "pred_ptr", None)
     pi = getattr(tree, "pred_idx", None)
     if pp is None or pi is None:
@@ -100,7 +102,7 @@ def defer_flags(tree) -> np.ndarray | None:
     nt = len(lv)
     minsucc = np.full(nt, np.iinfo(np.int64).max, np.int64)
     np.minimum.at(minsucc, np.asarray(pi, np.int64), np.repeat(lv, np.diff(np.asarray(pp, np.int64))))
-    return (minsucc >= lv + 2).astype(np.int8)
+    return np.clip(minsucc - lv, 0, 100).astype(np.int8)
 
 
 def fp64_peak(device: int = 0) -> tuple[float, float]:
