@@ -123,7 +123,11 @@ int lbk_upload_values(lbk_ctx* ctx, const double* values, lbk_status* st);
 int lbk_factorize(lbk_ctx* ctx, double pivot_tol, double static_eps, float* ms, lbk_status* st);
 
 /* End-to-end: host A values in, host factor values (pool order, in place of
- * A's pattern) and per-diagonal-row local permutations out. */
+ * A's pattern) and per-diagonal-row local permutations out.  With a page-
+ * locked lu_values buffer (lbk_host_alloc / cudaHostRegister) every block's
+ * factor values are gathered and copied to the host on a copy stream as soon
+ * as the level that finishes the block is done, overlapping the rest of the
+ * factorization (one cached graph per output buffer). */
 int lbk_factorize_host(lbk_ctx* ctx, const double* a_values, double* lu_values, int32_t* perms,
                        double pivot_tol, double static_eps, lbk_status* st);
 

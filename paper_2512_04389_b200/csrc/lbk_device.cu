@@ -218,6 +218,21 @@ struct lbk_ctx {
   std::vector<char> isdiag;
   // device triangular solve (lbk_solve): block grid + lazily built graph
   std::vector<int64_t> pos, hbi, hbj;
+  // streamed end-to-end output: each block's factor values leave for the host
+  // as soon as the level that finishes it is done (lbk_factorize_host)
+  std::vector<int32_t> blk_final_tl;  // tree level of the task that finishes each block
+
+  std::vector<int64_t> ref_off, ref_len;  // reference pool range of each block
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t cev = nullptr;
+  std::vector<cudaEvent_t> lev;     // per launch level: critical work done (copy-stream fork)
+  cudaGraphExec_t sgraph = nullptr;
+  double* sgraph_out = nullptr;
+  double s_tol = NAN, s_eps = NAN;
+  DevBuf<int64_t> sranges;          // (offset, length) pairs, grouped by launch level
+  std::vector<int64_t> hsranges;
+  std::vector<int64_t> spiece_off;  // per launch level: first gather piece (+ sentinel)
+  std::vector<int64_t> srange_off;  // per launch level: first pair index (+ sentinel)
   std::vector<int32_t> dext;       // per diagonal block, per 64-col chunk: (row hi, row lo) of its pattern
   std::vector<int64_t> dext_off;   // per block: offset into dext (diagonal blocks)
   DevBuf<int32_t> sdext;
@@ -354,6 +369,9 @@ int lbk_create(lbk_ctx** out, int device, lbk_status* st) {
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->dstream, cudaStreamNonBlocking, prio_lo);
   if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&c->dstream2, cudaStreamNonBlocking, prio_lo);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking);
+
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->cev, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->dfork, cudaEventDisableTiming);
   if (const char* x = std::getenv("LBK_EXEC_PER_SM")) c->exec_per_sm = std::max(1, std::atoi(x));
   if (const char* x = std::getenv("LBK_DEFER_CTAS")) c->defer_ctas = std::max(0, std::atoi(x));
@@ -382,6 +400,11 @@ void lbk_destroy(lbk_ctx* c) {
   for (auto ev : c->dev2) cudaEventDestroy(ev);
   if (c->dstream) cudaStreamDestroy(c->dstream);
   if (c->dstream2) cudaStreamDestroy(c->dstream2);
+  if (c->cstream) cudaStreamDestroy(c->cstream);
+
+  if (c->cev) cudaEventDestroy(c->cev);
+  for (auto ev : c->lev) cudaEventDestroy(ev);
+  if (c->sgraph) cudaGraphExecDestroy(c->sgraph);
   if (c->dfork) cudaEventDestroy(c->dfork);
   if (c->solve_graph) cudaGraphExecDestroy(c->solve_graph);
   if (c->stream) cudaStreamDestroy(c->stream);
@@ -423,6 +446,18 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     // ---- storage kind, R / C lists ------------------------------------------------
     std::vector<BlockDev> hb(nb);
     c->wlen.assign(nb, 0);
+    c->ref_off.assign(T_ent, T_ent + nb);
+    c->ref_len.assign(T_nz, T_nz + nb);
+    c->blk_final_tl.assign(nb, -1);
+    for (int64_t t = 0; t < ntasks; ++t) {
+      const int64_t i = steps[t];
+      int64_t fb = -1;
+      if (kinds[t] == KIND_GETRF) fb = bid[i * p + i];
+      else if (kinds[t] == KIND_GESSM) fb = bid[i * p + tcols[t]];
+      else if (kinds[t] == KIND_TSTRF) fb = bid[trows[t] * p + i];
+      if (fb >= 0) c->blk_final_tl[fb] = tlevels[t];
+    }
+
     c->dext.clear();
     c->dext_off.assign(nb, -1);
     c->isdiag.assign(nb, 0);
@@ -1198,6 +1233,49 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
   for (auto ev : c->dev2) cudaEventDestroy(ev);
   c->dev.assign(c->levels.size(), nullptr);
   c->dev2.assign(c->levels.size(), nullptr);
+  for (auto ev : c->lev) cudaEventDestroy(ev);
+  c->lev.assign(c->levels.size(), nullptr);
+  for (auto& ev : c->lev) LBK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), st);
+  if (c->sgraph) {
+    cudaGraphExecDestroy(c->sgraph);
+    c->sgraph = nullptr;
+  }
+  {
+    // per launch level: the reference-pool ranges of the blocks it finishes
+    // (adjacent blocks merged; pool order is column-major block order)
+    std::vector<std::vector<std::pair<int64_t, int64_t>>> per(c->levels.size());
+    std::vector<int32_t> tl_to_l;
+    for (size_t l = 0; l < c->levels.size(); ++l) {
+      const int32_t tl = c->levels[l].tree_level;
+      if (static_cast<int32_t>(tl_to_l.size()) <= tl) tl_to_l.resize(tl + 1, -1);
+      tl_to_l[tl] = static_cast<int32_t>(l);
+    }
+    for (int64_t b = 0; b < nb; ++b) {
+      const int32_t tl = c->blk_final_tl[b];
+      if (tl < 0 || tl >= static_cast<int32_t>(tl_to_l.size()) || tl_to_l[tl] < 0 || c->ref_len[b] == 0) continue;
+      auto& v = per[tl_to_l[tl]];
+      if (!v.empty() && v.back().first + v.back().second == c->ref_off[b]) v.back().second += c->ref_len[b];
+      else v.push_back({c->ref_off[b], c->ref_len[b]});
+    }
+    std::vector<int64_t> flat, pieces;  // copy ranges; gather pieces of <= 64K entries (one CTA each)
+    c->srange_off.assign(1, 0);
+    c->spiece_off.assign(1, 0);
+    constexpr int64_t PIECE = 1 << 16;
+    for (auto& v : per) {
+      for (auto& pr : v) {
+        flat.push_back(pr.first);
+        flat.push_back(pr.second);
+        for (int64_t o = 0; o < pr.second; o += PIECE) {
+          pieces.push_back(pr.first + o);
+          pieces.push_back(std::min(PIECE, pr.second - o));
+        }
+      }
+      c->srange_off.push_back(static_cast<int64_t>(flat.size() / 2));
+      c->spiece_off.push_back(static_cast<int64_t>(pieces.size() / 2));
+    }
+    LBK_CUDA(c->sranges.upload(pieces.empty() ? std::vector<int64_t>(2, 0) : pieces), st);
+    c->hsranges = flat;
+  }
   for (auto& ev : c->dev) LBK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), st);
   for (auto& ev : c->dev2) LBK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), st);
   ok(st);
@@ -1222,15 +1300,15 @@ namespace {
 // Launch levels [lo, hi) only; the prologue (zero, scatter, counter reset)
 // belongs to the first segment and the gather to the last one.
 void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std::vector<cudaEvent_t>* evs,
-                           size_t lo, size_t hi, bool first, bool last) {
+                           size_t lo, size_t hi, bool first, bool last, double* stream_out = nullptr) {
   DevPools P = pools(c);
   cudaStream_t s0 = c->stream;
   const bool exact = (c->flags & 2) != 0 || !std::isnan(static_eps);
   const bool use_exec = !exact && c->use_exec;
   if (first) {
   cudaMemsetAsync(c->err.p, 0xff, 2 * sizeof(unsigned long long), s0);
-  cudaMemsetAsync(c->vals.p, 0, c->nnz_work * sizeof(double), s0);
-  scatter_kernel<<<148 * 8, 256, 0, s0>>>(c->vin.p, c->map.p, c->vals.p, c->nnz);
+    cudaMemsetAsync(c->vals.p, 0, c->nnz_work * sizeof(double), s0);
+    scatter_kernel<<<148 * 8, 256, 0, s0>>>(c->vin.p, c->map.p, c->vals.p, c->nnz);
   if (use_exec && c->n_exec) {
     cudaMemcpyAsync(c->xdeps.p, c->xdeps0.p, c->n_exec * sizeof(int), cudaMemcpyDeviceToDevice, s0);
     cudaMemsetAsync(c->xheads.p, 0, c->levels.size() * sizeof(int), s0);
@@ -1318,6 +1396,19 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
     }
     for (int k = 0; k < NBRANCH; ++k)
       if (br[k]) cudaStreamWaitEvent(s0, c->join[k], 0);
+    if (stream_out && c->srange_off[l + 1] > c->srange_off[l]) {
+      // the blocks this level finished: gather + copy to the host on the copy stream
+      cudaEventRecord(c->lev[l], s0);
+      cudaStreamWaitEvent(c->cstream, c->lev[l], 0);
+      const int64_t r0 = c->srange_off[l], nr = c->srange_off[l + 1] - r0;
+      const int64_t p0 = c->spiece_off[l], np_ = c->spiece_off[l + 1] - p0;
+      range_gather_kernel<<<static_cast<int>(std::min<int64_t>(np_, 148 * 4)), 256, 0, c->cstream>>>(
+          c->vals.p, c->map.p, c->vout.p, c->sranges.p + 2 * p0, np_);
+      for (int64_t q = 0; q < nr; ++q) {
+        const int64_t off = c->hsranges[2 * (r0 + q)], len = c->hsranges[2 * (r0 + q) + 1];
+        cudaMemcpyAsync(stream_out + off, c->vout.p + off, len * sizeof(double), cudaMemcpyDeviceToHost, c->cstream);
+      }
+    }
     if (L.ngemmD || L.ngemmE) {
       // deferred SSSSM updates start once this level's critical work is done
       // and run (low stream priority) beside the next one (slack 2) or two
@@ -1343,6 +1434,11 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
     rec(0, s0);
   }
   for (const auto& pq : pending) cudaStreamWaitEvent(s0, pq.first, 0);
+  if (stream_out) {
+    cudaEventRecord(c->cev, c->cstream);
+    cudaStreamWaitEvent(s0, c->cev, 0);
+    return;
+  }
   if (last) gather_kernel<<<148 * 8, 256, 0, s0>>>(c->vals.p, c->map.p, c->vout.p, c->nnz);
 }
 
@@ -1445,6 +1541,36 @@ int lbk_factorize(lbk_ctx* c, double pivot_tol, double static_eps, float* ms, lb
 int lbk_factorize_host(lbk_ctx* c, const double* a_values, double* lu_values, int32_t* perms, double pivot_tol,
                        double static_eps, lbk_status* st) {
   LBK_CUDA(cudaSetDevice(c->device), st);
+  cudaPointerAttributes pa{};
+  const bool pinned = cudaPointerGetAttributes(&pa, lu_values) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+  (void)cudaGetLastError();
+  if (pinned && nsegments(c) == 1) {
+    // streamed output: every block's factor values are copied to the host while
+    // later levels still run (one graph per output buffer)
+    if (!c->sgraph || c->sgraph_out != lu_values || !same(c->s_tol, pivot_tol) || !same(c->s_eps, static_eps)) {
+      if (c->sgraph) cudaGraphExecDestroy(c->sgraph);
+      c->sgraph = nullptr;
+      cudaGraph_t g;
+      LBK_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), st);
+      (void)cudaGetLastError();
+      capture_factorization(c, pivot_tol, static_eps, nullptr, 0, c->levels.size(), true, true, lu_values);
+      cudaError_t e = cudaStreamEndCapture(c->stream, &g);
+      if (e != cudaSuccess) return cuda_fail(st, e, "streamed graph capture");
+      e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaGraphInstantiate(&c->sgraph, g, cudaGraphInstantiateFlagUseNodePriority);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return cuda_fail(st, e, "streamed graph");
+      c->sgraph_out = lu_values;
+      c->s_tol = pivot_tol;
+      c->s_eps = static_eps;
+    }
+    LBK_CUDA(cudaMemcpyAsync(c->vin.p, a_values, c->nnz * sizeof(double), cudaMemcpyHostToDevice, c->stream), st);
+    LBK_CUDA(cudaGraphLaunch(c->sgraph, c->stream), st);
+    if (perms && c->ndiag_rows)
+      LBK_CUDA(cudaMemcpyAsync(perms, c->perm.p, c->ndiag_rows * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream),
+               st);
+    return finish(c, st);
+  }
   if (build_graph(c, pivot_tol, static_eps, st)) return st->code;
   LBK_CUDA(cudaMemcpyAsync(c->vin.p, a_values, c->nnz * sizeof(double), cudaMemcpyHostToDevice, c->stream), st);
   LBK_CUDA(launch_all(c), st);

@@ -252,6 +252,16 @@ __global__ void scatter_kernel(const double* __restrict__ in, const int64_t* __r
     work[map[e]] = in[e];
 }
 
+// ranges[2 x n] = (offset, length) of reference-pool entries to gather (one CTA
+// per range, strided).
+__global__ void range_gather_kernel(const double* __restrict__ work, const int64_t* __restrict__ map,
+                                    double* __restrict__ out, const int64_t* __restrict__ ranges, int64_t n) {
+  for (int64_t q = blockIdx.x; q < n; q += gridDim.x) {
+    const int64_t off = ranges[2 * q], len = ranges[2 * q + 1];
+    for (int64_t e = threadIdx.x; e < len; e += blockDim.x) out[off + e] = work[map[off + e]];
+  }
+}
+
 __global__ void gather_kernel(const double* __restrict__ work, const int64_t* __restrict__ map,
                               double* __restrict__ out, int64_t n) {
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
