@@ -131,6 +131,15 @@ int lbk_factorize(lbk_ctx* ctx, double pivot_tol, double static_eps, float* ms, 
 int lbk_factorize_host(lbk_ctx* ctx, const double* a_values, double* lu_values, int32_t* perms,
                        double pivot_tol, double static_eps, lbk_status* st);
 
+/* Refactorization input (new values on A's pattern, KLU-style refactor):
+ * lbk_bind_matrix gives the reference-pool position of every entry of A in
+ * CSC order (grid.pool_positions); lbk_refactor_host then takes A's nnz values
+ * instead of the whole pool (fill entries are zero) and is otherwise
+ * lbk_factorize_host. */
+int lbk_bind_matrix(lbk_ctx* ctx, int64_t nnz_a, const int64_t* pool_pos, lbk_status* st);
+int lbk_refactor_host(lbk_ctx* ctx, const double* a_values, double* lu_values, int32_t* perms, double pivot_tol,
+                      double static_eps, lbk_status* st);
+
 /* Copy the last factorization's values / perms to the host. */
 int lbk_download(lbk_ctx* ctx, double* lu_values, int32_t* perms, lbk_status* st);
 

@@ -232,6 +232,10 @@ struct lbk_ctx {
   DevBuf<int64_t> sranges;          // (offset, length) pairs, grouped by launch level
   std::vector<int64_t> hsranges;
   std::vector<int64_t> spiece_off;  // per launch level: first gather piece (+ sentinel)
+  // refactorization input: A's entries (CSC order) -> reference pool positions
+  DevBuf<int64_t> amap;
+  DevBuf<double> avals;
+  int64_t nnz_a = 0;
   std::vector<int64_t> srange_off;  // per launch level: first pair index (+ sentinel)
   std::vector<int32_t> dext;       // per diagonal block, per 64-col chunk: (row hi, row lo) of its pattern
   std::vector<int64_t> dext_off;   // per block: offset into dext (diagonal blocks)
@@ -1538,9 +1542,52 @@ int lbk_factorize(lbk_ctx* c, double pivot_tol, double static_eps, float* ms, lb
 
 // End-to-end: host A values in, host factor values (reference pool order)
 // and per-diagonal-row local permutations out.
+namespace {
+int factorize_host_impl(lbk_ctx* c, const double* a_values, bool a_is_pool, double* lu_values, int32_t* perms,
+                        double pivot_tol, double static_eps, lbk_status* st);
+}
+
 int lbk_factorize_host(lbk_ctx* c, const double* a_values, double* lu_values, int32_t* perms, double pivot_tol,
                        double static_eps, lbk_status* st) {
+  return factorize_host_impl(c, a_values, true, lu_values, perms, pivot_tol, static_eps, st);
+}
+
+int lbk_bind_matrix(lbk_ctx* c, int64_t nnz_a, const int64_t* pool_pos, lbk_status* st) {
   LBK_CUDA(cudaSetDevice(c->device), st);
+  for (int64_t k = 0; k < nnz_a; ++k)
+    if (pool_pos[k] < 0 || pool_pos[k] >= c->nnz) return fail(st, LBK_ERR_DIM_MISMATCH, "pool position out of range");
+  LBK_CUDA(c->amap.alloc(std::max<int64_t>(nnz_a, 1)), st);
+  if (nnz_a) LBK_CUDA(cudaMemcpy(c->amap.p, pool_pos, nnz_a * sizeof(int64_t), cudaMemcpyHostToDevice), st);
+  LBK_CUDA(c->avals.alloc(std::max<int64_t>(nnz_a, 1)), st);
+  c->nnz_a = nnz_a;
+  ok(st);
+  return 0;
+}
+
+int lbk_refactor_host(lbk_ctx* c, const double* a_values, double* lu_values, int32_t* perms, double pivot_tol,
+                      double static_eps, lbk_status* st) {
+  if (!c->amap.p) return fail(st, LBK_ERR_BAD_ARG, "lbk_refactor_host before lbk_bind_matrix");
+  return factorize_host_impl(c, a_values, false, lu_values, perms, pivot_tol, static_eps, st);
+}
+
+}  // extern "C"
+
+namespace {
+int factorize_host_impl(lbk_ctx* c, const double* a_values, bool a_is_pool, double* lu_values, int32_t* perms,
+                        double pivot_tol, double static_eps, lbk_status* st) {
+  LBK_CUDA(cudaSetDevice(c->device), st);
+  // A's values into the reference pool (vin): the whole pool, or A's entries
+  // expanded through the bound positions (fill entries are zero)
+  auto upload_input = [&]() -> cudaError_t {
+    if (a_is_pool)
+      return cudaMemcpyAsync(c->vin.p, a_values, c->nnz * sizeof(double), cudaMemcpyHostToDevice, c->stream);
+    cudaError_t e = cudaMemcpyAsync(c->avals.p, a_values, c->nnz_a * sizeof(double), cudaMemcpyHostToDevice,
+                                    c->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(c->vin.p, 0, c->nnz * sizeof(double), c->stream);
+    if (e == cudaSuccess && c->nnz_a)
+      expand_kernel<<<148 * 4, 256, 0, c->stream>>>(c->avals.p, c->amap.p, c->vin.p, c->nnz_a);
+    return e == cudaSuccess ? cudaGetLastError() : e;
+  };
   cudaPointerAttributes pa{};
   const bool pinned = cudaPointerGetAttributes(&pa, lu_values) == cudaSuccess && pa.type == cudaMemoryTypeHost;
   (void)cudaGetLastError();
@@ -1564,7 +1611,7 @@ int lbk_factorize_host(lbk_ctx* c, const double* a_values, double* lu_values, in
       c->s_tol = pivot_tol;
       c->s_eps = static_eps;
     }
-    LBK_CUDA(cudaMemcpyAsync(c->vin.p, a_values, c->nnz * sizeof(double), cudaMemcpyHostToDevice, c->stream), st);
+    LBK_CUDA(upload_input(), st);
     LBK_CUDA(cudaGraphLaunch(c->sgraph, c->stream), st);
     if (perms && c->ndiag_rows)
       LBK_CUDA(cudaMemcpyAsync(perms, c->perm.p, c->ndiag_rows * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream),
@@ -1572,7 +1619,7 @@ int lbk_factorize_host(lbk_ctx* c, const double* a_values, double* lu_values, in
     return finish(c, st);
   }
   if (build_graph(c, pivot_tol, static_eps, st)) return st->code;
-  LBK_CUDA(cudaMemcpyAsync(c->vin.p, a_values, c->nnz * sizeof(double), cudaMemcpyHostToDevice, c->stream), st);
+  LBK_CUDA(upload_input(), st);
   LBK_CUDA(launch_all(c), st);
   LBK_CUDA(cudaMemcpyAsync(lu_values, c->vout.p, c->nnz * sizeof(double), cudaMemcpyDeviceToHost, c->stream), st);
   if (perms && c->ndiag_rows)
@@ -1580,6 +1627,9 @@ int lbk_factorize_host(lbk_ctx* c, const double* a_values, double* lu_values, in
              st);
   return finish(c, st);
 }
+}  // namespace
+
+extern "C" {
 
 // ---- distribution hooks (2D block-cyclic owner-computes, paper_2512_04389_b200/parallel.py) ----
 

@@ -262,6 +262,14 @@ __global__ void range_gather_kernel(const double* __restrict__ work, const int64
   }
 }
 
+// in[pos[k]] = a[k]: A's entries into the reference pool (refactorization input)
+__global__ void expand_kernel(const double* __restrict__ a, const int64_t* __restrict__ pos, double* __restrict__ in,
+                              int64_t n) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    in[pos[k]] = a[k];
+}
+
 __global__ void gather_kernel(const double* __restrict__ work, const int64_t* __restrict__ map,
                               double* __restrict__ out, int64_t n) {
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;

@@ -124,6 +124,21 @@ def pool_grid(grid) -> GridPool:
     return pool
 
 
+def pool_positions(f: FilledPattern, a: CscMatrix, plan: BlockingPlan) -> np.ndarray:
+    """Position in the pooled grid values (reference pool order) of every entry
+    of A (CSC order): partition() run on the entry numbers instead of the
+    values.  Refactorizations with new values on A's pattern then only move
+    A's entries to the device (Engine.bind_matrix / refactor_host)."""
+    ids = CscMatrix(a.n, a.col_ptr, a.row_idx, np.arange(1, a.nnz + 1, dtype=np.float64))
+    vals = partition(f, ids, plan).pool.values
+    nz = np.flatnonzero(vals)
+    pmap = np.full(a.nnz, -1, np.int64)
+    pmap[vals[nz].astype(np.int64) - 1] = nz
+    if (pmap < 0).any():
+        raise DimensionMismatch("A has entries outside the filled pattern")
+    return pmap
+
+
 def partition(f: FilledPattern, a: CscMatrix, plan: BlockingPlan) -> BlockGrid:
     """Cut the filled pattern into blocks, scattering A's values (grid.py:85-148)."""
     n = f.n

@@ -76,6 +76,8 @@ def _dev():
     d(lib, "lbk_set_cuts", C.c_int, [vp, C.c_int64, i8p, st])
     d(lib, "lbk_set_task_defer", C.c_int, [vp, C.c_int64, i8p, st])
     d(lib, "lbk_solve", C.c_int, [vp, f64p, f64p, st])
+    d(lib, "lbk_bind_matrix", C.c_int, [vp, C.c_int64, i64p, st])
+    d(lib, "lbk_refactor_host", C.c_int, [vp, f64p, f64p, i32p, C.c_double, C.c_double, st])
     d(lib, "lbk_num_segments", C.c_int, [vp])
     d(lib, "lbk_run_segment", C.c_int, [vp, C.c_int32, C.c_double, C.c_double, st])
     d(lib, "lbk_finish_raw", C.c_int, [vp, C.POINTER(C.c_float), C.POINTER(C.c_uint64), st])
@@ -283,6 +285,24 @@ class Engine:
         self.lib.lbk_factorize_host(self.ctx, P(a_values, f64p), P(out_values, f64p),
                                     P(out_perms, i32p) if out_perms is not None else None,
                                     pivot_tol, self._eps(static_pivot, self.grid.value_max), C.byref(st))
+        return st
+
+    def bind_matrix(self, pool_pos) -> None:
+        """Reference-pool position of every entry of A (grid.pool_positions): enables refactor_host."""
+        pp = np.ascontiguousarray(pool_pos, dtype=np.int64)
+        st = _native.LbkStatus()
+        if self.lib.lbk_bind_matrix(self.ctx, len(pp), P(pp, i64p), C.byref(st)):
+            _native.raise_status(st, "lbk_bind_matrix")
+        self.nnz_a = len(pp)
+
+    def refactor_host(self, a_values, out_values, out_perms, pivot_tol=DEFAULT_PIVOT_TOL, static_pivot=None):
+        """End to end from A's own values (CSC order, nnz(A)): new values on the
+        same pattern in, factor values (reference pool order) + perms out."""
+        st = _native.LbkStatus()
+        self.generation += 1
+        self.lib.lbk_refactor_host(self.ctx, P(a_values, f64p), P(out_values, f64p),
+                                   P(out_perms, i32p) if out_perms is not None else None,
+                                   pivot_tol, self._eps(static_pivot, self.grid.value_max), C.byref(st))
         return st
 
     def level_times(self, pivot_tol=DEFAULT_PIVOT_TOL, static_pivot=None, check=True) -> np.ndarray:

@@ -111,3 +111,33 @@ def test_streamed_output_matches_plain_download(name):
         assert eng.run_host(vin, streamed, perms).code == 0
         assert np.asarray(streamed).tobytes() == plain.tobytes()
     eng.close()
+
+
+def test_refactor_from_matrix_values():
+    """lbk_refactor_host: A's own values in (bound pool positions) == the pooled path;
+    new values on the same pattern give the factors of the new matrix."""
+    from paper_2512_04389_b200.grid import pool_positions
+    from paper_2512_04389_b200.numeric import Engine, pinned_empty
+
+    a = G.poisson3d(12, "nd")
+    f = M.symbolic_factorize(M.symmetrize_pattern(a))
+    plan = M.irregular_plan(M.percentage_curve(M.diag_block_pointer(f)), a.n)
+    g = M.partition(f, a, plan)
+    t = M.dependency_levels(g)
+    eng = Engine(g, t)
+    eng.bind_matrix(pool_positions(f, a, plan))
+    perms = np.empty(max(eng.n_diag_rows, 1), np.int32)
+    plain = np.empty(eng.nnz)
+    assert eng.run_host(np.ascontiguousarray(g.pool.values), plain, perms).code == 0
+    out = pinned_empty(eng.nnz)
+    assert eng.refactor_host(np.ascontiguousarray(a.values), out, perms).code == 0
+    assert np.asarray(out).tobytes() == plain.tobytes()
+    # new values, same pattern
+    a2 = M.CscMatrix(a.n, a.col_ptr, a.row_idx, a.values * 1.5 + (a.row_idx == np.repeat(
+        np.arange(a.n), np.diff(a.col_ptr))) * 0.25)
+    g2 = M.partition(f, a2, plan)
+    assert eng.refactor_host(np.ascontiguousarray(a2.values), out, perms).code == 0
+    ref = np.empty(eng.nnz)
+    assert eng.run_host(np.ascontiguousarray(g2.pool.values), ref, perms).code == 0
+    assert np.asarray(out).tobytes() == ref.tobytes()
+    eng.close()
