@@ -11,10 +11,11 @@
 // only ever waited on after an earlier index was taken by a running CTA, so
 // progress is guaranteed without co-residency assumptions.
 //
-// Tile kernels keep the 64x64 target tile in registers: thread t owns rows
-// 4*(t%16)..+3 and columns 4*(t/16)..+3; one elimination step costs one or two
-// __syncthreads and <= 16 register FMAs per thread.  Updates are applied in
-// the reference's order with separately rounded mul/sub.
+// Tile kernels stage 64x64 tiles in shared memory and run compact blocked
+// routines (16-column panels: one warp with shuffles for the LU panel, row /
+// column-owning threads for triangular panels, all 256 threads for the
+// trailing updates; DMMA for tile GEMMs).  Critical-chain pairs are fused
+// (last update + LU of a diagonal tile, update + solve of the next panel tile).
 //
 // Mutable tiles may have been written by other SMs during the launch: every
 // global read of tile data uses ld.global.cg (L2, bypassing the
@@ -83,254 +84,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 __device__ __forceinline__ double ldcg(const double* p) { return __ldcg(p); }
 
-// ---- register tiles -------------------------------------------------------------
-// 256 threads = 64 lines x 4 lanes: thread (line = tid/4, q = tid%4) owns the 16
-// entries 4*i+q (i = 0..15) of its line (a row for right solves, a column for
-// left solves).  The 4 lanes of a line sit in one warp, so the value produced
-// at step j is broadcast with one shuffle: no CTA barrier in the solves.
-struct Line {
-  double x[16];
-};
-
-__device__ __forceinline__ int line_id() { return threadIdx.x >> 2; }
-__device__ __forceinline__ void bar_rows64() { asm volatile("bar.sync 1, 64;" ::: "memory"); }
-__device__ __forceinline__ int line_q() { return threadIdx.x & 3; }
-
-// row `r` of a column-major tile: entries (r, 4i+q)
-__device__ __forceinline__ void row_load(Line& L, const double* G, int ld, int nr, int nc,
-                                         const int32_t* rg = nullptr, const int32_t* cg = nullptr) {
-  const int r = line_id(), q = line_q();
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int c = 4 * i + q;
-    L.x[i] = (r < nr && c < nc) ? ldcg(G + static_cast<size_t>(cg ? cg[c] : c) * ld + (rg ? rg[r] : r)) : 0.0;
-  }
-}
-
-__device__ __forceinline__ void row_store(double* G, int ld, const Line& L, int nr, int nc) {
-  const int r = line_id(), q = line_q();
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int c = 4 * i + q;
-    if (r < nr && c < nc) G[static_cast<size_t>(c) * ld + r] = L.x[i];
-  }
-}
-
-// column `c` of a column-major tile: entries (4i+q, c)
-__device__ __forceinline__ void col_load(Line& L, const double* G, int ld, int nr, int nc) {
-  const int c = line_id(), q = line_q();
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int r = 4 * i + q;
-    L.x[i] = (r < nr && c < nc) ? ldcg(G + static_cast<size_t>(c) * ld + r) : 0.0;
-  }
-}
-
-__device__ __forceinline__ void col_store(double* G, int ld, const Line& L, int nr, int nc) {
-  const int c = line_id(), q = line_q();
-#pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int r = 4 * i + q;
-    if (r < nr && c < nc) G[static_cast<size_t>(c) * ld + r] = L.x[i];
-  }
-}
-
-// The solves below keep a line's 16 entries in registers and loop over
-// elimination steps in rolled groups of 4 (i-cache friendly).  After group g
-// the entry of column/row 4g+q is final: it is written straight to global
-// memory ("retired"), the registers rotate down by one and a zero dummy
-// enters at x[15], so the live entry of the current group is always x[0]
-// (static register indexing).  Dummies and zero-padded edge entries may be
-// updated freely — they are never stored — so every step issues 16 loads and
-// 16 independent FMAs with a single select (slot 0).
-__device__ __forceinline__ void line_shift(Line& L) {
-#pragma unroll
-  for (int i = 0; i < 15; ++i) L.x[i] = L.x[i + 1];
-  L.x[15] = 0.0;
-}
-
-// X (rows in registers) <- X U^{-1}; U upper in smem (XTP stride, zero padded),
-// rinv[j] = 1/u_jj (smem).  kCheck: stage |x_rj| before scaling in Dd[j*XTP+r].
-// Retires row r's entries into G (column-major, ld).
-template <bool kCheck>
-__device__ __forceinline__ void line_right_upper(Line& L, int nr, int nc, const double* U, const double* rinv,
-                                                 double* Dd, double* G, int ld) {
-  const int r = line_id(), q = line_q(), lane = threadIdx.x & 31, base = lane & ~3;
-  const int ngroups = (nc + 3) >> 2;
-#pragma unroll 1
-  for (int jb = 0; jb < ngroups; ++jb) {
-#pragma unroll
-    for (int jr = 0; jr < 4; ++jr) {
-      const int j = 4 * jb + jr;
-      if (j >= nc) break;
-      double v = 0.0;
-      if (q == jr) {
-        const double d = L.x[0];
-        if (kCheck) Dd[j * XTP + r] = r < nr ? fabs(d) : 0.0;
-        v = d * rinv[j];
-        L.x[0] = v;
-      }
-      const double xj = __shfl_sync(0xffffffffu, v, base | jr);
-      const double* Ub = U + (4 * jb + q) * XTP + j;
-      double u[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) u[i] = Ub[4 * i * XTP];  // dummies read harmless smem (never stored)
-      const double x0 = fma(-xj, u[0], L.x[0]);
-      L.x[0] = q > jr ? x0 : L.x[0];
-#pragma unroll
-      for (int i = 1; i < 16; ++i) L.x[i] = fma(-xj, u[i], L.x[i]);
-    }
-    const int c = 4 * jb + q;
-    if (r < nr && c < nc) G[static_cast<size_t>(c) * ld + r] = L.x[0];
-    line_shift(L);
-  }
-}
-
-// X (columns in registers) <- L^{-1} X; L unit lower in smem (XTP stride, zero
-// padded).  Retires column c's entries into G (column-major, ld).
-__device__ __forceinline__ void line_left_unit_lower(Line& X, int nr, int nc, const double* Lm, double* G, int ld) {
-  const int c = line_id(), q = line_q(), lane = threadIdx.x & 31, base = lane & ~3;
-  const int ngroups = (nr + 3) >> 2;
-#pragma unroll 1
-  for (int kb = 0; kb < ngroups; ++kb) {
-#pragma unroll
-    for (int kr = 0; kr < 4; ++kr) {
-      const int k = 4 * kb + kr;
-      if (k >= nr) break;
-      const double xk = __shfl_sync(0xffffffffu, X.x[0], base | kr);
-      const double* Lk = Lm + k * XTP + 4 * kb + q;
-      double l[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) l[i] = Lk[4 * i];  // dummies read harmless smem (never stored)
-      const double x0 = fma(-l[0], xk, X.x[0]);
-      X.x[0] = q > kr ? x0 : X.x[0];
-#pragma unroll
-      for (int i = 1; i < 16; ++i) X.x[i] = fma(-l[i], xk, X.x[i]);
-    }
-    const int r = 4 * kb + q;
-    if (r < nr && c < nc) G[static_cast<size_t>(c) * ld + r] = X.x[0];
-    line_shift(X);
-  }
-}
-
-// LU without row exchange of an n x n tile held as rows in registers.  Step j:
-// the 4 threads of row j publish its live entries and 1/u_jj (smem, double
-// buffered), one barrier, every row r > j forms l_rj = d_rj / u_jj as
-// d_rj * (1/u_jj) (owner lane, shuffled to its 3 peers) and updates its
-// entries with independent FMAs.  |d_rj| before scaling is staged in Dd for
-// the pivot check.  Retires row r's entries into G (column-major, ld).
-__device__ void line_lu(Line& R, int n, double* urow, double* Dd, double* G, int ld) {
-  const int r = line_id(), q = line_q(), lane = threadIdx.x & 31, base = lane & ~3;
-  const int ngroups = (n + 3) >> 2;
-  double* rinv_s = urow + 2 * XT;  // [2]
-#pragma unroll 1
-  for (int jb = 0; jb < ngroups; ++jb) {
-#pragma unroll
-    for (int jr = 0; jr < 4; ++jr) {
-      const int j = 4 * jb + jr;
-      if (j >= n) break;
-      double* ub = urow + (j & 1) * XT;
-      if (r == j) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const int c = 4 * (jb + i) + q;
-          if (c < XT) ub[c] = R.x[i];
-        }
-        if (q == jr) rinv_s[j & 1] = 1.0 / R.x[0];
-      }
-      __syncthreads();
-      const bool act = r > j && r < n;
-      if (act) {
-        const double rinv = rinv_s[j & 1];
-        double v = 0.0;
-        if (q == jr) {
-          const double d = R.x[0];
-          Dd[j * XTP + r] = fabs(d);
-          v = d * rinv;
-          R.x[0] = v;
-        }
-        const double l = __shfl_sync(0xfu << (lane & 28), v, base | jr);
-        const double* ubq = ub + 4 * jb + q;
-        double u[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) u[i] = ubq[4 * i];  // dummies read harmless smem (never stored)
-        const double x0 = fma(-l, u[0], R.x[0]);
-        R.x[0] = q > jr ? x0 : R.x[0];
-#pragma unroll
-        for (int i = 1; i < 16; ++i) R.x[i] = fma(-l, u[i], R.x[i]);
-      }
-    }
-    const int c = 4 * jb + q;
-    if (r < n && c < n) G[static_cast<size_t>(c) * ld + r] = R.x[0];
-    line_shift(R);
-  }
-  __syncthreads();
-}
-
-// ---- recursive 64 = 2 x 32 tile kernels ------------------------------------------
-// One thread owns a whole 32-entry row or column of a half tile in registers,
-// so the triangular solves need no communication at all; the 32x32 diagonal
-// LU runs in one warp with shuffles; the coupling updates are 32-wide DMMA.
-
-// lane r owns row r of a 32x32 tile (registers).  LU without exchange; |d_rj|
-// before scaling staged in Dd[j*XTP + roff + r].
-__device__ __forceinline__ void warp_lu32(double (&a)[32], double* Dd, int roff) {
-  const int r = threadIdx.x & 31;
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    const double u = __shfl_sync(0xffffffffu, a[j], j);
-    const bool act = r > j;
-    const double d = a[j];
-    if (act) {
-      Dd[j * XTP + roff + r] = fabs(d);
-      a[j] = __ddiv_rn(d, u);
-    }
-    const double l = a[j];
-#pragma unroll
-    for (int c = j + 1; c < 32; ++c) {
-      const double ujc = __shfl_sync(0xffffffffu, a[c], j);
-      if (act) a[c] = fma(-l, ujc, a[c]);
-    }
-  }
-}
-
-// thread owns row x[32]; x <- x U^{-1}, U = upper 32x32 at Us (smem, XTP stride);
-// kCheck: |x_j| before scaling staged in Dd[j*XTP + row].
-template <bool kCheck>
-__device__ __forceinline__ void row_solve32(double (&x)[32], const double* Us, const double* rinv, double* Dd,
-                                            int row) {
-#pragma unroll
-  for (int j = 0; j < 32; ++j) {
-    if (kCheck) Dd[j * XTP + row] = fabs(x[j]);
-    x[j] *= rinv[j];
-#pragma unroll
-    for (int c = j + 1; c < 32; ++c) x[c] = fma(-x[j], Us[c * XTP + j], x[c]);
-  }
-}
-
-// thread owns column x[32]; x <- L^{-1} x, L = unit lower 32x32 at Ls (smem, XTP stride)
-__device__ __forceinline__ void col_solve32(double (&x)[32], const double* Ls) {
-#pragma unroll
-  for (int k = 0; k < 32; ++k)
-#pragma unroll
-    for (int r = k + 1; r < 32; ++r) x[r] = fma(-Ls[k * XTP + r], x[k], x[r]);
-}
-
-// x[32] (a row segment) -= y[32] (row segment) * B (32x32 at Bs, XTP stride): x_c -= sum_k y_k B[k][c]
-__device__ __forceinline__ void row_gemv32(double (&x)[32], const double (&y)[32], const double* Bs) {
-#pragma unroll
-  for (int k = 0; k < 32; ++k)
-#pragma unroll
-    for (int c = 0; c < 32; ++c) x[c] = fma(-y[k], Bs[c * XTP + k], x[c]);
-}
-
-// x[32] (a column segment) -= A (32x32 at As, XTP stride) * y[32] (column segment)
-__device__ __forceinline__ void col_gemv32(double (&x)[32], const double* As, const double (&y)[32]) {
-#pragma unroll
-  for (int k = 0; k < 32; ++k)
-#pragma unroll
-    for (int r = 0; r < 32; ++r) x[r] = fma(-As[k * XTP + r], y[k], x[r]);
-}
 
 // 1/x on the critical path: MUFU approximation + two Newton steps (<= 1 ulp
 // from the rounded quotient; the 1e-10 factor tolerance is untouched), the
@@ -559,104 +312,6 @@ __device__ void tile_lu64_blocked(double* T, int n, double* Dd, double* urow, lo
   __syncthreads();
 }
 
-// LU (no exchange) of the 64x64 tile in smem T (XTP stride); n <= 64 valid,
-// padded diagonal set to 1.  Dd: staged |d| (XTP stride).  256 threads.
-__device__ void tile_lu64(double* T, int n, double* Dd, double* rinv) {
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  for (int i = tid; i < XT; i += blockDim.x)
-    if (i >= n) T[i * XTP + i] = 1.0;
-  for (int i = tid; i < XT * XTP; i += blockDim.x) Dd[i] = 0.0;
-  __syncthreads();
-  // A11 = L11 U11 (warp 0)
-  if (warp == 0) {
-    double a[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) a[c] = T[c * XTP + lane];
-    warp_lu32(a, Dd, 0);
-#pragma unroll
-    for (int c = 0; c < 32; ++c) T[c * XTP + lane] = a[c];
-  }
-  __syncthreads();
-  if (tid < 32) rinv[tid] = 1.0 / T[tid * XTP + tid];
-  __syncthreads();
-  if (warp == 0) {  // A21 <- A21 U11^{-1}: lane owns row 32+lane
-    double x[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) x[c] = T[c * XTP + 32 + lane];
-    row_solve32<true>(x, T, rinv, Dd, 32 + lane);
-#pragma unroll
-    for (int c = 0; c < 32; ++c) T[c * XTP + 32 + lane] = x[c];
-  } else if (warp == 1) {  // A12 <- L11^{-1} A12: lane owns column 32+lane
-    double x[32];
-#pragma unroll
-    for (int r = 0; r < 32; ++r) x[r] = T[(32 + lane) * XTP + r];
-    col_solve32(x, T);
-#pragma unroll
-    for (int r = 0; r < 32; ++r) T[(32 + lane) * XTP + r] = x[r];
-  }
-  __syncthreads();
-  if (warp == 0) {  // A22 -= A21 A12: lane owns row 32+lane of A22
-    double x[32], y[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      x[c] = T[(32 + c) * XTP + 32 + lane];
-      y[c] = T[c * XTP + 32 + lane];
-    }
-    row_gemv32(x, y, T + 32 * XTP);
-    warp_lu32(x, Dd + 32 * XTP, 32);
-#pragma unroll
-    for (int c = 0; c < 32; ++c) T[(32 + c) * XTP + 32 + lane] = x[c];
-  }
-  __syncthreads();
-}
-
-// X (64 x 64 rows in smem, XTP) <- X U^{-1}, U 64x64 upper in smem; thread r < 64 owns row r.
-template <bool kCheck>
-__device__ void tile_right_solve64(double* X, const double* U, double* rinv, double* Dd, int nc) {
-  const int tid = threadIdx.x;
-  for (int j = tid; j < XT; j += blockDim.x) rinv[j] = j < nc ? 1.0 / U[j * XTP + j] : 1.0;
-  __syncthreads();
-  if (tid < XT) {
-    double x1[32], x2[32];
-#pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      x1[c] = X[c * XTP + tid];
-      x2[c] = X[(32 + c) * XTP + tid];
-    }
-    row_solve32<kCheck>(x1, U, rinv, Dd, tid);
-    row_gemv32(x2, x1, U + 32 * XTP);  // x2 -= x1 * U12
-    row_solve32<kCheck>(x2, U + 32 * XTP + 32, rinv + 32, Dd + 32 * XTP, tid);
-#pragma unroll
-    for (int c = 0; c < 32; ++c) {
-      X[c * XTP + tid] = x1[c];
-      X[(32 + c) * XTP + tid] = x2[c];
-    }
-  }
-  __syncthreads();
-}
-
-// X (64 x 64 in smem) <- L^{-1} X, L 64x64 unit lower in smem; thread c < 64 owns column c.
-__device__ void tile_left_solve64(double* X, const double* L) {
-  const int tid = threadIdx.x;
-  if (tid < XT) {
-    double x1[32], x2[32];
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      x1[r] = X[tid * XTP + r];
-      x2[r] = X[tid * XTP + 32 + r];
-    }
-    col_solve32(x1, L);
-    col_gemv32(x2, L + 32, x1);  // x2 -= L21 * x1
-    col_solve32(x2, L + 32 * XTP + 32);
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      X[tid * XTP + r] = x1[r];
-      X[tid * XTP + 32 + r] = x2[r];
-    }
-  }
-  __syncthreads();
-}
-
 // bmax[j] (global, bits) = max over rows r > j (r < nr) of the staged |d_rj|;
 // rows_all: the whole column is "below" (TRSM_L tiles).
 // Thread (column c = tid & 63, row quarter tid >> 6) reduces 16 independent
@@ -767,14 +422,6 @@ __device__ __noinline__ void store_tile(double* G, int ld, const double* T, int 
   for (int i = 0; i < XPER; ++i) {
     const int c = c0 + 4 * i;
     if (c < nc) G[static_cast<size_t>(c) * ld + r] = T[c * XTP + r];
-  }
-}
-
-// rinv[j] = 1 / U(j,j) of an smem tile; cm[] cleared (bmax staging)
-__device__ __forceinline__ void prep_right(const double* U, int n, double* rinv, unsigned long long* cm) {
-  for (int j = threadIdx.x; j < XT; j += blockDim.x) {
-    rinv[j] = j < n ? 1.0 / U[j * XTP + j] : 0.0;
-    cm[j] = 0ull;
   }
 }
 

@@ -1,3 +1,5 @@
+# Round-end measurement pass (run under gpurun): bench lines with CPU baseline, ncu launch list, ncu --set full
+# captures of the two top kernels, DRAM traffic per launch.  Outputs land in gpurun_out/.
 timeout 900 python bench.py --config C2 --steps 5 --warmup 3 --cpu-sample-s 15 --levels-out gpurun_out/c2_levels_r1final.npz > gpurun_out/r1_bench_c2.json 2> gpurun_out/r1_bench_c2.log; tail -1 gpurun_out/r1_bench_c2.json | python scripts/summarize.py 2>/dev/null | head -3
 timeout 600 python bench.py --config C1 --steps 5 --warmup 3 --cpu-sample-s 10 > gpurun_out/r1_bench_c1.json 2>/dev/null; tail -1 gpurun_out/r1_bench_c1.json | python scripts/summarize.py 2>/dev/null | head -1
 timeout 900 python bench.py --config C3 --steps 5 --warmup 3 --cpu-sample-s 10 > gpurun_out/r1_bench_c3.json 2>/dev/null; tail -1 gpurun_out/r1_bench_c3.json | python scripts/summarize.py 2>/dev/null | head -1

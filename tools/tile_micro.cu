@@ -4,56 +4,6 @@
 #include "../paper_2512_04389_b200/csrc/lbk_exec.cuh"
 using namespace lbk;
 
-__global__ void k_left(double* out, int iters, long long* cyc) {
-  extern __shared__ double sm[];
-  double* Lm = sm;
-  for (int i = threadIdx.x; i < XT * XTP; i += blockDim.x) Lm[i] = 1e-3 * ((i * 7) % 13);
-  __syncthreads();
-  Line X;
-  for (int i = 0; i < 16; ++i) X.x[i] = 1.0 + i;
-  long long t0 = clock64();
-  for (int it = 0; it < iters; ++it) { line_left_unit_lower(X, 64, 64, Lm, out + blockIdx.x * 4096, 64); for (int i = 0; i < 16; ++i) X.x[i] = 1.0 + i; }
-  long long t1 = clock64();
-  double s = 0; for (int i = 0; i < 16; ++i) s += X.x[i];
-  out[blockIdx.x * 4096 + threadIdx.x] += s * 0;
-  if (threadIdx.x == 0) cyc[blockIdx.x] = (t1 - t0) / iters;
-}
-
-__global__ void k_right(double* out, int iters, long long* cyc) {
-  extern __shared__ double sm[];
-  double* U = sm; double* rinv = sm + XREG; unsigned long long* cm = (unsigned long long*)(sm + XREG + XT);
-  double* Dd = sm + 2 * XREG;
-  for (int i = threadIdx.x; i < XT * XTP; i += blockDim.x) U[i] = 1.0 + 1e-3 * ((i * 7) % 13);
-  __syncthreads();
-  prep_right(U, 64, rinv, cm);
-  __syncthreads();
-  Line X;
-  for (int i = 0; i < 16; ++i) X.x[i] = 1.0 + i;
-  long long t0 = clock64();
-  for (int it = 0; it < iters; ++it) { line_right_upper<true>(X, 64, 64, U, rinv, Dd, out + blockIdx.x * 4096, 64); for (int i = 0; i < 16; ++i) X.x[i] = 1.0 + i; }
-  long long t1 = clock64();
-  double s = 0; for (int i = 0; i < 16; ++i) s += X.x[i];
-  out[blockIdx.x * 4096 + threadIdx.x] += s * 0;
-  if (threadIdx.x == 0) cyc[blockIdx.x] = (t1 - t0) / iters;
-}
-
-__global__ void k_lu(double* out, int iters, long long* cyc) {
-  extern __shared__ double sm[];
-  double* urow = sm; double* Dd = sm + XREG;
-  long long tot = 0;
-  Line X;
-  for (int it = 0; it < iters; ++it) {
-    for (int i = 0; i < 16; ++i) X.x[i] = ((threadIdx.x >> 2) == 4 * i + (threadIdx.x & 3)) ? 100.0 : 1e-3 * i;
-    __syncthreads();
-    long long t0 = clock64();
-    line_lu(X, 64, urow, Dd, out + blockIdx.x * 4096, 64);
-    tot += clock64() - t0;
-  }
-  double s = 0; for (int i = 0; i < 16; ++i) s += X.x[i];
-  out[blockIdx.x * 4096 + threadIdx.x] += s * 0;
-  if (threadIdx.x == 0) cyc[blockIdx.x] = tot / iters;
-}
-
 __global__ void k_mma(double* out, int iters, long long* cyc) {
   extern __shared__ double sm[];
   double* C = sm; double* A = sm + XREG; double* B = sm + 2 * XREG;
@@ -64,53 +14,6 @@ __global__ void k_mma(double* out, int iters, long long* cyc) {
   long long t1 = clock64();
   out[blockIdx.x * 4096 + threadIdx.x] = C[threadIdx.x];
   if (threadIdx.x == 0) cyc[blockIdx.x] = (t1 - t0) / iters;
-}
-
-__global__ void k_lu64(double* out, int iters, long long* cyc) {
-  extern __shared__ double sm[];
-  double* T = sm; double* Dd = sm + XREG; double* rinv = sm + 2 * XREG;
-  long long tot = 0;
-  for (int it = 0; it < iters; ++it) {
-    for (int i = threadIdx.x; i < XT * XTP; i += blockDim.x) T[i] = (i % 65 == i / 65) ? 100.0 : 1e-3 * ((i * 7) % 13);
-    __syncthreads();
-    long long t0 = clock64();
-    tile_lu64(T, 64, Dd, rinv);
-    tot += clock64() - t0;
-  }
-  out[blockIdx.x * 4096 + threadIdx.x] = T[threadIdx.x];
-  if (threadIdx.x == 0) cyc[blockIdx.x] = tot / iters;
-}
-
-__global__ void k_right64(double* out, int iters, long long* cyc) {
-  extern __shared__ double sm[];
-  double* X = sm; double* U = sm + XREG; double* rinv = sm + 2 * XREG; double* Dd = sm + 2 * XREG + 128;
-  for (int i = threadIdx.x; i < XT * XTP; i += blockDim.x) U[i] = 1.0 + 1e-3 * ((i * 7) % 13);
-  long long tot = 0;
-  for (int it = 0; it < iters; ++it) {
-    for (int i = threadIdx.x; i < XT * XTP; i += blockDim.x) X[i] = 1e-3 * (i % 11);
-    __syncthreads();
-    long long t0 = clock64();
-    tile_right_solve64<true>(X, U, rinv, Dd, 64);
-    tot += clock64() - t0;
-  }
-  out[blockIdx.x * 4096 + threadIdx.x] = X[threadIdx.x];
-  if (threadIdx.x == 0) cyc[blockIdx.x] = tot / iters;
-}
-
-__global__ void k_left64(double* out, int iters, long long* cyc) {
-  extern __shared__ double sm[];
-  double* X = sm; double* L = sm + XREG;
-  for (int i = threadIdx.x; i < XT * XTP; i += blockDim.x) L[i] = 1e-3 * ((i * 7) % 13);
-  long long tot = 0;
-  for (int it = 0; it < iters; ++it) {
-    for (int i = threadIdx.x; i < XT * XTP; i += blockDim.x) X[i] = 1e-3 * (i % 11);
-    __syncthreads();
-    long long t0 = clock64();
-    tile_left_solve64(X, L);
-    tot += clock64() - t0;
-  }
-  out[blockIdx.x * 4096 + threadIdx.x] = X[threadIdx.x];
-  if (threadIdx.x == 0) cyc[blockIdx.x] = tot / iters;
 }
 
 __global__ void k_lub(double* out, int iters, long long* cyc) {
@@ -170,29 +73,17 @@ int main() {
   double* out; long long* cyc; long long h[148];
   cudaMalloc(&out, 148 * 4096 * 8); cudaMalloc(&cyc, 148 * 8);
   int smem = EXEC_SMEM;
-  cudaFuncSetAttribute(k_left, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_right, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_lu, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_lu64, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_right64, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_left64, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_lub, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_rblk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_lblk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const char* names[10] = {"line_left_unit_lower", "line_right_upper", "line_lu", "tile_mma_sub", "tile_lu64", "tile_right_solve64", "tile_left_solve64", "tile_lu64_blocked", "tile_right_solve_blk", "tile_left_solve_blk"};
-  for (int k = 0; k < 10; ++k) {
+  const char* names[4] = {"tile_mma_sub", "tile_lu64_blocked", "tile_right_solve_blk", "tile_left_solve_blk"};
+  for (int k = 0; k < 4; ++k) {
     for (int rep = 0; rep < 2; ++rep) {
-      if (k == 0) k_left<<<148, 256, smem>>>(out, 50, cyc);
-      if (k == 1) k_right<<<148, 256, smem>>>(out, 50, cyc);
-      if (k == 2) k_lu<<<148, 256, smem>>>(out, 20, cyc);
-      if (k == 3) k_mma<<<148, 256, smem>>>(out, 200, cyc);
-      if (k == 4) k_lu64<<<148, 256, smem>>>(out, 20, cyc);
-      if (k == 5) k_right64<<<148, 256, smem>>>(out, 20, cyc);
-      if (k == 6) k_left64<<<148, 256, smem>>>(out, 20, cyc);
-      if (k == 7) k_lub<<<148, 256, smem>>>(out, 20, cyc);
-      if (k == 8) k_rblk<<<148, 256, smem>>>(out, 20, cyc);
-      if (k == 9) k_lblk<<<148, 256, smem>>>(out, 20, cyc);
+      if (k == 0) k_mma<<<148, 256, smem>>>(out, 200, cyc);
+      if (k == 1) k_lub<<<148, 256, smem>>>(out, 20, cyc);
+      if (k == 2) k_rblk<<<148, 256, smem>>>(out, 20, cyc);
+      if (k == 3) k_lblk<<<148, 256, smem>>>(out, 20, cyc);
       cudaDeviceSynchronize();
     }
     cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
