@@ -167,3 +167,21 @@ def test_host_library_exports_every_declared_symbol():
         dev = ctypes.CDLL(_native.DEV_LIB)
         for s in dev_syms:
             assert hasattr(dev, s), s
+
+
+def test_pool_positions_place_every_entry_of_a():
+    """grid.pool_positions (the refactorization input map): the pooled grid values
+    are exactly A's values at those positions and zero elsewhere (fill)."""
+    from paper_2512_04389_b200 import generators as G
+    from paper_2512_04389_b200.grid import pool_positions
+
+    for a in (G.poisson3d(8, "nd"), G.bbd(3000, 60, 10, seed=3)):
+        f = M.symbolic_factorize(M.symmetrize_pattern(a))
+        plan = M.irregular_plan(M.percentage_curve(M.diag_block_pointer(f)), a.n)
+        vals = M.partition(f, a, plan).pool.values
+        pmap = pool_positions(f, a, plan)
+        assert len(np.unique(pmap)) == a.nnz
+        assert np.array_equal(vals[pmap], a.values)
+        rest = np.ones(len(vals), bool)
+        rest[pmap] = False
+        assert not np.any(vals[rest])
