@@ -203,14 +203,24 @@ __device__ void tile_left_solve_blk(double* X, const double* Lm, int nr) {
     const int pe = pb + PB;
     if (pe >= nr) break;
     {
-      // row r = pe + (tid & 63): X[r, c] -= sum_k L[r, pb + k] X[pb + k, c]
-      const int r = pe + (tid & (XT - 1));
-      if (r < nr) {
-        double l[PB];
+      // X[r, c] -= sum_k L[r, pb + k] X[pb + k, c] for the R = nr - pe rows below
+      // the panel: work units (row, group of 4 columns) dealt over all 256
+      // threads (4 independent chains per unit)
+      const int R = nr - pe;
+#pragma unroll 1
+      for (int e = tid; e < R * (XT / 4); e += blockDim.x) {
+        const int r = pe + e % R, c0 = 4 * (e / R);
+        double a4[4];
 #pragma unroll
-        for (int k = 0; k < PB; ++k) l[k] = Lm[(pb + k) * XTP + r];
-        trail16(l, tid >> 6, XT, [&](int c) { return X + c * XTP + r; },
-                [&](int c) { return X + c * XTP + pb; });
+        for (int j = 0; j < 4; ++j) a4[j] = X[(c0 + j) * XTP + r];
+#pragma unroll
+        for (int k = 0; k < PB; ++k) {
+          const double l = Lm[(pb + k) * XTP + r];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) a4[j] = fma(-l, X[(c0 + j) * XTP + pb + k], a4[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) X[(c0 + j) * XTP + r] = a4[j];
       }
     }
     __syncthreads();
@@ -296,14 +306,24 @@ __device__ void tile_lu64_blocked(double* T, int n, double* Dd, double* urow, lo
     }
     __syncthreads();
     if (prof) { const long long t1 = clock64(); if (tid == 0) prof[1] += t1 - t0; t0 = t1; }
-    // (3) A22 -= L21 U12: thread owns row r = pe + (tid & 63) (if < n), columns pe + (tid >> 6) + 4q
+    // (3) A22 -= L21 U12: work units (row, group of 4 columns) dealt over all 256 threads
     {
-      const int r = pe + (tid & (XT - 1)), c0 = pe + (tid >> 6);
-      if (r < n) {
-        double l[PB];
+      const int R = n - pe, CG = (n - pe + 3) / 4;
+#pragma unroll 1
+      for (int e = tid; e < R * CG; e += blockDim.x) {
+        const int r = pe + e % R, c0 = pe + 4 * (e / R);
+        double a4[4];
 #pragma unroll
-        for (int k = 0; k < PB; ++k) l[k] = T[(pb + k) * XTP + r];
-        trail16(l, c0, n, [&](int c) { return T + c * XTP + r; }, [&](int c) { return T + c * XTP + pb; });
+        for (int j = 0; j < 4; ++j) a4[j] = c0 + j < n ? T[(c0 + j) * XTP + r] : 0.0;
+#pragma unroll
+        for (int k = 0; k < PB; ++k) {
+          const double l = T[(pb + k) * XTP + r];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) a4[j] = fma(-l, T[min(c0 + j, XT - 1) * XTP + pb + k], a4[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (c0 + j < n) T[(c0 + j) * XTP + r] = a4[j];
       }
     }
     __syncthreads();
