@@ -313,6 +313,7 @@ void drop_graphs(lbk_ctx* c) {
 }
 
 constexpr double RECT_SMALL = 64.0 * 64.0;
+constexpr size_t DEFER_MIN_TILES = 64;  // smaller deferred groups run with the level's critical SSSSM launch
 
 int choose_warps(int acc_len) { return std::max(1, std::min(4, MAX_SMEM / (acc_len * 8))); }
 
@@ -886,6 +887,12 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       L.acc_len = acc_len[lv];
       L.warps = choose_warps(L.acc_len);
       gall.insert(gall.end(), gen[lv].begin(), gen[lv].end());
+      if (gemD[lv].size() + gemE[lv].size() < DEFER_MIN_TILES) {  // not worth separate launches
+        gem[lv].insert(gem[lv].end(), gemD[lv].begin(), gemD[lv].end());
+        gem[lv].insert(gem[lv].end(), gemE[lv].begin(), gemE[lv].end());
+        gemD[lv].clear();
+        gemE[lv].clear();
+      }
       L.gemm_off = static_cast<int64_t>(mall.size());
       L.ngemm = static_cast<int32_t>(gem[lv].size());
       mall.insert(mall.end(), gem[lv].begin(), gem[lv].end());
@@ -1338,16 +1345,27 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
       }
     }
     const bool has_t = !exact && (use_exec ? L.nexec > 0 : L.ntcol > 0);
-    const bool br[NBRANCH] = {L.ngemm > 0, (!use_exec && L.npanel > 0) || (exact && L.nexact > 0), has_t};
+    // instrumented replays (evs) run the deferred SSSSM groups inside their own
+    // level, after its critical DMMA launch: every kernel family is then timed
+    // without the cross-level overlap (which only shares the GPU differently)
+    const bool inline_defer = evs != nullptr && (L.ngemmD || L.ngemmE);
+    const bool br[NBRANCH] = {L.ngemm > 0 || inline_defer, (!use_exec && L.npanel > 0) || (exact && L.nexact > 0),
+                              has_t};
     // instrumented replays: per level [end, gemm b/e, panel b/e, getrf b/e, csc b/e]
     auto rec = [&](int k, cudaStream_t s) {
-      if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 12 + k], s, cudaEventRecordExternal);
+      if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 13 + k], s, cudaEventRecordExternal);
     };
     if (br[0] || br[1] || br[2]) cudaEventRecord(c->fork, s0);
     if (br[0]) {
       cudaStreamWaitEvent(c->aux[0], c->fork, 0);
       rec(1, c->aux[0]);
-      gemm_map_kernel<<<L.ngemm, 256, GEMM_SMEM, c->aux[0]>>>(c->gitems.p + L.gemm_off, c->gtasks.p, P);
+      if (L.ngemm) gemm_map_kernel<<<L.ngemm, 256, GEMM_SMEM, c->aux[0]>>>(c->gitems.p + L.gemm_off, c->gtasks.p, P);
+      if (inline_defer) {
+        if (L.ngemmD)
+          gemm_map_kernel<<<L.ngemmD, 256, GEMM_SMEM, c->aux[0]>>>(c->gitems.p + L.gemmD_off, c->gtasks.p, P);
+        if (L.ngemmE)
+          gemm_map_kernel<<<L.ngemmE, 256, GEMM_SMEM, c->aux[0]>>>(c->gitems.p + L.gemmE_off, c->gtasks.p, P);
+      }
       rec(2, c->aux[0]);
       cudaEventRecord(c->join[0], c->aux[0]);
     }
@@ -1413,12 +1431,11 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
         cudaMemcpyAsync(stream_out + off, c->vout.p + off, len * sizeof(double), cudaMemcpyDeviceToHost, c->cstream);
       }
     }
-    if (L.ngemmD || L.ngemmE) {
+    if ((L.ngemmD || L.ngemmE) && !inline_defer) {
       // deferred SSSSM updates start once this level's critical work is done
       // and run (low stream priority) beside the next one (slack 2) or two
       // (slack >= 3) levels
       cudaEventRecord(c->dfork, s0);
-      if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 12 + 9], s0, cudaEventRecordExternal);
       for (int cls = 0; cls < 2; ++cls) {
         const int32_t nd = cls ? L.ngemmE : L.ngemmD;
         if (!nd) continue;
@@ -1429,7 +1446,6 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
           gemm_map_loop_kernel<<<std::min(nd, c->defer_ctas), 256, GEMM_SMEM, ds>>>(items, nd, c->gtasks.p, P);
         else
           gemm_map_kernel<<<nd, 256, GEMM_SMEM, ds>>>(items, c->gtasks.p, P);
-        if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 12 + 10 + cls], ds, cudaEventRecordExternal);
         cudaEvent_t ev = cls ? c->dev2[l] : c->dev[l];
         cudaEventRecord(ev, ds);
         pending.push_back({ev, L.tree_level + (cls ? 3 : 2)});
@@ -1591,7 +1607,7 @@ int factorize_host_impl(lbk_ctx* c, const double* a_values, bool a_is_pool, doub
   cudaPointerAttributes pa{};
   const bool pinned = cudaPointerGetAttributes(&pa, lu_values) == cudaSuccess && pa.type == cudaMemoryTypeHost;
   (void)cudaGetLastError();
-  if (pinned && nsegments(c) == 1) {
+  if (pinned && nsegments(c) == 1 && c->nnz >= (int64_t{1} << 24)) {
     // streamed output: every block's factor values are copied to the host while
     // later levels still run (one graph per output buffer)
     if (!c->sgraph || c->sgraph_out != lu_values || !same(c->s_tol, pivot_tol) || !same(c->s_eps, static_eps)) {
@@ -1893,7 +1909,7 @@ void lbk_host_free(void* ptr) {
 int lbk_level_times(lbk_ctx* c, double pivot_tol, double static_eps, float* out_ms, lbk_status* st) {
   LBK_CUDA(cudaSetDevice(c->device), st);
   const size_t nl = c->levels.size();
-  std::vector<cudaEvent_t> ev(1 + nl * 12);
+  std::vector<cudaEvent_t> ev(1 + nl * 13);
   for (auto& e : ev) LBK_CUDA(cudaEventCreate(&e), st);
   cudaGraph_t g;
   cudaGraphExec_t ge = nullptr;
@@ -1909,17 +1925,11 @@ int lbk_level_times(lbk_ctx* c, double pivot_tol, double static_eps, float* out_
   if (e == cudaSuccess)
     for (size_t l = 0; l < nl; ++l) {
       const Level& L = c->levels[l];
-      const size_t b = 1 + l * 12, prev = l ? 1 + (l - 1) * 12 : 0;
+      const size_t b = 1 + l * 13, prev = l ? 1 + (l - 1) * 13 : 0;
       float* o = out_ms + l * 5;
       for (int k = 0; k < 5; ++k) o[k] = 0.f;
       cudaEventElapsedTime(&o[0], ev[prev], ev[b]);
-      if (L.ngemm) cudaEventElapsedTime(&o[1], ev[b + 1], ev[b + 2]);
-      for (int cls = 0; cls < 2; ++cls)  // deferred DMMA SSSSM: counted with the family (overlaps the next levels)
-        if (cls ? L.ngemmE : L.ngemmD) {
-          float d = 0.f;
-          cudaEventElapsedTime(&d, ev[b + 9], ev[b + 10 + cls]);
-          o[1] += d;
-        }
+      if (L.ngemm || L.ngemmD || L.ngemmE) cudaEventElapsedTime(&o[1], ev[b + 1], ev[b + 2]);
       if (L.npanel || (exact && L.nexact)) cudaEventElapsedTime(&o[2], ev[b + 3], ev[b + 4]);
       if (!exact && L.ntcol) cudaEventElapsedTime(&o[3], ev[b + 5], ev[b + 6]);
       if (L.nitems) cudaEventElapsedTime(&o[4], ev[b + 7], ev[b + 8]);
