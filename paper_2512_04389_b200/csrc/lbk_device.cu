@@ -24,6 +24,8 @@
 #include <vector>
 
 #include "../../include/lbk.h"
+#include <map>
+
 #include "lbk_common.cuh"
 #include "lbk_dense.cuh"
 #include "lbk_exec.cuh"
@@ -88,7 +90,8 @@ struct Level {
   int32_t ntfin;
   int64_t exec_off, sptr_off, succ_off;  // persistent tile-DAG executor (tiled mode)
   int32_t nexec;
-  int32_t tree_level;  // ASAP level of the task DAG this launch level runs
+  int32_t tree_level;     // ASAP level of the task DAG this launch level runs
+  int32_t tree_level_hi;  // last tree level whose executor work runs in this launch (merged panel level)
 };
 
 constexpr int NBRANCH = 3;
@@ -124,8 +127,8 @@ struct ExecBuilder {
   // GEMMs feeding them overtake the bulk trailing updates of the current
   // step, which a plain step-major order would dequeue first.
   static int cost_of(int type) {
-    static const int c[14] = {150, 360, 180, 130, 64, 60, 130, 64, 180, 64, 100000, 420, 190, 240};
-    return type >= 0 && type < 14 ? c[type] : 64;
+    static const int c[15] = {150, 360, 180, 130, 64, 60, 130, 64, 180, 64, 100000, 420, 190, 240, 1};
+    return type >= 0 && type < 15 ? c[type] : 64;
   }
   void flush(Level* L, std::vector<XTask>* tasks, std::vector<int32_t>* sptr, std::vector<int32_t>* succ,
              std::vector<int32_t>* deps0) {
@@ -874,14 +877,27 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     std::vector<int32_t> xsucc_ptr, xsucc, xdeps0;
     c->levels.clear();
     c->subs.clear();
+    // A GETRF-only level followed by a panel-only level run in ONE executor
+    // launch: each panel tile waits only for the tile columns (GESSM) / rows
+    // (TSTRF) of the diagonal factor it reads, so the panel substitution
+    // chains trail the GETRF chain instead of starting after it.
+    auto only_exec = [&](int32_t l) {
+      return gen[l].empty() && gem[l].empty() && gemD[l].empty() && gemE[l].empty();
+    };
+    std::vector<char> merged_into_prev(nlevels, 0);
     for (int32_t lv = 0; lv < nlevels; ++lv) {
       if (gen[lv].empty() && gem[lv].empty() && gemD[lv].empty() && gemE[lv].empty() && pan[lv].empty() &&
           exa[lv].empty())
         continue;
+      const bool merge_next = c->use_exec && !all_full && lv + 1 < nlevels && only_exec(lv) && only_exec(lv + 1) &&
+                              !tgetrf[lv].empty() && ptask[lv].empty() && tgetrf[lv + 1].empty() &&
+                              !ptask[lv + 1].empty() &&
+                              (c->cut_after.empty() || !c->cut_after[lv]) && std::getenv("LBK_NO_MERGE") == nullptr;
       if (static_cast<int64_t>(acc_len[lv]) * 8 > MAX_SMEM || pan_smem[lv] > MAX_SMEM || exa_smem[lv] > MAX_SMEM)
         return fail(st, LBK_ERR_BAD_ARG, "block span too large for the shared-memory accumulator");
       Level L{};
       L.tree_level = lv;
+      L.tree_level_hi = merge_next ? lv + 1 : lv;
       L.item_off = static_cast<int64_t>(gall.size());
       L.nitems = static_cast<int32_t>(gen[lv].size());
       L.acc_len = acc_len[lv];
@@ -985,6 +1001,9 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       // ---- persistent tile-DAG executor work of this level (tiled mode) ----
       {
         ExecBuilder X;
+        // per diagonal block factored in this launch: tile-column (L part) and
+        // tile-row (U part) completion markers for merged panel work
+        std::map<int64_t, std::vector<int>> coldone, rowdone;
         for (size_t q = 0; q < tgetrf[lv].size(); ++q) {
           const int64_t b = tgetrf[lv][q];
           const int m = hb[b].nrows, nt = (m + XT - 1) / XT;
@@ -1001,6 +1020,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
                 bu = std::max(bu, col - r);
               }
             if (bl <= BAND_MAX && bu <= BAND_MAX && m <= 32767) {
+              std::vector<int> band_tasks;
               // independent segments: cut before column s when no entry couples
               // [.., s) with [s, ..) (block-diagonal bodies inside one block)
               std::vector<int> lo(m, m);  // lowest row/col index coupled to index x from the other side
@@ -1017,9 +1037,14 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
               for (int s1 = 1; s1 <= m; ++s1) {
                 const bool boundary = s1 == m || (sufmin[s1] >= s1 && s1 - s0 >= 64);
                 if (boundary) {
-                  X.add(X_BAND, b, s0, bl, bu, s1 - s0, stp, 0, {});
+                  band_tasks.push_back(X.add(X_BAND, b, s0, bl, bu, s1 - s0, stp, 0, {}));
                   s0 = s1;
                 }
+              }
+              if (merge_next) {
+                const int done = X.add(X_NOP, b, b, 0, 0, 0, stp, 0, band_tasks);
+                coldone[b].assign(nt, done);
+                rowdone[b].assign(nt, done);
               }
               continue;
             }
@@ -1047,16 +1072,20 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           // the critical chain
           std::vector<int> fused_deps;
           bool fused = false;
+          std::vector<std::vector<int>> colw(nt), roww(nt);  // writers of each tile column's L / row's U part
           for (int kb = 0; kb < nt; ++kb) {
             const int g = fused ? X.add(X_GETRF_UPD, b, b, kb, kb, kb - 1, stp, kb * 4, fused_deps)
                                 : X.add(X_GETRF, b, b, kb, kb, kb, stp, kb * 4, prev(kb, kb, {}));
             fused = false;
+            colw[kb].push_back(g);
+            roww[kb].push_back(g);
             L_(kb, kb) = g;
             fin_deps.push_back(g);
             for (int r = kb + 1; r < nt; ++r) {
               lt[r] = -1;
               if (!occ[q][static_cast<size_t>(kb) * nt + r]) continue;
               lt[r] = X.add(X_TRSM_L, b, b, r, kb, kb, stp, kb * 4 + 1, prev(r, kb, {g}));
+              colw[kb].push_back(lt[r]);
               L_(r, kb) = lt[r];
               fin_deps.push_back(lt[r]);
             }
@@ -1064,6 +1093,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
               ut[cc] = -1;
               if (!occ[q][static_cast<size_t>(cc) * nt + kb]) continue;
               ut[cc] = X.add(X_TRSM_U, b, b, kb, cc, kb, stp, kb * 4 + 1, prev(kb, cc, {g}));
+              roww[kb].push_back(ut[cc]);
               L_(kb, cc) = ut[cc];
             }
             for (int cc = kb + 1; cc < nt; ++cc) {
@@ -1081,8 +1111,24 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
             }
           }
           X.add(X_FINAL, b, b, 0, 0, 0, stp, 1 << 30, fin_deps);
+          if (merge_next) {  // chained markers: column t done implies columns < t done
+            coldone[b].assign(nt, -1);
+            rowdone[b].assign(nt, -1);
+            for (int t2 = 0; t2 < nt; ++t2) {
+              std::vector<int> dc = colw[t2], dr = roww[t2];
+              if (t2) {
+                dc.push_back(coldone[b][t2 - 1]);
+                dr.push_back(rowdone[b][t2 - 1]);
+              }
+              coldone[b][t2] = X.add(X_NOP, b, b, t2, 0, 0, stp, 0, dc);
+              rowdone[b][t2] = X.add(X_NOP, b, b, t2, 1, 0, stp, 0, dr);
+            }
+          }
         }
-        for (const auto& pt : ptask[lv]) {
+        const std::vector<std::array<int32_t, 4>> none;
+        const auto& ptasks_here = merge_next ? ptask[lv + 1] : merged_into_prev[lv] ? none : ptask[lv];
+        if (merge_next) merged_into_prev[lv + 1] = 1;
+        for (const auto& pt : ptasks_here) {
           const int32_t dblk = pt[1], xb = pt[2], stp = pt[3];
           const int tr = (hb[xb].nR + XT - 1) / XT, tc = (hb[xb].nC + XT - 1) / XT;
           std::vector<int> last(static_cast<size_t>(tr) * tc, -1);
@@ -1128,13 +1174,25 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           std::vector<std::vector<int>> pend_deps(static_cast<size_t>(tr) * tc);
           auto P_ = [&](int r, int cc) -> int& { return pend[static_cast<size_t>(cc) * tr + r]; };
           auto PD_ = [&](int r, int cc) -> std::vector<int>& { return pend_deps[static_cast<size_t>(cc) * tr + r]; };
+          // merged launch: a task whose factor tiles come from the panel's tile
+          // kt (rows R_kt for GESSM, columns C_kt for TSTRF) waits for the
+          // diagonal factor's columns / rows up to the last of them
+          const bool has_marks = merge_next && coldone.count(dblk);
+          const std::vector<int32_t> Rd = has_marks ? (pt[0] == 1 ? rows_of(xb) : cols_of(xb)) : std::vector<int32_t>();
+          auto mark = [&](int kt) -> int {
+            if (!has_marks) return -1;
+            const int idx = std::min(static_cast<int>(Rd.size()), (kt + 1) * XT) - 1;
+            const auto& v = pt[0] == 1 ? coldone[dblk] : rowdone[dblk];
+            return v[std::min(static_cast<int>(v.size()) - 1, Rd[idx] / XT)];
+          };
           if (pt[0] == 1) {  // GESSM: forward substitution down the row blocks
             for (int kb = 0; kb < tr; ++kb)
               for (int cc = 0; cc < tc; ++cc) {
                 if (!X_(kb, cc)) continue;
+                if (P_(kb, cc) >= 0) PD_(kb, cc).push_back(mark(kb));
                 const int d = P_(kb, cc) >= 0
                                   ? X.add(X_PG_FUSED, xb, dblk, kb, cc, P_(kb, cc), stp, kb * 4 + 1, PD_(kb, cc))
-                                  : X.add(X_PG_DIAG, xb, dblk, kb, cc, kb, stp, kb * 4 + 1, {L_(kb, cc)});
+                                  : X.add(X_PG_DIAG, xb, dblk, kb, cc, kb, stp, kb * 4 + 1, {L_(kb, cc), mark(kb)});
                 L_(kb, cc) = d;
                 for (int r = kb + 1; r < tr; ++r)
                   if (X_(r, cc) && D_(r, kb)) {  // L tile (r, kb)
@@ -1143,16 +1201,17 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
                       PD_(r, cc) = {d, L_(r, cc)};
                       continue;
                     }
-                    L_(r, cc) = X.add(X_PG_UPD, xb, dblk, r, cc, kb, stp, kb * 4 + 2, {d, L_(r, cc)});
+                    L_(r, cc) = X.add(X_PG_UPD, xb, dblk, r, cc, kb, stp, kb * 4 + 2, {d, L_(r, cc), mark(kb)});
                   }
               }
           } else {  // TSTRF: substitution along the column blocks
             for (int kb = 0; kb < tc; ++kb)
               for (int r = 0; r < tr; ++r) {
                 if (!X_(r, kb)) continue;
+                if (P_(r, kb) >= 0) PD_(r, kb).push_back(mark(kb));
                 const int d = P_(r, kb) >= 0
                                   ? X.add(X_PT_FUSED, xb, dblk, r, kb, P_(r, kb), stp, kb * 4 + 1, PD_(r, kb))
-                                  : X.add(X_PT_DIAG, xb, dblk, r, kb, kb, stp, kb * 4 + 1, {L_(r, kb)});
+                                  : X.add(X_PT_DIAG, xb, dblk, r, kb, kb, stp, kb * 4 + 1, {L_(r, kb), mark(kb)});
                 L_(r, kb) = d;
                 for (int cc = kb + 1; cc < tc; ++cc)
                   if (X_(r, cc) && D_(kb, cc)) {  // U tile (kb, cc)
@@ -1161,7 +1220,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
                       PD_(r, cc) = {d, L_(r, cc)};
                       continue;
                     }
-                    L_(r, cc) = X.add(X_PT_UPD, xb, dblk, r, cc, kb, stp, kb * 4 + 2, {d, L_(r, cc)});
+                    L_(r, cc) = X.add(X_PT_UPD, xb, dblk, r, cc, kb, stp, kb * 4 + 2, {d, L_(r, cc), mark(kb)});
                   }
               }
           }
@@ -1257,9 +1316,10 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     std::vector<std::vector<std::pair<int64_t, int64_t>>> per(c->levels.size());
     std::vector<int32_t> tl_to_l;
     for (size_t l = 0; l < c->levels.size(); ++l) {
-      const int32_t tl = c->levels[l].tree_level;
-      if (static_cast<int32_t>(tl_to_l.size()) <= tl) tl_to_l.resize(tl + 1, -1);
-      tl_to_l[tl] = static_cast<int32_t>(l);
+      const int32_t hi = c->levels[l].tree_level_hi;
+      if (static_cast<int32_t>(tl_to_l.size()) <= hi) tl_to_l.resize(hi + 1, -1);
+      for (int32_t tl = c->levels[l].tree_level; tl <= hi; ++tl)
+        if (tl_to_l[tl] < 0 || tl == c->levels[l].tree_level) tl_to_l[tl] = static_cast<int32_t>(l);
     }
     for (int64_t b = 0; b < nb; ++b) {
       const int32_t tl = c->blk_final_tl[b];
@@ -1337,7 +1397,7 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
   for (size_t l = lo; l < hi; ++l) {
     const Level& L = c->levels[l];
     for (size_t q = 0; q < pending.size();) {
-      if (pending[q].second <= L.tree_level) {
+      if (pending[q].second <= L.tree_level_hi) {
         cudaStreamWaitEvent(s0, pending[q].first, 0);
         pending.erase(pending.begin() + q);
       } else {

@@ -54,6 +54,7 @@ enum XType : int8_t {
   X_GETRF_UPD = 11,  // tile (r,r) -= tile(r,k) tile(k,r), then its LU (the diagonal chain, fused)
   X_PG_FUSED = 12,   // GESSM: X_PG_UPD from step k into tile (r,c), then X_PG_DIAG of (r,c)
   X_PT_FUSED = 13,   // TSTRF: X_PT_UPD from step k into tile (r,c), then X_PT_DIAG of (r,c)
+  X_NOP = 14,        // dependency marker (tile column / row of a diagonal factor complete)
 };
 
 struct XTask {
