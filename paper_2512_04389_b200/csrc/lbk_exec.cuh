@@ -32,6 +32,10 @@
 
 namespace lbk {
 
+#ifndef LBK_SPIN_NS
+#define LBK_SPIN_NS 32  // back-off of a CTA waiting on its task's dependency counter
+#endif
+
 constexpr int XT = 64;          // tile edge
 constexpr int XTP = XT + 1;     // padded smem column stride
 constexpr int XS = XT + 4;      // DMMA operand stride
@@ -760,7 +764,7 @@ __global__ void __launch_bounds__(256) exec_kernel(XLevel L, DevPools P, double 
       if (t < L.ntasks) {
         if (L.trace) L.trace[8 * t] = gtimer();
         volatile int* dp = L.deps + t;
-        while (*dp > 0) __nanosleep(32);
+        while (*dp > 0) __nanosleep(LBK_SPIN_NS);
         __threadfence();
         if (L.trace) L.trace[8 * t + 1] = gtimer();
       }
