@@ -499,7 +499,6 @@ __device__ void band_getrf(const BlockDev& A, const DevPools& P, double* sm, int
       Bs[idx] = (r >= 0 && r < m) ? ldcg(G + static_cast<size_t>(c) * ld + r) : 0.0;
     }
     __syncthreads();
-#pragma unroll 1
     if (bl * (bu + 1) <= 32) {
       // narrow band: the bl x (bu + 1) update pairs fit one warp (fixed lane ->
       // (i, j) map); steps only need a __syncwarp, the other warps wait

@@ -17,13 +17,13 @@ from oracle import structure as OS
 pytestmark = pytest.mark.gpu
 
 
-def banded(n, bl, bu, rng, diag_boost=4.0, zero_at=None, weak_at=None):
+def banded(n, bl, bu, rng, diag_boost=4.0, zero_at=None, weak_at=None, keep=0.7):
     rows, cols, vals = [], [], []
     for c in range(n):
         for r in range(max(0, c - bu), min(n, c + bl + 1)):
             if r == c:
                 continue
-            if rng.random() < 0.7:
+            if rng.random() < keep:
                 rows += [r, c]
                 cols += [c, r]
                 vals += [rng.uniform(-1, 1), rng.uniform(-1, 1)]
@@ -48,10 +48,14 @@ def run_both(a, positions):
     return g, t, og
 
 
-@pytest.mark.parametrize("bl,bu,n", [(1, 1, 700), (4, 4, 1000), (15, 15, 900), (3, 9, 600), (20, 20, 500)])
-def test_band_values_match_oracle(bl, bu, n):
+@pytest.mark.parametrize("bl,bu,n,keep", [(1, 1, 700, 0.7), (4, 4, 1000, 0.7), (15, 15, 900, 0.7), (3, 9, 600, 0.7),
+                                          (20, 20, 500, 0.7), (1, 1, 4000, 1.0), (2, 2, 3200, 1.0),
+                                          (3, 3, 5000, 1.0), (4, 4, 4500, 1.0)])
+def test_band_values_match_oracle(bl, bu, n, keep):
+    """keep=1.0: a full band (no independent segments), so blocks longer than one
+    shared-memory chunk of the register sweep (~1000-2600 columns) cross chunks."""
     rng = np.random.default_rng(bl * 100 + bu)
-    a = banded(n, max(bl, bu), max(bl, bu), rng)
+    a = banded(n, max(bl, bu), max(bl, bu), rng, keep=keep)
     positions = [0, n // 2, n]  # two banded diagonal blocks of > 128 rows
     g, t, og = run_both(a, positions)
     lu = M.factorize(g, t)
