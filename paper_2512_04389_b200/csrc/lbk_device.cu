@@ -90,6 +90,7 @@ struct Level {
   int32_t ntfin;
   int64_t exec_off, sptr_off, succ_off;  // persistent tile-DAG executor (tiled mode)
   int32_t nexec;
+  int32_t band4 = 0;      // holds band sweeps of half-bandwidth 4: exec_band_kernel
   int32_t tree_level;     // ASAP level of the task DAG this launch level runs
   int32_t tree_level_hi;  // last tree level whose executor work runs in this launch (merged panel level)
 };
@@ -154,6 +155,8 @@ struct ExecBuilder {
       for (int p : preds[i]) out[pos[p]].push_back(pos[i]);
     L->exec_off = static_cast<int64_t>(tasks->size());
     L->nexec = n;
+    L->band4 = 0;
+    for (int i = 0; i < n; ++i) L->band4 |= t[i].type == X_BAND && t[i].r == 4 && t[i].c == 4;
     L->sptr_off = static_cast<int64_t>(sptr->size());
     L->succ_off = static_cast<int64_t>(succ->size());
     int32_t acc = 0;
@@ -181,6 +184,7 @@ struct lbk_ctx {
   cudaStream_t dstream2 = nullptr;
   std::vector<int8_t> defer;          // per task: may run concurrently with the next level
   int exec_per_sm = 2;
+  int band_per_sm = 1;  // exec_band_kernel residency (register bound)
   int defer_ctas = 0;  // > 0: deferred SSSSM work on this many looping CTAs (LBK_DEFER_CTAS)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<cudaGraphExec_t> graphs;  // one per segment (see lbk_set_cuts)
@@ -362,6 +366,13 @@ int lbk_create(lbk_ctx** out, int device, lbk_status* st) {
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(tile_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TGEMM_SMEM);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, EXEC_SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(exec_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, EXEC_SMEM);
+  if (e == cudaSuccess) {
+    int nb = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, exec_band_kernel, 256, EXEC_SMEM);
+    c->band_per_sm = std::max(1, nb);
+  }
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(solve_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_SMEM);
   if (e == cudaSuccess)
@@ -1454,8 +1465,13 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
         X.head = c->xheads.p + l;
         X.ntasks = L.nexec;
         X.trace = (evs && c->xtrace.p) ? c->xtrace.p + 8 * L.exec_off : nullptr;
-        const int grid = std::max(1, std::min(L.nexec, 148 * c->exec_per_sm));
-        exec_kernel<<<grid, 256, EXEC_SMEM, s2>>>(X, P, pivot_tol);
+        if (L.band4) {
+          const int grid = std::max(1, std::min(L.nexec, 148 * std::min(c->exec_per_sm, c->band_per_sm)));
+          exec_band_kernel<<<grid, 256, EXEC_SMEM, s2>>>(X, P, pivot_tol);
+        } else {
+          const int grid = std::max(1, std::min(L.nexec, 148 * c->exec_per_sm));
+          exec_kernel<<<grid, 256, EXEC_SMEM, s2>>>(X, P, pivot_tol);
+        }
       } else {
         getrf_colmax_kernel<<<L.ntcol, 256, 0, s2>>>(c->titems.p + L.tcol_off, P);
         for (int k = 0; k < L.nsub; ++k) {

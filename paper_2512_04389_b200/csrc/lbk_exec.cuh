@@ -473,6 +473,125 @@ constexpr int BAND_CH = 128;
 
 static_assert(((BAND_CH + BAND_MAX) * (2 * BAND_MAX + 1) + 2 * BAND_CH * 16) * 8 <= EXEC_SMEM, "band smem");
 
+// Narrow symmetric bands (bl = bu = B <= 4), one thread: the whole 5x5 active window of the
+// elimination lives in that thread's registers (entry (r, c) in w[r % 5][c % 5],
+// so nothing moves when the window slides; the column loop is unrolled by 5).
+// Per column: one reciprocal, bl multipliers, a 4x4 fma update, the final U
+// row and L column out to shared memory and the entering row / column in.
+// The chain between columns is reciprocal -> multiply -> fma (no barrier, no
+// shuffle), and the rest of the column's work overlaps it.  Same arithmetic as
+// the barrier-stepped sweep below (l = d * rcp_fast(u), fma updates in column
+// order), so the factors are identical.  Chunks of the segment are staged
+// through shared memory by the whole CTA; the thread keeps its window across
+// chunks, so a chunk only needs its columns plus the 5 the window reaches past it.
+
+template <int B, int Q>
+__device__ __forceinline__ void band_reg_col(double (&w)[5][5], double* base, double* Sv, int Wm1, bool rin,
+                                             bool cin) {
+  // base = &Bs(kk, kk); (kk, kk + j) at base + j * Wm1; (kk + i, kk) at base + i
+  const double u = w[Q][Q];
+  const double rinv = rcp_fast(u);
+  base[0] = u;
+#pragma unroll
+  for (int j = 1; j <= B; ++j) base[j * Wm1] = w[Q][(Q + j) % 5];
+  double below = 0.0;
+#pragma unroll
+  for (int i = 1; i <= B; ++i) {
+    const double d = w[(Q + i) % 5][Q];
+    const double l = d * rinv;
+    below = fmax(below, fabs(d));
+    base[i] = l;
+#pragma unroll
+    for (int j = 1; j <= B; ++j) w[(Q + i) % 5][(Q + j) % 5] = fma(-l, w[Q][(Q + j) % 5], w[(Q + i) % 5][(Q + j) % 5]);
+  }
+  *Sv = below;
+  // entering row kk + 5 (columns kk + 1 .. kk + 5) and column kk + 5 (rows kk + 1 .. kk + 4)
+#pragma unroll
+  for (int j = 1; j < 5; ++j)
+    if (5 - j <= B) w[Q][(Q + j) % 5] = rin ? base[j * Wm1 + 5] : 0.0;
+  w[Q][Q] = cin ? base[5 * Wm1 + 5] : 0.0;
+#pragma unroll
+  for (int i = 1; i < 5; ++i)
+    if (5 - i <= B) w[(Q + i) % 5][Q] = cin ? base[5 * Wm1 + i] : 0.0;
+}
+
+template <int B>
+__device__ __noinline__ void band_getrf_reg(const BlockDev& A, const DevPools& P, double* sm, int s0, int m, int step,
+                                            double pivot_tol) {
+  constexpr int W = 2 * B + 1, Wm1 = W - 1;
+  const int ld = A.nrows, tid = threadIdx.x;
+  constexpr int SMEM_D = EXEC_SMEM / 8;
+  constexpr int CH = ((SMEM_D - 5 * W) / (W + 1)) / 5 * 5 < 1000 ? ((SMEM_D - 5 * W) / (W + 1)) / 5 * 5 : 1000;
+  double* G = P.vals + A.ent + static_cast<size_t>(s0) * ld + s0;
+  double* Bs = sm;                // (CH + 5) x W band values, (r, c) at (c - c0) * W + r - c + B
+  double* S = sm + (CH + 5) * W;  // CH staged max |d| below the diagonal
+  double* colmax = P.colmax + A.dg + s0;
+  double w[5][5];
+  for (int c0 = 0; c0 < m; c0 += CH) {
+    const int ce = min(m, c0 + CH + 5), kend = min(m, c0 + CH);
+    const int total = (ce - c0) * W;
+    __syncthreads();
+    for (int b = tid; b < total; b += 8 * XTHREADS) {  // all loads of a batch in flight at once
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int idx = b + u * XTHREADS, c = c0 + idx / W, r = c - B + idx % W;
+        v[u] = (idx < total && r >= 0 && r < m) ? ldcg(G + static_cast<size_t>(c) * ld + r) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (b + u * XTHREADS < total) Bs[b + u * XTHREADS] = v[u];
+    }
+    __syncthreads();
+    // column maxima of the columns whose band is still pristine in this chunk
+    // (the sweep stores final U rows into columns [kend, ce))
+    for (int c = (c0 == 0 ? 0 : c0 + 5) + tid; c < ce; c += blockDim.x) {
+      double mx = 0.0;
+#pragma unroll
+      for (int q = 0; q < W; ++q) {
+        const int r = c - B + q;
+        if (r >= 0 && r < m) mx = fmax(mx, fabs(Bs[(c - c0) * W + q]));
+      }
+      colmax[c] = mx;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (c0 == 0) {
+#pragma unroll
+        for (int r = 0; r < 5; ++r)
+#pragma unroll
+          for (int c = 0; c < 5; ++c)
+            w[r][c] = (c - r <= B && r - c <= B && r < m && c < ce) ? Bs[c * W + r - c + B] : 0.0;
+      }
+#pragma unroll 1
+      for (int k = c0; k < kend; k += 5) {
+        double* base = Bs + (k - c0) * W + B;
+        band_reg_col<B, 0>(w, base, S + k - c0, Wm1, k + 5 < m, k + 5 < ce);
+        if (k + 1 >= kend) break;
+        band_reg_col<B, 1>(w, base + W, S + k + 1 - c0, Wm1, k + 6 < m, k + 6 < ce);
+        if (k + 2 >= kend) break;
+        band_reg_col<B, 2>(w, base + 2 * W, S + k + 2 - c0, Wm1, k + 7 < m, k + 7 < ce);
+        if (k + 3 >= kend) break;
+        band_reg_col<B, 3>(w, base + 3 * W, S + k + 3 - c0, Wm1, k + 8 < m, k + 8 < ce);
+        if (k + 4 >= kend) break;
+        band_reg_col<B, 4>(w, base + 4 * W, S + k + 4 - c0, Wm1, k + 9 < m, k + 9 < ce);
+      }
+    }
+    __syncthreads();
+    for (int k = c0 + tid; k < kend; k += blockDim.x) {
+      const double uk = Bs[(k - c0) * W + B];
+      const double below = S[k - c0];
+      const double piv = fmax(fabs(uk), below);
+      if (piv == 0.0 || piv < pivot_tol * colmax[k] || isnan(uk)) record(&P.err[0], step, s0 + k);
+      else if (below > fabs(uk)) record(&P.err[1], step, s0 + k);
+    }
+    for (int idx = tid; idx < total; idx += blockDim.x) {
+      const int c = c0 + idx / W, r = c - B + idx % W;
+      if (r >= 0 && r < m) G[static_cast<size_t>(c) * ld + r] = Bs[idx];
+    }
+  }
+}
+
 // Segment [s0, s0 + m) of the block: independent of the rest of the block
 // (no band entry crosses its ends), so it is factored on its own.
 __device__ void band_getrf(const BlockDev& A, const DevPools& P, double* sm, int bl, int bu, int s0, int m, int step,
@@ -564,6 +683,7 @@ __device__ void band_getrf(const BlockDev& A, const DevPools& P, double* sm, int
   }
 }
 
+template <bool kBandReg>
 __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double pivot_tol,
                          unsigned long long* ph = nullptr) {
   double* T0 = sm;                  // target tile (XTP stride)
@@ -747,14 +867,20 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       break;
     }
     case X_BAND:
-      band_getrf(A, P, sm, tk.r, tk.c, tk.d, tk.k, tk.step, pivot_tol);
+      // (one instance only: more instances push the executor past 255 registers)
+      if (kBandReg && tk.r == 4 && tk.c == 4) band_getrf_reg<4>(A, P, sm, tk.d, tk.k, tk.step, pivot_tol);
+      else band_getrf(A, P, sm, tk.r, tk.c, tk.d, tk.k, tk.step, pivot_tol);
       break;
     default:
       break;
   }
 }
 
-__global__ void __launch_bounds__(256) exec_kernel(XLevel L, DevPools P, double pivot_tol) {
+// kBandReg: the launch holds band sweeps of half-bandwidth 4 (BBD bodies),
+// run by the register-window sweep; its registers (> 128) allow one CTA per SM,
+// so levels without such sweeps use the plain instance at two CTAs per SM.
+template <bool kBandReg>
+__device__ __forceinline__ void exec_body(const XLevel& L, const DevPools& P, double pivot_tol) {
   extern __shared__ double sm[];
   __shared__ int s_t;
   for (;;) {
@@ -773,7 +899,7 @@ __global__ void __launch_bounds__(256) exec_kernel(XLevel L, DevPools P, double 
     const int t = s_t;
     if (t >= L.ntasks) break;
     const XTask tk = L.tasks[t];
-    run_task(tk, P, sm, pivot_tol, L.trace ? L.trace + 8 * t + 3 : nullptr);
+    run_task<kBandReg>(tk, P, sm, pivot_tol, L.trace ? L.trace + 8 * t + 3 : nullptr);
     // every thread fences its own tile writes before the barrier, so the
     // successor releases after it are ordered behind all of them; the
     // releases are spread over the CTA (a GETRF tile has ~2x(tiles per
@@ -787,6 +913,14 @@ __global__ void __launch_bounds__(256) exec_kernel(XLevel L, DevPools P, double 
     }
     if (threadIdx.x == 0 && L.trace) L.trace[8 * t + 2] = gtimer();
   }
+}
+
+__global__ void __launch_bounds__(256) exec_kernel(XLevel L, DevPools P, double pivot_tol) {
+  exec_body<false>(L, P, pivot_tol);
+}
+
+__global__ void __launch_bounds__(256) exec_band_kernel(XLevel L, DevPools P, double pivot_tol) {
+  exec_body<true>(L, P, pivot_tol);
 }
 
 }  // namespace lbk

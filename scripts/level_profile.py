@@ -21,6 +21,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("cfg")
 ap.add_argument("--plan", default="irregular")
 ap.add_argument("--top", type=int, default=15)
+ap.add_argument("--range", default=None, help="also list levels lo:hi in order")
 args = ap.parse_args()
 strategy, bs = (args.plan, None) if ":" not in args.plan else ("regular", int(args.plan.split(":")[1]))
 a, f, g, t = bench.build_case(args.cfg, strategy, bs)
@@ -33,7 +34,10 @@ tr, info = eng.exec_trace()
 tr = tr.astype(np.int64)
 print(f"# {args.cfg} {args.plan}: graph {ms:.2f} ms; instrumented level sum {lt[:, 0].sum():.2f} ms "
       f"(dmma {lt[:, 1].sum():.2f} panel {lt[:, 2].sum():.2f} exec {lt[:, 3].sum():.2f} csc {lt[:, 4].sum():.2f})")
-order = np.argsort(-lt[:, 0])[: args.top]
+order = list(np.argsort(-lt[:, 0])[: args.top])
+if args.range:
+    lo, hi = (int(v) for v in args.range.split(":"))
+    order += list(range(lo, min(hi, len(lt))))
 for L in order:
     sel = info[:, 5] == L
     mix = {}
