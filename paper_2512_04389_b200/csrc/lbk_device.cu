@@ -185,6 +185,7 @@ struct lbk_ctx {
   std::vector<int8_t> defer;          // per task: may run concurrently with the next level
   int exec_per_sm = 2;
   int band_per_sm = 1;  // exec_band_kernel residency (register bound)
+  bool use_bandreg = true;  // LBK_NO_BANDREG: band levels on the plain executor (A/B experiments)
   int defer_ctas = 0;  // > 0: deferred SSSSM work on this many looping CTAs (LBK_DEFER_CTAS)
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   std::vector<cudaGraphExec_t> graphs;  // one per segment (see lbk_set_cuts)
@@ -393,6 +394,7 @@ int lbk_create(lbk_ctx** out, int device, lbk_status* st) {
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->cev, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->dfork, cudaEventDisableTiming);
   if (const char* x = std::getenv("LBK_EXEC_PER_SM")) c->exec_per_sm = std::max(1, std::atoi(x));
+  c->use_bandreg = std::getenv("LBK_NO_BANDREG") == nullptr;
   if (const char* x = std::getenv("LBK_DEFER_CTAS")) c->defer_ctas = std::max(0, std::atoi(x));
   if (e != cudaSuccess) {
     delete c;
@@ -1405,6 +1407,7 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
   // deferred SSSSM work of launch level l runs beside the next tree level; a
   // level at tree level T waits for the deferred work of tree levels <= T - 2
   std::vector<std::pair<cudaEvent_t, int32_t>> pending;  // (done event, first tree level that needs it)
+  int64_t pend_lv = -1, pend_bytes = 0;  // streamed output not yet flushed
   for (size_t l = lo; l < hi; ++l) {
     const Level& L = c->levels[l];
     for (size_t q = 0; q < pending.size();) {
@@ -1465,7 +1468,7 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
         X.head = c->xheads.p + l;
         X.ntasks = L.nexec;
         X.trace = (evs && c->xtrace.p) ? c->xtrace.p + 8 * L.exec_off : nullptr;
-        if (L.band4) {
+        if (L.band4 && c->use_bandreg) {
           const int grid = std::max(1, std::min(L.nexec, 148 * std::min(c->exec_per_sm, c->band_per_sm)));
           exec_band_kernel<<<grid, 256, EXEC_SMEM, s2>>>(X, P, pivot_tol);
         } else {
@@ -1495,16 +1498,35 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
     for (int k = 0; k < NBRANCH; ++k)
       if (br[k]) cudaStreamWaitEvent(s0, c->join[k], 0);
     if (stream_out && c->srange_off[l + 1] > c->srange_off[l]) {
-      // the blocks this level finished: gather + copy to the host on the copy stream
-      cudaEventRecord(c->lev[l], s0);
-      cudaStreamWaitEvent(c->cstream, c->lev[l], 0);
-      const int64_t r0 = c->srange_off[l], nr = c->srange_off[l + 1] - r0;
-      const int64_t p0 = c->spiece_off[l], np_ = c->spiece_off[l + 1] - p0;
-      range_gather_kernel<<<static_cast<int>(std::min<int64_t>(np_, 148 * 4)), 256, 0, c->cstream>>>(
-          c->vals.p, c->map.p, c->vout.p, c->sranges.p + 2 * p0, np_);
-      for (int64_t q = 0; q < nr; ++q) {
-        const int64_t off = c->hsranges[2 * (r0 + q)], len = c->hsranges[2 * (r0 + q) + 1];
-        cudaMemcpyAsync(stream_out + off, c->vout.p + off, len * sizeof(double), cudaMemcpyDeviceToHost, c->cstream);
+      // the blocks finished since the last flush: gather + copy to the host on
+      // the copy stream, batched over levels (>= 16 MB or 256 ranges, or the
+      // last level) with ranges less than 256 KB apart merged: one small copy
+      // per level and range would serialise the copy stream behind many
+      // launch-latency-bound nodes.  A merged gap re-sends values whose blocks
+      // are not final yet; their own (later, same-stream) copy overwrites them.
+      if (pend_lv < 0) pend_lv = static_cast<int64_t>(l);
+      for (int64_t q = c->srange_off[l]; q < c->srange_off[l + 1]; ++q) pend_bytes += c->hsranges[2 * q + 1] * 8;
+    }
+    if (stream_out && pend_lv >= 0) {
+      const int64_t pend_ranges = c->srange_off[l + 1] - c->srange_off[pend_lv];
+      if (pend_bytes >= (16ll << 20) || pend_ranges >= 256 || l + 1 == hi) {
+        cudaEventRecord(c->lev[l], s0);
+        cudaStreamWaitEvent(c->cstream, c->lev[l], 0);
+        const int64_t r0 = c->srange_off[pend_lv], nr = c->srange_off[l + 1] - r0;
+        const int64_t p0 = c->spiece_off[pend_lv], np_ = c->spiece_off[l + 1] - p0;
+        range_gather_kernel<<<static_cast<int>(std::min<int64_t>(np_, 148 * 4)), 256, 0, c->cstream>>>(
+            c->vals.p, c->map.p, c->vout.p, c->sranges.p + 2 * p0, np_);
+        std::vector<std::pair<int64_t, int64_t>> rs(nr);
+        for (int64_t q = 0; q < nr; ++q) rs[q] = {c->hsranges[2 * (r0 + q)], c->hsranges[2 * (r0 + q) + 1]};
+        std::sort(rs.begin(), rs.end());
+        for (size_t q = 0; q < rs.size();) {
+          int64_t off = rs[q].first, end = off + rs[q].second;
+          for (++q; q < rs.size() && rs[q].first - end <= (32 << 10); ++q) end = std::max(end, rs[q].first + rs[q].second);
+          cudaMemcpyAsync(stream_out + off, c->vout.p + off, (end - off) * sizeof(double), cudaMemcpyDeviceToHost,
+                          c->cstream);
+        }
+        pend_lv = -1;
+        pend_bytes = 0;
       }
     }
     if ((L.ngemmD || L.ngemmE) && !inline_defer) {

@@ -1,0 +1,10 @@
+# Band-sweep round pass (run under gpurun): GPU suite + smoke, C3/C5 bench lines with CPU baseline,
+# irregular-vs-regular balance on C5 and C3 (the paper's comparison), band task statistics.
+timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 300 python __graft_entry__.py smoke 2>&1 | tail -1
+timeout 900 python bench.py --config C3 --steps 5 --warmup 3 --cpu-sample-s 10 > gpurun_out/r1_bench_c3.json 2>/dev/null; tail -1 gpurun_out/r1_bench_c3.json | python scripts/summarize.py 2>/dev/null | head -1
+timeout 900 python bench.py --config C5 --steps 5 --warmup 3 --cpu-sample-s 10 > gpurun_out/r1_bench_c5.json 2>/dev/null; tail -1 gpurun_out/r1_bench_c5.json | python scripts/summarize.py 2>/dev/null | head -1
+timeout 900 python scripts/balance_bench.py C5 --out gpurun_out/r1_balance_c5.jsonl 2>&1 | grep "^#"
+timeout 1200 python scripts/balance_bench.py C3 --sizes 500,1000,2000,5000 --out gpurun_out/r1_balance_c3.jsonl 2>&1 | grep "^#"
+timeout 300 python scripts/band_stats.py C5 > gpurun_out/r1_band_stats_c5.txt 2>&1
+timeout 300 python scripts/band_stats.py C3 > gpurun_out/r1_band_stats_c3.txt 2>&1
