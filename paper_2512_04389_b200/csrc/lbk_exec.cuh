@@ -486,8 +486,7 @@ static_assert(((BAND_CH + BAND_MAX) * (2 * BAND_MAX + 1) + 2 * BAND_CH * 16) * 8
 // chunks, so a chunk only needs its columns plus the 5 the window reaches past it.
 
 template <int B, int Q>
-__device__ __forceinline__ void band_reg_col(double (&w)[5][5], double* base, double* Sv, int Wm1, bool rin,
-                                             bool cin) {
+__device__ __forceinline__ void band_reg_col(double (&w)[5][5], double* base, double* Sv, int Wm1) {
   // base = &Bs(kk, kk); (kk, kk + j) at base + j * Wm1; (kk + i, kk) at base + i
   const double u = w[Q][Q];
   const double rinv = rcp_fast(u);
@@ -499,20 +498,22 @@ __device__ __forceinline__ void band_reg_col(double (&w)[5][5], double* base, do
   for (int i = 1; i <= B; ++i) {
     const double d = w[(Q + i) % 5][Q];
     const double l = d * rinv;
-    below = fmax(below, fabs(d));
+    const double ad = fabs(d);
+    below = ad > below ? ad : below;  // = fmax (a NaN |d| is skipped), fewer instructions
     base[i] = l;
 #pragma unroll
     for (int j = 1; j <= B; ++j) w[(Q + i) % 5][(Q + j) % 5] = fma(-l, w[Q][(Q + j) % 5], w[(Q + i) % 5][(Q + j) % 5]);
   }
   *Sv = below;
-  // entering row kk + 5 (columns kk + 1 .. kk + 5) and column kk + 5 (rows kk + 1 .. kk + 4)
+  // entering row kk + 5 (columns kk + 1 .. kk + 5) and column kk + 5 (rows kk + 1 .. kk + 4);
+  // unpredicated: rows >= m and the columns past the staged chunk hold zeros
 #pragma unroll
   for (int j = 1; j < 5; ++j)
-    if (5 - j <= B) w[Q][(Q + j) % 5] = rin ? base[j * Wm1 + 5] : 0.0;
-  w[Q][Q] = cin ? base[5 * Wm1 + 5] : 0.0;
+    if (5 - j <= B) w[Q][(Q + j) % 5] = base[j * Wm1 + 5];
+  w[Q][Q] = base[5 * Wm1 + 5];
 #pragma unroll
   for (int i = 1; i < 5; ++i)
-    if (5 - i <= B) w[(Q + i) % 5][Q] = cin ? base[5 * Wm1 + i] : 0.0;
+    if (5 - i <= B) w[(Q + i) % 5][Q] = base[5 * Wm1 + i];
 }
 
 template <int B>
@@ -531,7 +532,8 @@ __device__ __noinline__ void band_getrf_reg(const BlockDev& A, const DevPools& P
     const int ce = min(m, c0 + CH + 5), kend = min(m, c0 + CH);
     const int total = (ce - c0) * W;
     __syncthreads();
-    for (int b = tid; b < total; b += 8 * XTHREADS) {  // all loads of a batch in flight at once
+    // all loads of a batch in flight at once; slots past the segment are zero-filled
+    for (int b = tid; b < (CH + 5) * W; b += 8 * XTHREADS) {
       double v[8];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
@@ -540,7 +542,7 @@ __device__ __noinline__ void band_getrf_reg(const BlockDev& A, const DevPools& P
       }
 #pragma unroll
       for (int u = 0; u < 8; ++u)
-        if (b + u * XTHREADS < total) Bs[b + u * XTHREADS] = v[u];
+        if (b + u * XTHREADS < (CH + 5) * W) Bs[b + u * XTHREADS] = v[u];
     }
     __syncthreads();
     // column maxima of the columns whose band is still pristine in this chunk
@@ -566,15 +568,15 @@ __device__ __noinline__ void band_getrf_reg(const BlockDev& A, const DevPools& P
 #pragma unroll 1
       for (int k = c0; k < kend; k += 5) {
         double* base = Bs + (k - c0) * W + B;
-        band_reg_col<B, 0>(w, base, S + k - c0, Wm1, k + 5 < m, k + 5 < ce);
+        band_reg_col<B, 0>(w, base, S + k - c0, Wm1);
         if (k + 1 >= kend) break;
-        band_reg_col<B, 1>(w, base + W, S + k + 1 - c0, Wm1, k + 6 < m, k + 6 < ce);
+        band_reg_col<B, 1>(w, base + W, S + k + 1 - c0, Wm1);
         if (k + 2 >= kend) break;
-        band_reg_col<B, 2>(w, base + 2 * W, S + k + 2 - c0, Wm1, k + 7 < m, k + 7 < ce);
+        band_reg_col<B, 2>(w, base + 2 * W, S + k + 2 - c0, Wm1);
         if (k + 3 >= kend) break;
-        band_reg_col<B, 3>(w, base + 3 * W, S + k + 3 - c0, Wm1, k + 8 < m, k + 8 < ce);
+        band_reg_col<B, 3>(w, base + 3 * W, S + k + 3 - c0, Wm1);
         if (k + 4 >= kend) break;
-        band_reg_col<B, 4>(w, base + 4 * W, S + k + 4 - c0, Wm1, k + 9 < m, k + 9 < ce);
+        band_reg_col<B, 4>(w, base + 4 * W, S + k + 4 - c0, Wm1);
       }
     }
     __syncthreads();
