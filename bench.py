@@ -168,11 +168,27 @@ def max_over_ranks(x: float, world: int) -> float:
     return float(t.item())
 
 
-def cpu_baseline_sample(g, t, flops_t, budget_s):
-    from oracle import cpu_baseline as CB
+def reference_cpu(config: str, run_budget_s: float, runs: int):
+    """The unmodified reference (baseline/_ref) timed to completion on the host cores.
 
-    r = CB.sample(g, t, flops_t, budget_s=budget_s)
-    return r, CB.host_cores(), CB.blas_threads(), CB.cpu_model()
+    oracle/ref_timing.py: ``lublock.factorize(grid, tree, workers=1)`` like cmd_factor
+    (cli.py:194-215) on the largest same-family instance whose predicted memory and
+    per-run time fit (SURVEY.md §8d guard).  ``runs`` further runs after the sizing run;
+    returns (cpu_baseline dict, list of per-run seconds, case).
+    """
+    from oracle import ref_timing as R
+
+    case, s0 = R.pick_case(config, run_budget_s, log=log)
+    secs = [case.factorize_seconds() for _ in range(runs)] if runs > 0 else [s0]
+    v = case.flops / statistics.median(secs) / 1e9
+    fam, full, _ = R.FAMILIES[config]
+    scope = ("the full configuration" if case.size == full else
+             f"the largest {fam} instance whose predicted run time fits {run_budget_s:.0f}s and whose predicted "
+             f"memory fits 0.8 x MemAvailable (full size {full} does not)")
+    cpu = {"value": v, "unit": "GFLOP/s", "cores": os.cpu_count(), "blas_threads": R.blas_threads(),
+           "cpu": R.cpu_model(), "kind": "reference",
+           "sample": f"{case.describe()}; median of {len(secs)} runs ({statistics.median(secs):.2f}s); {scope}"}
+    return cpu, secs, case
 
 
 def plan_arg(s: str):
@@ -185,32 +201,35 @@ def plan_arg(s: str):
 
 
 def run_reference(args):
-    world, rank, _ = dist_init("gloo")
-    if rank != 0:
+    """--impl reference: the reference's own CPU factorization, rank 0 only (others exit 0)."""
+    if int(os.environ.get("RANK", "0")) != 0:
         return 0
-    strategy, bs = plan_arg(args.plan)
-    a, f, g, t = build_case(args.config, strategy, bs)
-    from paper_2512_04389_b200.workmodel import task_work
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    # each step is one full reference factorization; size the instance so that the whole
+    # warmup + steps run ends within a few minutes
+    budget = min(max(args.ref_budget_s / max(args.steps + args.warmup, 1), 2.0), 120.0)
+    from oracle import ref_timing as R
 
-    flops_t, _ = task_work(g, t)
-    for _ in range(args.warmup):
-        cpu_baseline_sample(g, t, flops_t, min(args.cpu_sample_s, 2.0))
-    vals = []
-    info = None
-    for _ in range(args.steps):
-        info = cpu_baseline_sample(g, t, flops_t, args.cpu_sample_s)
-        vals.append(info[0]["value"])
-    r, cores, blas, model = info
-    v = statistics.median(vals)
-    sample = (f"oracle port of lublock.factorize (workers=1, numpy/OpenBLAS), serial construction-order prefix: "
-              f"{r['tasks']}/{r['total_tasks']} tasks, {r['flops'] / 1e9:.3f} GFLOP in {r['seconds']:.1f}s per step")
+    case, s0 = R.pick_case(args.config, budget, log=log)
+    for _ in range(max(args.warmup - 1, 0)):  # the sizing run above was the first warm-up
+        case.factorize_seconds()
+    secs = [case.factorize_seconds() for _ in range(args.steps)]
+    med = statistics.median(secs)
+    v = case.flops / med / 1e9
+    fam, full, _ = R.FAMILIES[args.config]
+    scope = ("the full configuration" if case.size == full else
+             f"largest same-family instance with predicted run <= {budget:.1f}s and memory <= 0.8 x MemAvailable; "
+             f"full size {full} is infeasible within the bench budget (C2: > 1,930 s and > 62 GB, SURVEY.md 8d)")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "plan": args.plan, "n": a.n, "nnz_filled": f.nnz_filled},
-            "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cores, "blas_threads": blas,
-                             "cpu": model, "kind": "port", "sample": sample},
-            "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * med, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "plan": args.plan, "instance": f"{fam} {case.size}", "n": case.n,
+                       "nnz_filled": case.nnz_filled, "gflop": case.flops / 1e9},
+            "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": os.cpu_count(),
+                             "blas_threads": R.blas_threads(), "cpu": R.cpu_model(), "kind": "reference",
+                             "sample": f"{case.describe()}; each step one full run; {scope}"},
+            "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "runs_s": secs}
     print(json.dumps(line), flush=True)
     return 0
 
@@ -222,7 +241,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="C2")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-sample-s", type=float, default=15.0)
+    ap.add_argument("--cpu-sample-s", type=float, default=30.0, help="per-run budget of the cpu_baseline leg")
+    ap.add_argument("--ref-budget-s", type=float, default=400.0,
+                    help="--impl reference: target seconds for all warmup + timed reference runs")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--levels-out", default=None, help="write per-level device times + work to this .npz")
@@ -421,12 +442,7 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        r, cores, blas, model = cpu_baseline_sample(g, t, flops_t, args.cpu_sample_s)
-        cpu = {"value": r["value"], "unit": "GFLOP/s", "cores": cores, "blas_threads": blas, "cpu": model,
-               "kind": "port",
-               "sample": f"oracle port of lublock.factorize (workers=1), serial construction-order prefix of "
-                         f"the same C-config task list: {r['tasks']}/{r['total_tasks']} tasks, "
-                         f"{r['flops'] / 1e9:.3f} GFLOP in {r['seconds']:.1f}s"}
+        cpu, _, _ = reference_cpu(args.config, args.cpu_sample_s, 0)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,

@@ -138,6 +138,58 @@ def factorize(grid, tree, pivot_tol=1e-12, static_pivot=None):
     return state, perms
 
 
+def factorize_prefix(grid, tree, max_step=None, budget_s=None, pivot_tol=1e-12):
+    """The serial execution of ``factorize`` restricted to the task-list prefix of steps
+    0..s (construction order puts every task of step i before any task of step i+1,
+    grid.py:223-378), densifying blocks on first touch.  Stops after step ``max_step``
+    or, with ``budget_s``, after the first step that ends past the budget.
+
+    Blocks (bi, bj) with min(bi, bj) <= s are FINAL after step s (their GETRF / GESSM /
+    TSTRF at step min(bi, bj) and every SSSSM into them, steps < min(bi, bj), are in the
+    prefix), so a full-size device factorization can be checked value by value on them.
+    No-swap inputs only (the row-swap quirk needs the whole dense scratch).
+    Returns (s, {(bi, bj): dense} of the final blocks).
+    """
+    import time
+
+    state = {}
+
+    def blk(key):
+        d = state.get(key)
+        if d is None:
+            d = dense(grid.blocks[key])
+            state[key] = d
+        return d
+
+    t0 = time.perf_counter()
+    nt = len(tree.kinds)
+    last = -1
+    t = 0
+    while t < nt:
+        step = int(tree.steps[t])
+        if max_step is not None and step > max_step:
+            break
+        if budget_s is not None and last >= 0 and time.perf_counter() - t0 > budget_s:
+            break
+        while t < nt and int(tree.steps[t]) == step:
+            kind, i, r, c = int(tree.kinds[t]), step, int(tree.rows[t]), int(tree.cols[t])
+            if kind == SSSSM:
+                if (r, c) in grid.blocks:
+                    blk((r, c))[...] -= blk((r, i)) @ blk((i, c))
+            elif kind == GESSM:
+                gessm(blk((i, i)), blk((i, c)))
+            elif kind == TSTRF:
+                tstrf(blk((r, i)), blk((i, i)))
+            else:
+                _, swapped = getrf(blk((i, i)), pivot_tol, None, i)
+                if swapped:
+                    raise ValueError("factorize_prefix: row swap in block %d (no-swap inputs only)" % i)
+            t += 1
+        last = step
+    final = {k: d for k, d in state.items() if min(k) <= last}
+    return last, final
+
+
 def to_block(d) -> Block:
     """Dense -> CSC dropping exact zeros (factorize.py:179-192)."""
     cols, rows = np.nonzero(d.T)

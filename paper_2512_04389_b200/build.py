@@ -6,6 +6,11 @@
                    so the .so only needs the driver on the GPU box.
 
 Outputs land in paper_2512_04389_b200/_lib (git-ignored, travels with gpurun).
+
+Checker only (never imported by the package): where /root/reference exists,
+the unmodified reference is pip-installed into baseline/_ref (git-ignored,
+travels with gpurun) for the CPU-reference timing (oracle/ref_timing.py) and
+the golden fixtures.
 """
 
 from __future__ import annotations
@@ -43,7 +48,25 @@ def _stale(out, srcs):
     return any(os.path.getmtime(s) > t for s in srcs)
 
 
+REF_SRC = "/root/reference/pkg"
+REF_DST = os.path.join(os.path.dirname(PKG), "baseline", "_ref")
+
+
+def install_reference(verbose: bool = False) -> None:
+    """pip install --no-index --target baseline/_ref of the read-only reference (built from a /tmp copy)."""
+    if not os.path.isdir(REF_SRC) or os.path.isdir(os.path.join(REF_DST, "lublock")):
+        return
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as tmp:
+        src = os.path.join(tmp, "pkg")
+        shutil.copytree(REF_SRC, src)
+        _run([sys.executable, "-m", "pip", "install", "--no-index", "--no-build-isolation", "--no-deps",
+              "--find-links", "/opt/wheelhouse", "--target", REF_DST, "-q", src], verbose)
+
+
 def build(verbose: bool = False, force: bool = False) -> None:
+    install_reference(verbose)
     os.makedirs(OUT, exist_ok=True)
     hdr = os.path.join(INC, "lbk.h")
     host_src = os.path.join(SRC, "lbk_host.cpp")

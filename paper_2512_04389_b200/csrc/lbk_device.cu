@@ -58,6 +58,9 @@ struct DevBuf {
     cudaError_t e = alloc(v.size());
     if (e != cudaSuccess) return e;
     if (!v.empty()) e = cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+    // a pageable cudaMemcpy may return before its DMA lands, and it is not ordered
+    // with the non-blocking engine streams: finish it before any kernel reads p
+    if (e == cudaSuccess && !v.empty()) e = cudaDeviceSynchronize();
     return e;
   }
 };
@@ -1295,7 +1298,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       if (T_bi[b] == T_bj[b])
         for (int r = 0; r < hb[b].nrows; ++r) idp[hb[b].dg + r] = r;
     LBK_CUDA(cudaMemcpy(c->perm.p, idp.data(), idp.size() * sizeof(int32_t), cudaMemcpyHostToDevice), st);
-    LBK_CUDA(c->perm0.upload(idp), st);
+    LBK_CUDA(c->perm0.upload(idp), st);  // (upload synchronizes the device: both copies have landed)
   } catch (const std::bad_alloc&) {
     return fail(st, LBK_ERR_OOM, "host allocation in lbk_plan");
   }
@@ -1672,6 +1675,7 @@ int lbk_bind_matrix(lbk_ctx* c, int64_t nnz_a, const int64_t* pool_pos, lbk_stat
     if (pool_pos[k] < 0 || pool_pos[k] >= c->nnz) return fail(st, LBK_ERR_DIM_MISMATCH, "pool position out of range");
   LBK_CUDA(c->amap.alloc(std::max<int64_t>(nnz_a, 1)), st);
   if (nnz_a) LBK_CUDA(cudaMemcpy(c->amap.p, pool_pos, nnz_a * sizeof(int64_t), cudaMemcpyHostToDevice), st);
+  LBK_CUDA(cudaDeviceSynchronize(), st);  // order the pageable copy before kernels on the engine streams
   LBK_CUDA(c->avals.alloc(std::max<int64_t>(nnz_a, 1)), st);
   c->nnz_a = nnz_a;
   ok(st);
@@ -1842,16 +1846,21 @@ int lbk_download(lbk_ctx* c, double* lu_values, int32_t* perms, lbk_status* st) 
 int lbk_download_work(lbk_ctx* c, double* work, int64_t* nwork, lbk_status* st) {
   LBK_CUDA(cudaSetDevice(c->device), st);
   if (nwork) *nwork = c->nnz_work;
-  if (work)
+  if (work) {
+    LBK_CUDA(cudaStreamSynchronize(c->stream), st);  // the legacy-stream copy does not wait for it
     LBK_CUDA(cudaMemcpy(work, c->vals.p, c->nnz_work * sizeof(double), cudaMemcpyDeviceToHost), st);
+  }
   ok(st);
   return 0;
 }
 
 int lbk_set_perms(lbk_ctx* c, const int32_t* perms, lbk_status* st) {
   LBK_CUDA(cudaSetDevice(c->device), st);
-  if (c->ndiag_rows)
+  if (c->ndiag_rows) {
+    LBK_CUDA(cudaStreamSynchronize(c->stream), st);
     LBK_CUDA(cudaMemcpy(c->perm.p, perms, c->ndiag_rows * sizeof(int32_t), cudaMemcpyHostToDevice), st);
+    LBK_CUDA(cudaDeviceSynchronize(), st);  // order the pageable copy before kernels on the engine streams
+  }
   ok(st);
   return 0;
 }

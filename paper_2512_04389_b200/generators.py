@@ -39,9 +39,14 @@ def _stencil_triplets(shape, diag):
     return n, np.concatenate(rows), np.concatenate(cols), np.concatenate(vals)
 
 
+def poisson2d_triplets(k: int = 64):
+    """(n, rows, cols, values) of ``poisson2d``."""
+    return _stencil_triplets((k, k), 4.0)
+
+
 def poisson2d(k: int = 64) -> CscMatrix:
     """C1: 5-point Laplacian on a k x k grid, Dirichlet; diag 4, neighbours -1; index r*k+c."""
-    n, r, c, v = _stencil_triplets((k, k), 4.0)
+    n, r, c, v = poisson2d_triplets(k)
     return csc_from_triplets(n, (r, c, v))
 
 
@@ -88,21 +93,35 @@ def permute_symmetric(a: CscMatrix, perm: np.ndarray) -> CscMatrix:
     return csc_from_triplets(a.n, (r, c, a.values.copy()))
 
 
-def poisson3d(k: int = 64, order: str = "nd", leaf: int = 8) -> CscMatrix:
-    """C2/C4: 7-point Laplacian on k^3 (diag 6, neighbours -1), ND-ordered by default."""
+def poisson3d_triplets(k: int = 64, order: str = "nd", leaf: int = 8):
+    """(n, rows, cols, values) of ``poisson3d`` before COO->CSC (also fed to the reference's own
+    ``csc_from_triplets`` by the CPU-reference timing, oracle/ref_timing.py)."""
     n, r, c, v = _stencil_triplets((k, k, k), 6.0)
     if order == "natural":
-        return csc_from_triplets(n, (r, c, v))
+        return n, r, c, v
     if order != "nd":
         raise ValueError(f"unknown order {order!r}")
     perm = nested_dissection_3d(k, leaf)
     inv = np.empty_like(perm)
     inv[perm] = np.arange(n, dtype=np.int64)
-    return csc_from_triplets(n, (inv[r], inv[c], v))
+    return n, inv[r], inv[c], v
+
+
+def poisson3d(k: int = 64, order: str = "nd", leaf: int = 8) -> CscMatrix:
+    """C2/C4: 7-point Laplacian on k^3 (diag 6, neighbours -1), ND-ordered by default."""
+    n, r, c, v = poisson3d_triplets(k, order, leaf)
+    return csc_from_triplets(n, (r, c, v))
 
 
 def bbd(n: int, border: int, blocks: int, *, seed: int = 0, band: int = 4, keep: float = 0.5,
         ports: int = 4, port_links: int = 8, border_density: float = 0.001) -> CscMatrix:
+    """CSC of ``bbd_triplets`` (same arguments)."""
+    return csc_from_triplets(n, bbd_triplets(n, border, blocks, seed=seed, band=band, keep=keep, ports=ports,
+                                             port_links=port_links, border_density=border_density))
+
+
+def bbd_triplets(n: int, border: int, blocks: int, *, seed: int = 0, band: int = 4, keep: float = 0.5,
+                 ports: int = 4, port_links: int = 8, border_density: float = 0.001):
     """C3/C5: bordered-block-diagonal 'circuit-like' matrix.
 
     Body: ``n-border`` rows cut into ``blocks`` contiguous diagonal blocks
@@ -158,7 +177,7 @@ def bbd(n: int, border: int, blocks: int, *, seed: int = 0, band: int = 4, keep:
     rows = np.concatenate([li, lj, np.arange(n)])
     cols = np.concatenate([lj, li, np.arange(n)])
     vals = np.concatenate([v_lower, v_upper, diag])
-    return csc_from_triplets(n, (rows, cols, vals))
+    return rows, cols, vals
 
 
 CONFIGS = {

@@ -262,6 +262,7 @@ class Engine:
     def upload(self, values=None):
         v = np.ascontiguousarray(self.pool.values if values is None else values, dtype=np.float64)
         st = _native.LbkStatus()
+        self.generation += 1  # replaces the resident values: factors of earlier runs are stale
         if self.lib.lbk_upload_values(self.ctx, P(v, f64p), C.byref(st)):
             _native.raise_status(st, "lbk_upload_values")
         self._resident = True
@@ -313,6 +314,7 @@ class Engine:
             self.upload()
         out = np.zeros((self.n_launch_levels, 5), np.float32)
         st = _native.LbkStatus()
+        self.generation += 1
         self.lib.lbk_level_times(self.ctx, pivot_tol, self._eps(static_pivot, self.grid.value_max),
                                  out.ctypes.data_as(C.POINTER(C.c_float)), C.byref(st))
         if check or st.code in (_native.LBK_ERR_CUDA, _native.LBK_ERR_OOM):
@@ -328,6 +330,8 @@ class Engine:
     def run_segment(self, seg: int, pivot_tol=DEFAULT_PIVOT_TOL, static_pivot=None) -> None:
         """Enqueue graph segment `seg` on the engine stream (asynchronous)."""
         st = _native.LbkStatus()
+        if seg == 0:
+            self.generation += 1
         if self.lib.lbk_run_segment(self.ctx, int(seg), pivot_tol, self._eps(static_pivot, self.grid.value_max),
                                     C.byref(st)):
             _native.raise_status(st, "lbk_run_segment")
@@ -380,6 +384,7 @@ class Engine:
             self.upload()
         n = C.c_int64()
         st = _native.LbkStatus()
+        self.generation += 1
         self.lib.lbk_exec_trace(self.ctx, pivot_tol, math.nan, None, None, C.byref(n), C.byref(st))
         tr = np.zeros((n.value, 8), np.uint64)
         info = np.zeros((n.value, 6), np.int32)
@@ -544,7 +549,11 @@ def build_factors_full(grid, pool: GridPool, work: np.ndarray, perms_pool: np.nd
 
 def engine_for(grid, tree, *, device: int = 0, dense: bool = False, chunk: int = DEFAULT_CHUNK,
                dense_threshold: float | None = DEFAULT_DENSE_THRESHOLD) -> Engine:
-    """Cached device plan of (grid, tree); dense=True uses full-rectangle blocks everywhere."""
+    """Cached device plan of (grid, tree); dense=True uses full-rectangle blocks everywhere.
+
+    One plan per (device, dense, chunk, dense_threshold) and grid: a call with a different
+    tree object closes the cached plan (frees its device memory) and replaces it, so
+    calling ``factorize(grid, dependency_levels(grid))`` in a loop does not grow memory."""
     cache = getattr(grid, "_lbk_engines", None)
     if cache is None:
         cache = {}
@@ -552,9 +561,13 @@ def engine_for(grid, tree, *, device: int = 0, dense: bool = False, chunk: int =
             grid._lbk_engines = cache
         except AttributeError:
             pass
-    key = (id(tree), device, dense, chunk, dense_threshold)
+    key = (device, dense, chunk, dense_threshold)
     eng = cache.get(key)
-    if eng is None or eng.tree is not tree:
+    if eng is not None and eng.tree is not tree:
+        eng.close()
+        eng = None
+    if eng is None:
+        cache.pop(key, None)
         eng = Engine(grid, tree, device=device, chunk=chunk, dense=dense, dense_threshold=dense_threshold)
         cache[key] = eng
     return eng

@@ -148,7 +148,8 @@ def factor_samples(fac, keys_l, keys_u, per_block=8):
             idx = np.unique(np.linspace(0, max(nz - 1, 0), min(per_block, nz)).astype(np.int64)) if nz else []
             for e in idx:
                 rows.append((bi, bj, int(e), float(b.values[e])))
-            sums.append((bi, bj, nz, float(np.abs(b.values).sum()), sha(b.col_ptr), sha(b.row_idx)))
+            sums.append((bi, bj, nz, float(np.abs(b.values).sum()), sha(b.col_ptr), sha(b.row_idx),
+                         float(np.dot(proj_weights(nz), b.values)), float(np.abs(b.values).max(initial=0.0))))
         out[tag + "_samples"] = rows
         out[tag + "_blocks"] = sums
     return out
@@ -171,18 +172,28 @@ def named_case(name, a, plan="irregular", bs=None, factor=True):
         rec["perm_global"] = sha(fac.perm_global())
         kl = sorted(fac.l_blocks, key=lambda k: (k[1], k[0]))
         ku = sorted(fac.u_blocks, key=lambda k: (k[1], k[0]))
-        s = factor_samples(fac, kl, ku, per_block=max(1, min(8, 20000 // max(1, len(kl)))))
+        per = 32 if name == "C5" else max(1, min(8, 20000 // max(1, len(kl))))
+        s = factor_samples(fac, kl, ku, per_block=per)
         for tag in ("L", "U"):
             arrays[tag + "_samples_key"] = np.array([r[:3] for r in s[tag + "_samples"]], np.int64)
             arrays[tag + "_samples_val"] = np.array([r[3] for r in s[tag + "_samples"]], np.float64)
             arrays[tag + "_blocks_key"] = np.array([r[:3] for r in s[tag + "_blocks"]], np.int64)
             arrays[tag + "_blocks_abssum"] = np.array([r[3] for r in s[tag + "_blocks"]], np.float64)
+            arrays[tag + "_blocks_proj"] = np.array([r[6] for r in s[tag + "_blocks"]], np.float64)
+            arrays[tag + "_blocks_absmax"] = np.array([r[7] for r in s[tag + "_blocks"]], np.float64)
             rec[tag + "_pattern_sha"] = sha(np.array([hash_pair(r[4], r[5]) for r in s[tag + "_blocks"]],
                                                      dtype=np.int64))
     np.savez_compressed(os.path.join(HERE, f"case_{name}.npz"), **arrays)
     print(f"   -> p={rec['p']} tasks={rec['tasks']} levels={rec['levels']} "
           f"factor={rec.get('factorize_s', 0):.2f}s res={rec.get('residual')}", flush=True)
     return rec
+
+
+def proj_weights(m: int) -> np.ndarray:
+    """Deterministic +-1 weights of a block's value projection (tests/golden: checksum of every value)."""
+    e = np.arange(m, dtype=np.uint64)
+    h = (e * np.uint64(0x9E3779B97F4A7C15)) >> np.uint64(40)
+    return np.where(h & np.uint64(1), 1.0, -1.0)
 
 
 def hash_pair(a: str, b: str) -> int:
@@ -246,6 +257,9 @@ def small_cases():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c2", action="store_true", help="also pin C2 structure (~5 min, ~35 GB RAM)")
+    ap.add_argument("--c3", action="store_true", help="pin C3 structure (reference symbolic on n=1e6)")
+    ap.add_argument("--c5", action="store_true", help="pin C5 structure + factor checksums (~22 GB scratch)")
+    ap.add_argument("--only", default=None, help="comma list of named cases to (re)make")
     ap.add_argument("--skip-small", action="store_true")
     args = ap.parse_args()
     with open(os.path.join(HERE, "spec.json"), "w") as fh:
@@ -268,6 +282,13 @@ def main():
     }
     if args.c2:
         todo["C2"] = (lambda: G.poisson3d(64, "nd"), "irregular", None, False)
+    if args.c3:
+        todo["C3"] = (lambda: G.bbd(1_000_000, 10_000, 1000, seed=0), "irregular", None, False)
+    if args.c5:
+        todo["C5"] = (lambda: G.bbd(200_000, 4_000, 200, seed=0), "irregular", None, True)
+    if args.only:
+        keep = set(args.only.split(","))
+        todo = {k: v for k, v in todo.items() if k in keep}
     for name, (mk, plan, bs, fac) in todo.items():
         a = mk()
         rec = named_case(name, a, plan, bs, fac)

@@ -203,3 +203,17 @@ def test_named_case_oracle(name):
         assert all(int(blocks[(int(bi), int(bj))].col_ptr[-1]) == int(nz) for bi, bj, nz in bk)
     res = numeric.residual(a, a.n, pos, lb, ub, perms)
     assert res <= max(1e-14, 10 * rec["residual"])
+
+
+def test_oracle_prefix_equals_full_run_on_final_blocks():
+    """factorize_prefix (used by the full-size GPU parity tests) == the full serial run, bit for bit,
+    on every block final after step s."""
+    a = to_csc(G.bbd(6000, 120, 12, seed=3))
+    (fcp, fri), pct, pos, g, t = S.pipeline(a)
+    state, _ = numeric.factorize(g, t)
+    for s_max in (0, g.p // 2, g.p - 1):
+        s, final = numeric.factorize_prefix(g, t, max_step=s_max)
+        assert s == s_max
+        assert set(final) == {k for k in state if min(k) <= s}
+        for k, d in final.items():
+            assert d.tobytes() == state[k].tobytes(), k
