@@ -191,6 +191,25 @@ def reference_cpu(config: str, run_budget_s: float, runs: int):
     return cpu, secs, case
 
 
+def spawn(n: int, backend: str | None) -> int:
+    """``bench.py --gpus N`` without a launcher: re-exec under torch.distributed.run, N ranks."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if have < n and backend != "gloo":
+        raise SystemExit(f"bench.py --gpus {n}: only {have} CUDA device(s) visible; the 2D block-cyclic run "
+                         f"needs one GPU per rank (use --dist-backend gloo to share one GPU in tests)")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1", "--nproc-per-node", str(n),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    log(f"[bench] spawning {n} ranks: {' '.join(cmd[2:])}")
+    return subprocess.call(cmd)
+
+
 def plan_arg(s: str):
     """'irregular' | 'selector' | 'regular:<block size>'."""
     if s.startswith("regular:"):
@@ -255,6 +274,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return spawn(args.gpus, args.dist_backend)
 
     world, rank, local = dist_init(args.dist_backend)
     import torch
@@ -272,25 +293,14 @@ def main():
     t0 = time.perf_counter()
     dt = None if args.dense_threshold < 0 else args.dense_threshold
     distributed = world > 1 and not args.replicas
-    dist_error = None
     if distributed:
         from paper_2512_04389_b200.parallel import DistEngine
 
-        try:
-            de = DistEngine(g, t, device=local, dense_threshold=dt)
-            de.upload()
-            de.run()  # one trial factorization: the exchange must work before we time it
-        except Exception as exc:  # reported in the JSON line; the job then runs replicas
-            dist_error = f"{type(exc).__name__}: {exc}"[:300]
-            log(f"[bench] distributed path failed on rank {rank}: {dist_error}")
-        flags = max_over_ranks(1.0 if dist_error else 0.0, world)
-        if flags > 0:
-            distributed = False
-            dist_error = dist_error or "failed on another rank"
-            try:
-                de.close()
-            except Exception:
-                pass
+        de = DistEngine(g, t, device=local, dense_threshold=dt)
+        de.upload()
+        _, st0 = de.run()  # one trial factorization: the exchange must work before we time it
+        if st0.code:
+            raise SystemExit(f"[bench] rank {rank}: distributed trial factorization failed: code {st0.code}")
     if distributed:
         eng = de.eng
 
@@ -453,9 +463,7 @@ def main():
                        else args.config, "plan": args.plan, "n": a.n, "nnz_A": a.nnz, "nnz_filled": f.nnz_filled,
                        "p": g.p, "tasks": t.task_count, "levels": t.n_levels, "gflop": total_flops / 1e9,
                        "parallelism": (f"2d-block-cyclic {de.pg.pr}x{de.pg.pc} (NCCL p2p)" if distributed
-                                       else (f"replicas{world}" + (f" (2d-block-cyclic failed: {dist_error})"
-                                                                   if dist_error else ""))
-                                       if world > 1 else "single"),
+                                       else f"replicas{world}" if world > 1 else "single"),
                        "l2": "inputs (factor values, %.2f GB) larger than L2; values restored by a device copy "
                              "before every step" % (8 * eng.nnz / 1e9)},
             "e2e": {"value": e2e_value, "unit": "GFLOP/s", "seconds_per_step": e2e_s,

@@ -209,6 +209,7 @@ struct lbk_ctx {
   DevBuf<int64_t> map;
   DevBuf<double> vals, vin, vout, colmax;
   DevBuf<unsigned long long> bmax, err;
+  DevBuf<int> dirty;  // [0]: working pool needs zeroing before the next run; [1]: non-finite input seen
   DevBuf<Item> items;
   DevBuf<GemmTask> gtasks;
   DevBuf<GemmItem> gitems;
@@ -1292,6 +1293,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     LBK_CUDA(c->vin.alloc(nnz), st);
     LBK_CUDA(c->vout.alloc(nnz), st);
     LBK_CUDA(c->err.alloc(2), st);
+    LBK_CUDA(c->dirty.upload(std::vector<int>{1, 0}), st);
     // identity permutations until a GETRF writes them
     std::vector<int32_t> idp(ndiag);
     for (int64_t b = 0; b < nb; ++b)
@@ -1393,9 +1395,18 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
   const bool exact = (c->flags & 2) != 0 || !std::isnan(static_eps);
   const bool use_exec = !exact && c->use_exec;
   if (first) {
-  cudaMemsetAsync(c->err.p, 0xff, 2 * sizeof(unsigned long long), s0);
-    cudaMemsetAsync(c->vals.p, 0, c->nnz_work * sizeof(double), s0);
-    scatter_kernel<<<148 * 8, 256, 0, s0>>>(c->vin.p, c->map.p, c->vals.p, c->nnz);
+    cudaMemsetAsync(c->err.p, 0xff, 2 * sizeof(unsigned long long), s0);
+    if (exact || c->seg_begin.size() > 2) {
+      cudaMemsetAsync(c->vals.p, 0, c->nnz_work * sizeof(double), s0);
+    } else {
+      // Outside the filled pattern the working pool stays exactly zero (the pattern
+      // is elimination-closed, grid.py:3-5: every product landing there is an exact
+      // zero) and the scatter rewrites every in-pattern entry, so the pool is only
+      // zeroed after a run that may have left non-zeros there (an error, non-finite
+      // input: 0 * inf) or at the first run.
+      zero_if_dirty_kernel<<<148 * 8, 256, 0, s0>>>(c->vals.p, c->nnz_work, c->dirty.p);
+    }
+    scatter_kernel<<<148 * 8, 256, 0, s0>>>(c->vin.p, c->map.p, c->vals.p, c->nnz, c->dirty.p + 1);
   if (use_exec && c->n_exec) {
     cudaMemcpyAsync(c->xdeps.p, c->xdeps0.p, c->n_exec * sizeof(int), cudaMemcpyDeviceToDevice, s0);
     cudaMemsetAsync(c->xheads.p, 0, c->levels.size() * sizeof(int), s0);
@@ -1555,6 +1566,7 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
     rec(0, s0);
   }
   for (const auto& pq : pending) cudaStreamWaitEvent(s0, pq.first, 0);
+  if (last) mark_dirty_kernel<<<1, 32, 0, s0>>>(c->err.p, c->dirty.p);
   if (stream_out) {
     cudaEventRecord(c->cev, c->cstream);
     cudaStreamWaitEvent(s0, c->cev, 0);

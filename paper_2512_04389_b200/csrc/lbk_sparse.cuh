@@ -245,11 +245,38 @@ __global__ void __launch_bounds__(256) level_kernel(const Item* __restrict__ ite
 
 // I/O between the reference layout (pool order of the filled pattern) and
 // the working layout: work[map[e]] = in[e] / out[e] = work[map[e]].
+// nonfinite: set when an input value is inf / NaN (its products may reach
+// positions outside the pattern: the pool is then zeroed before the next run).
 __global__ void scatter_kernel(const double* __restrict__ in, const int64_t* __restrict__ map,
-                               double* __restrict__ work, int64_t n) {
+                               double* __restrict__ work, int64_t n, int* nonfinite) {
+  bool bad = false;
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double v = in[e];
+    bad |= !isfinite(v);
+    work[map[e]] = v;
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *nonfinite = 1;
+}
+
+// work[0, n) = 0 when dirty[0] is set (grid-stride, 16-byte stores); a no-op launch otherwise
+__global__ void zero_if_dirty_kernel(double* __restrict__ work, int64_t n, const int* dirty) {
+  if (*reinterpret_cast<const volatile int*>(dirty) == 0) return;
+  const int64_t n2 = n / 2;
+  double2* w2 = reinterpret_cast<double2*>(work);  // cudaMalloc'd: 256-byte aligned
+  for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n2;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    work[map[e]] = in[e];
+    w2[e] = make_double2(0.0, 0.0);
+  if ((n & 1) && blockIdx.x == 0 && threadIdx.x == 0) work[n - 1] = 0.0;
+}
+
+// end of a run: the next run zeroes the pool iff this one recorded an error
+// (err words start at ~0) or read a non-finite input
+__global__ void mark_dirty_kernel(const unsigned long long* err, int* dirty) {
+  if (threadIdx.x == 0) {
+    dirty[0] = (err[0] != ~0ULL || err[1] != ~0ULL || dirty[1] != 0) ? 1 : 0;
+    dirty[1] = 0;
+  }
 }
 
 // ranges[2 x n] = (offset, length) of reference-pool entries to gather (one CTA

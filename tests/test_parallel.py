@@ -139,3 +139,19 @@ def test_gloo_distributed_factors_bitwise_equal(tmp_path, world, mat, bs):
     assert set(got) == set(ref)
     for k in ref:
         assert got[k].tobytes() == ref[k].tobytes(), k
+
+
+def test_bench_gpus_n_fails_loudly_without_enough_gpus():
+    """bench.py --gpus N spawns N ranks itself; with fewer visible GPUs it exits non-zero and says why."""
+    import subprocess
+    import sys
+
+    import torch
+
+    if torch.cuda.is_available() and torch.cuda.device_count() >= 2:
+        pytest.skip("enough GPUs to spawn")
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--gpus", "2", "--steps", "1",
+                        "--warmup", "3"], capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "needs one GPU per rank" in r.stderr
