@@ -75,7 +75,8 @@ int lbk_partition_count(int64_t n, const int64_t* f_col_ptr, const int64_t* f_ro
 int lbk_partition_fill(int64_t n, const int64_t* f_col_ptr, const int64_t* f_row_idx,
                        const int64_t* a_col_ptr, const int64_t* a_row_idx, const double* a_values,
                        int64_t p, const int64_t* positions, int64_t nblocks, int64_t* table,
-                       int64_t* col_ptr, int64_t* row_idx, double* values, int64_t* block_nnz);
+                       int64_t* col_ptr, int64_t* row_idx, double* values, int64_t* block_nnz,
+                       int64_t* a_pos /* nullable: int64[nnz(A)], pool position of each entry of A */);
 
 /* dependency_levels(grid) -> DependencyTree            grid.py:223-378 */
 int lbk_levels_run(int64_t p, int64_t nblocks, const int64_t* table, const int64_t* col_ptr,
@@ -139,6 +140,22 @@ int lbk_factorize_host(lbk_ctx* ctx, const double* a_values, double* lu_values, 
 int lbk_bind_matrix(lbk_ctx* ctx, int64_t nnz_a, const int64_t* pool_pos, lbk_status* st);
 int lbk_refactor_host(lbk_ctx* ctx, const double* a_values, double* lu_values, int32_t* perms, double pivot_tol,
                       double static_eps, lbk_status* st);
+
+/* Output layout of the drop-in factorize() (paper_2512_04389_b200/numeric.py):
+ * the LUFactors blocks exactly as the reference exports them
+ * (pkg/src/lublock/factorize.py:370-384: off-diagonal blocks as stored,
+ * diagonal blocks split into triu(d) and tril(d,-1)+I).  nout output entries,
+ * block b (pool order) in [xoff[b], xoff[b+1]); xref[x] = reference-pool
+ * entry of output entry x, or -1 for a constant 1.0 (unit diagonal).  Every
+ * later lbk_factorize_host / lbk_refactor_host / lbk_download writes this
+ * layout (nout entries, lbk_num_out). */
+int lbk_set_export(lbk_ctx* ctx, int64_t nout, const int64_t* xref, const int64_t* xoff, lbk_status* st);
+int64_t lbk_num_out(lbk_ctx* ctx);
+
+/* Exact zeros per block (int64[nblocks]) in the last factorization's output:
+ * the reference's export drops exact zeros (factorize.py:179-192); a caller
+ * compacts only the blocks that have any. */
+int lbk_export_zero_counts(lbk_ctx* ctx, int64_t* counts, lbk_status* st);
 
 /* Copy the last factorization's values / perms to the host. */
 int lbk_download(lbk_ctx* ctx, double* lu_values, int32_t* perms, lbk_status* st);

@@ -70,7 +70,7 @@ def host_lib():
         _declare(lib, "lbk_partition_count", C.c_int, [i64, c_i64p, c_i64p, i64, c_i64p, c_i64p, c_i64p])
         _declare(lib, "lbk_partition_fill", C.c_int,
                  [i64, c_i64p, c_i64p, c_i64p, c_i64p, c_f64p, i64, c_i64p, i64, c_i64p, c_i64p, c_i64p,
-                  c_f64p, c_i64p])
+                  c_f64p, c_i64p, c_i64p])
         _declare(lib, "lbk_levels_run", C.c_int,
                  [i64, i64, c_i64p, c_i64p, c_i64p, c_vpp, c_i64p, c_i64p])
         _declare(lib, "lbk_levels_fetch", C.c_int,

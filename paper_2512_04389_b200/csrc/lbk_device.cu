@@ -235,12 +235,24 @@ struct lbk_ctx {
   std::vector<int32_t> blk_final_tl;  // tree level of the task that finishes each block
 
   std::vector<int64_t> ref_off, ref_len;  // reference pool range of each block
+  // output layout (lbk_set_export): entries nout, per-block range, omap[x] = working
+  // position of output entry x (-1: a constant 1.0, the unit diagonal of L)
+  int64_t nout = 0;
+  std::vector<int64_t> out_off, out_len;
+  DevBuf<int64_t> omap, zcount, out_off_d;
   cudaStream_t cstream = nullptr;
   cudaEvent_t cev = nullptr;
   std::vector<cudaEvent_t> lev;     // per launch level: critical work done (copy-stream fork)
-  cudaGraphExec_t sgraph = nullptr;
-  double* sgraph_out = nullptr;
-  double s_tol = NAN, s_eps = NAN;
+  // streamed-output graphs, one per host output buffer (two slots: a caller
+  // alternating between two buffers - the previous factors still alive - does
+  // not recapture)
+  struct SGraph {
+    cudaGraphExec_t g = nullptr;
+    double* out = nullptr;
+    double tol = NAN, eps = NAN;
+    uint64_t used = 0;
+  } sg[2];
+  uint64_t sg_clock = 0;
   DevBuf<int64_t> sranges;          // (offset, length) pairs, grouped by launch level
   std::vector<int64_t> hsranges;
   std::vector<int64_t> spiece_off;  // per launch level: first gather piece (+ sentinel)
@@ -316,6 +328,16 @@ DevPools pools(lbk_ctx* c) {
   P.bmax = c->bmax.p;
   P.err = c->err.p;
   return P;
+}
+
+// output map: the export map when set, else the reference-pool map
+const int64_t* out_map(const lbk_ctx* c) { return c->omap.p ? c->omap.p : c->map.p; }
+
+void drop_sgraphs(lbk_ctx* c) {
+  for (auto& q : c->sg) {
+    if (q.g) cudaGraphExecDestroy(q.g);
+    q = lbk_ctx::SGraph{};
+  }
 }
 
 void drop_graphs(lbk_ctx* c) {
@@ -429,12 +451,65 @@ void lbk_destroy(lbk_ctx* c) {
 
   if (c->cev) cudaEventDestroy(c->cev);
   for (auto ev : c->lev) cudaEventDestroy(ev);
-  if (c->sgraph) cudaGraphExecDestroy(c->sgraph);
+  for (auto& q : c->sg)
+    if (q.g) cudaGraphExecDestroy(q.g);
   if (c->dfork) cudaEventDestroy(c->dfork);
   if (c->solve_graph) cudaGraphExecDestroy(c->solve_graph);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
+
+}  // extern "C"
+
+namespace {
+// Per launch level: the output ranges (c->out_off / out_len: reference pool order,
+// or the export layout) of the blocks the level finishes, for the streamed output.
+int build_out_ranges(lbk_ctx* c, lbk_status* st) {
+  const int64_t nb = static_cast<int64_t>(c->out_off.size());
+  {
+    // per launch level: the output ranges of the blocks it finishes
+    // (adjacent blocks merged; pool order is column-major block order)
+    std::vector<std::vector<std::pair<int64_t, int64_t>>> per(c->levels.size());
+    std::vector<int32_t> tl_to_l;
+    for (size_t l = 0; l < c->levels.size(); ++l) {
+      const int32_t hi = c->levels[l].tree_level_hi;
+      if (static_cast<int32_t>(tl_to_l.size()) <= hi) tl_to_l.resize(hi + 1, -1);
+      for (int32_t tl = c->levels[l].tree_level; tl <= hi; ++tl)
+        if (tl_to_l[tl] < 0 || tl == c->levels[l].tree_level) tl_to_l[tl] = static_cast<int32_t>(l);
+    }
+    for (int64_t b = 0; b < nb; ++b) {
+      const int32_t tl = c->blk_final_tl[b];
+      if (tl < 0 || tl >= static_cast<int32_t>(tl_to_l.size()) || tl_to_l[tl] < 0 || c->out_len[b] == 0) continue;
+      auto& v = per[tl_to_l[tl]];
+      if (!v.empty() && v.back().first + v.back().second == c->out_off[b]) v.back().second += c->out_len[b];
+      else v.push_back({c->out_off[b], c->out_len[b]});
+    }
+    std::vector<int64_t> flat, pieces;  // copy ranges; gather pieces of <= 64K entries (one CTA each)
+    c->srange_off.assign(1, 0);
+    c->spiece_off.assign(1, 0);
+    constexpr int64_t PIECE = 1 << 16;
+    for (auto& v : per) {
+      for (auto& pr : v) {
+        flat.push_back(pr.first);
+        flat.push_back(pr.second);
+        for (int64_t o = 0; o < pr.second; o += PIECE) {
+          pieces.push_back(pr.first + o);
+          pieces.push_back(std::min(PIECE, pr.second - o));
+        }
+      }
+      c->srange_off.push_back(static_cast<int64_t>(flat.size() / 2));
+      c->spiece_off.push_back(static_cast<int64_t>(pieces.size() / 2));
+    }
+    LBK_CUDA(c->sranges.upload(pieces.empty() ? std::vector<int64_t>(2, 0) : pieces), st);
+    c->hsranges = flat;
+  }
+  ok(st);
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
 
 // Build the device plan.  flags bit 0: DMMA storage/kernels (diagonal blocks
 // FULL, blocks whose R x C rectangle is >= tau dense RECT); bit 1: dense-
@@ -473,6 +548,10 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     c->wlen.assign(nb, 0);
     c->ref_off.assign(T_ent, T_ent + nb);
     c->ref_len.assign(T_nz, T_nz + nb);
+    c->out_off = c->ref_off;
+    c->out_len = c->ref_len;
+    c->omap.release();
+    c->zcount.release();
     c->blk_final_tl.assign(nb, -1);
     for (int64_t t = 0; t < ntasks; ++t) {
       const int64_t i = steps[t];
@@ -544,6 +623,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       c->store_count[store]++;
     }
     c->nnz = nnz;
+    c->nout = nnz;
     c->nnz_work = nnz_w;
     // ---- working CSC view, orig -> work map, R/C lists, CSR for sparse blocks ------
     std::vector<int32_t> hcp(ncp), hrows(nnz_w);
@@ -1324,47 +1404,8 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
   for (auto ev : c->lev) cudaEventDestroy(ev);
   c->lev.assign(c->levels.size(), nullptr);
   for (auto& ev : c->lev) LBK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), st);
-  if (c->sgraph) {
-    cudaGraphExecDestroy(c->sgraph);
-    c->sgraph = nullptr;
-  }
-  {
-    // per launch level: the reference-pool ranges of the blocks it finishes
-    // (adjacent blocks merged; pool order is column-major block order)
-    std::vector<std::vector<std::pair<int64_t, int64_t>>> per(c->levels.size());
-    std::vector<int32_t> tl_to_l;
-    for (size_t l = 0; l < c->levels.size(); ++l) {
-      const int32_t hi = c->levels[l].tree_level_hi;
-      if (static_cast<int32_t>(tl_to_l.size()) <= hi) tl_to_l.resize(hi + 1, -1);
-      for (int32_t tl = c->levels[l].tree_level; tl <= hi; ++tl)
-        if (tl_to_l[tl] < 0 || tl == c->levels[l].tree_level) tl_to_l[tl] = static_cast<int32_t>(l);
-    }
-    for (int64_t b = 0; b < nb; ++b) {
-      const int32_t tl = c->blk_final_tl[b];
-      if (tl < 0 || tl >= static_cast<int32_t>(tl_to_l.size()) || tl_to_l[tl] < 0 || c->ref_len[b] == 0) continue;
-      auto& v = per[tl_to_l[tl]];
-      if (!v.empty() && v.back().first + v.back().second == c->ref_off[b]) v.back().second += c->ref_len[b];
-      else v.push_back({c->ref_off[b], c->ref_len[b]});
-    }
-    std::vector<int64_t> flat, pieces;  // copy ranges; gather pieces of <= 64K entries (one CTA each)
-    c->srange_off.assign(1, 0);
-    c->spiece_off.assign(1, 0);
-    constexpr int64_t PIECE = 1 << 16;
-    for (auto& v : per) {
-      for (auto& pr : v) {
-        flat.push_back(pr.first);
-        flat.push_back(pr.second);
-        for (int64_t o = 0; o < pr.second; o += PIECE) {
-          pieces.push_back(pr.first + o);
-          pieces.push_back(std::min(PIECE, pr.second - o));
-        }
-      }
-      c->srange_off.push_back(static_cast<int64_t>(flat.size() / 2));
-      c->spiece_off.push_back(static_cast<int64_t>(pieces.size() / 2));
-    }
-    LBK_CUDA(c->sranges.upload(pieces.empty() ? std::vector<int64_t>(2, 0) : pieces), st);
-    c->hsranges = flat;
-  }
+  drop_sgraphs(c);
+  if (build_out_ranges(c, st)) return st->code;
   for (auto& ev : c->dev) LBK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), st);
   for (auto& ev : c->dev2) LBK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), st);
   ok(st);
@@ -1529,7 +1570,7 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
         const int64_t r0 = c->srange_off[pend_lv], nr = c->srange_off[l + 1] - r0;
         const int64_t p0 = c->spiece_off[pend_lv], np_ = c->spiece_off[l + 1] - p0;
         range_gather_kernel<<<static_cast<int>(std::min<int64_t>(np_, 148 * 4)), 256, 0, c->cstream>>>(
-            c->vals.p, c->map.p, c->vout.p, c->sranges.p + 2 * p0, np_);
+            c->vals.p, out_map(c), c->vout.p, c->sranges.p + 2 * p0, np_);
         std::vector<std::pair<int64_t, int64_t>> rs(nr);
         for (int64_t q = 0; q < nr; ++q) rs[q] = {c->hsranges[2 * (r0 + q)], c->hsranges[2 * (r0 + q) + 1]};
         std::sort(rs.begin(), rs.end());
@@ -1572,7 +1613,7 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
     cudaStreamWaitEvent(s0, c->cev, 0);
     return;
   }
-  if (last) gather_kernel<<<148 * 8, 256, 0, s0>>>(c->vals.p, c->map.p, c->vout.p, c->nnz);
+  if (last) gather_kernel<<<148 * 8, 256, 0, s0>>>(c->vals.p, out_map(c), c->vout.p, c->nout);
 }
 
 int nsegments(const lbk_ctx* c) { return static_cast<int>(c->seg_begin.size()) - 1; }
@@ -1724,9 +1765,13 @@ int factorize_host_impl(lbk_ctx* c, const double* a_values, bool a_is_pool, doub
   if (pinned && nsegments(c) == 1 && c->nnz >= (int64_t{1} << 24)) {
     // streamed output: every block's factor values are copied to the host while
     // later levels still run (one graph per output buffer)
-    if (!c->sgraph || c->sgraph_out != lu_values || !same(c->s_tol, pivot_tol) || !same(c->s_eps, static_eps)) {
-      if (c->sgraph) cudaGraphExecDestroy(c->sgraph);
-      c->sgraph = nullptr;
+    lbk_ctx::SGraph* slot = nullptr;
+    for (auto& q : c->sg)
+      if (q.g && q.out == lu_values && same(q.tol, pivot_tol) && same(q.eps, static_eps)) slot = &q;
+    if (!slot) {
+      slot = c->sg[0].used <= c->sg[1].used ? &c->sg[0] : &c->sg[1];  // least recently used
+      if (slot->g) cudaGraphExecDestroy(slot->g);
+      *slot = lbk_ctx::SGraph{};
       cudaGraph_t g;
       LBK_CUDA(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), st);
       (void)cudaGetLastError();
@@ -1734,15 +1779,16 @@ int factorize_host_impl(lbk_ctx* c, const double* a_values, bool a_is_pool, doub
       cudaError_t e = cudaStreamEndCapture(c->stream, &g);
       if (e != cudaSuccess) return cuda_fail(st, e, "streamed graph capture");
       e = cudaGetLastError();
-      if (e == cudaSuccess) e = cudaGraphInstantiate(&c->sgraph, g, cudaGraphInstantiateFlagUseNodePriority);
+      if (e == cudaSuccess) e = cudaGraphInstantiate(&slot->g, g, cudaGraphInstantiateFlagUseNodePriority);
       cudaGraphDestroy(g);
       if (e != cudaSuccess) return cuda_fail(st, e, "streamed graph");
-      c->sgraph_out = lu_values;
-      c->s_tol = pivot_tol;
-      c->s_eps = static_eps;
+      slot->out = lu_values;
+      slot->tol = pivot_tol;
+      slot->eps = static_eps;
     }
+    slot->used = ++c->sg_clock;
     LBK_CUDA(upload_input(), st);
-    LBK_CUDA(cudaGraphLaunch(c->sgraph, c->stream), st);
+    LBK_CUDA(cudaGraphLaunch(slot->g, c->stream), st);
     if (perms && c->ndiag_rows)
       LBK_CUDA(cudaMemcpyAsync(perms, c->perm.p, c->ndiag_rows * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream),
                st);
@@ -1751,7 +1797,7 @@ int factorize_host_impl(lbk_ctx* c, const double* a_values, bool a_is_pool, doub
   if (build_graph(c, pivot_tol, static_eps, st)) return st->code;
   LBK_CUDA(upload_input(), st);
   LBK_CUDA(launch_all(c), st);
-  LBK_CUDA(cudaMemcpyAsync(lu_values, c->vout.p, c->nnz * sizeof(double), cudaMemcpyDeviceToHost, c->stream), st);
+  LBK_CUDA(cudaMemcpyAsync(lu_values, c->vout.p, c->nout * sizeof(double), cudaMemcpyDeviceToHost, c->stream), st);
   if (perms && c->ndiag_rows)
     LBK_CUDA(cudaMemcpyAsync(perms, c->perm.p, c->ndiag_rows * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream),
              st);
@@ -1843,10 +1889,67 @@ int lbk_block_layout(lbk_ctx* c, int64_t* layout) {
 
 int lbk_download(lbk_ctx* c, double* lu_values, int32_t* perms, lbk_status* st) {
   LBK_CUDA(cudaSetDevice(c->device), st);
-  LBK_CUDA(cudaMemcpyAsync(lu_values, c->vout.p, c->nnz * sizeof(double), cudaMemcpyDeviceToHost, c->stream), st);
+  LBK_CUDA(cudaMemcpyAsync(lu_values, c->vout.p, c->nout * sizeof(double), cudaMemcpyDeviceToHost, c->stream), st);
   if (perms && c->ndiag_rows)
     LBK_CUDA(cudaMemcpyAsync(perms, c->perm.p, c->ndiag_rows * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream),
              st);
+  LBK_CUDA(cudaStreamSynchronize(c->stream), st);
+  ok(st);
+  return 0;
+}
+
+// Output in the export layout of the caller (LUFactors blocks as stored by the
+// reference's export, factorize.py:370-384): nout entries, block b's output in
+// [xoff[b], xoff[b+1]) (blocks in pool order), xref[x] = reference-pool entry of
+// output entry x, or -1 for a constant 1.0 (the unit diagonal of L).
+int lbk_set_export(lbk_ctx* c, int64_t nout, const int64_t* xref, const int64_t* xoff, lbk_status* st) {
+  LBK_CUDA(cudaSetDevice(c->device), st);
+  const int64_t nb = static_cast<int64_t>(c->ref_off.size());
+  if (xoff[0] != 0 || xoff[nb] != nout) return fail(st, LBK_ERR_BAD_ARG, "export offsets do not cover nout");
+  for (int64_t x = 0; x < nout; ++x)
+    if (xref[x] < -1 || xref[x] >= c->nnz) return fail(st, LBK_ERR_BAD_ARG, "export entry out of range");
+  LBK_CUDA(cudaStreamSynchronize(c->stream), st);
+  DevBuf<int64_t> xr;
+  std::vector<int64_t> hx(xref, xref + nout);
+  LBK_CUDA(xr.upload(hx), st);
+  LBK_CUDA(c->omap.alloc(std::max<int64_t>(nout, 1)), st);
+  compose_map_kernel<<<148 * 4, 256, 0, c->stream>>>(xr.p, c->map.p, c->omap.p, nout);
+  LBK_CUDA(cudaGetLastError(), st);
+  LBK_CUDA(cudaStreamSynchronize(c->stream), st);
+  c->nout = nout;
+  c->out_off.assign(xoff, xoff + nb);
+  c->out_len.resize(nb);
+  for (int64_t b = 0; b < nb; ++b) c->out_len[b] = xoff[b + 1] - xoff[b];
+  LBK_CUDA(c->out_off_d.upload(std::vector<int64_t>(xoff, xoff + nb + 1)), st);
+  LBK_CUDA(c->zcount.alloc(std::max<int64_t>(nb, 1)), st);
+  LBK_CUDA(c->vout.alloc(std::max<int64_t>(nout, 1)), st);
+  drop_graphs(c);  // the gather nodes captured the old output map / buffer
+  drop_sgraphs(c);
+  return build_out_ranges(c, st);
+}
+
+int64_t lbk_num_out(lbk_ctx* c) { return c ? c->nout : 0; }
+
+// Exact zeros per block in the last factorization's output (export layout):
+// the caller drops them like the reference's export (factorize.py:179-192)
+// only where a block has any.
+int lbk_export_zero_counts(lbk_ctx* c, int64_t* counts, lbk_status* st) {
+  LBK_CUDA(cudaSetDevice(c->device), st);
+  const int64_t nb = static_cast<int64_t>(c->out_off.size());
+  if (!c->zcount.p) {
+    LBK_CUDA(c->zcount.alloc(std::max<int64_t>(nb, 1)), st);
+    LBK_CUDA(c->out_off_d.upload([&] {
+      std::vector<int64_t> o(c->out_off);
+      o.push_back(c->nout);
+      return o;
+    }()), st);
+  }
+  if (nb) {
+    zero_count_kernel<<<static_cast<int>(std::min<int64_t>(nb, 148 * 8)), 256, 0, c->stream>>>(c->vout.p, c->out_off_d.p,
+                                                                                              nb, c->zcount.p);
+    LBK_CUDA(cudaGetLastError(), st);
+    LBK_CUDA(cudaMemcpyAsync(counts, c->zcount.p, nb * sizeof(int64_t), cudaMemcpyDeviceToHost, c->stream), st);
+  }
   LBK_CUDA(cudaStreamSynchronize(c->stream), st);
   ok(st);
   return 0;

@@ -73,7 +73,7 @@ int partition_count(int64_t n, const int64_t* fcp, const int64_t* fri, int64_t p
 
 int partition_fill(int64_t n, const int64_t* fcp, const int64_t* fri, const int64_t* acp, const int64_t* ari,
                    const double* aval, int64_t p, const int64_t* pos, int64_t* table, int64_t nb_total,
-                   int64_t* col_ptr, int64_t* row_idx, double* values, int64_t* block_nnz) {
+                   int64_t* col_ptr, int64_t* row_idx, double* values, int64_t* block_nnz, int64_t* apos) {
   std::vector<int32_t> rowblk(n);
   for (int64_t b = 0; b < p; ++b)
     for (int64_t r = pos[b]; r < pos[b + 1]; ++r) rowblk[r] = static_cast<int32_t>(b);
@@ -116,7 +116,10 @@ int partition_fill(int64_t n, const int64_t* fcp, const int64_t* fri, const int6
         row_idx[k] = r - pos[b];
         // A's entries of this column are a sorted subset of the filled column
         double v = 0.0;
-        if (a < a1 && ari[a] == r) v = aval[a++];
+        if (a < a1 && ari[a] == r) {
+          if (apos) apos[a] = k;  // pool position of A's entry a
+          v = aval[a++];
+        }
         values[k] = v;
         col_ptr[T_cp[blk_id[b]] + (c - c0) + 1]++;
       }
@@ -365,10 +368,10 @@ int lbk_partition_count(int64_t n, const int64_t* f_col_ptr, const int64_t* f_ro
 int lbk_partition_fill(int64_t n, const int64_t* f_col_ptr, const int64_t* f_row_idx, const int64_t* a_col_ptr,
                        const int64_t* a_row_idx, const double* a_values, int64_t p, const int64_t* positions,
                        int64_t nblocks, int64_t* table, int64_t* col_ptr, int64_t* row_idx, double* values,
-                       int64_t* block_nnz) {
+                       int64_t* block_nnz, int64_t* a_pos) {
   try {
     return partition_fill(n, f_col_ptr, f_row_idx, a_col_ptr, a_row_idx, a_values, p, positions, table, nblocks,
-                          col_ptr, row_idx, values, block_nnz);
+                          col_ptr, row_idx, values, block_nnz, a_pos);
   } catch (const std::bad_alloc&) {
     return LBK_ERR_OOM;
   }

@@ -285,7 +285,10 @@ __global__ void range_gather_kernel(const double* __restrict__ work, const int64
                                     double* __restrict__ out, const int64_t* __restrict__ ranges, int64_t n) {
   for (int64_t q = blockIdx.x; q < n; q += gridDim.x) {
     const int64_t off = ranges[2 * q], len = ranges[2 * q + 1];
-    for (int64_t e = threadIdx.x; e < len; e += blockDim.x) out[off + e] = work[map[off + e]];
+    for (int64_t e = threadIdx.x; e < len; e += blockDim.x) {
+      const int64_t m = map[off + e];
+      out[off + e] = m >= 0 ? work[m] : 1.0;  // -1: unit diagonal of an exported L block
+    }
   }
 }
 
@@ -300,8 +303,40 @@ __global__ void expand_kernel(const double* __restrict__ a, const int64_t* __res
 __global__ void gather_kernel(const double* __restrict__ work, const int64_t* __restrict__ map,
                               double* __restrict__ out, int64_t n) {
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
-       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    out[e] = work[map[e]];
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t m = map[e];
+    out[e] = m >= 0 ? work[m] : 1.0;
+  }
+}
+
+// omap[x] = xref[x] < 0 ? -1 : map[xref[x]]  (export layout -> working positions)
+__global__ void compose_map_kernel(const int64_t* __restrict__ xref, const int64_t* __restrict__ map,
+                                   int64_t* __restrict__ omap, int64_t n) {
+  for (int64_t x = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < n;
+       x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = xref[x];
+    omap[x] = r < 0 ? -1 : map[r];
+  }
+}
+
+// zc[b] = number of exact zeros in out[off[b], off[b+1]) (one CTA per block, strided)
+__global__ void zero_count_kernel(const double* __restrict__ out, const int64_t* __restrict__ off, int64_t nb,
+                                  int64_t* __restrict__ zc) {
+  __shared__ int part[8];
+  for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    int cnt = 0;
+    const int64_t e1 = off[b + 1];
+    for (int64_t e = off[b] + threadIdx.x; e < e1; e += blockDim.x) cnt += out[e] == 0.0;
+    for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t t = 0;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) t += part[w];
+      zc[b] = t;
+    }
+    __syncthreads();
+  }
 }
 
 }  // namespace lbk

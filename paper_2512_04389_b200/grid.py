@@ -87,6 +87,10 @@ class BlockGrid:
     nnz_filled: int
     value_max: float
     pool: GridPool | None = field(default=None, repr=False, compare=False)
+    # pool position of every entry of A (CSC order) when built by ``partition``: the
+    # remaining pool entries are the fill (exactly 0.0, grid.py:85-148), so the device
+    # factorization only needs A's nnz values (numeric.factorize)
+    a_pos: np.ndarray | None = field(default=None, repr=False, compare=False)
 
     def lower_blocks(self, i: int) -> np.ndarray:
         return i + 1 + np.flatnonzero(self.block_nnz[i + 1:, i])
@@ -126,17 +130,10 @@ def pool_grid(grid) -> GridPool:
 
 def pool_positions(f: FilledPattern, a: CscMatrix, plan: BlockingPlan) -> np.ndarray:
     """Position in the pooled grid values (reference pool order) of every entry
-    of A (CSC order): partition() run on the entry numbers instead of the
-    values.  Refactorizations with new values on A's pattern then only move
-    A's entries to the device (Engine.bind_matrix / refactor_host)."""
-    ids = CscMatrix(a.n, a.col_ptr, a.row_idx, np.arange(1, a.nnz + 1, dtype=np.float64))
-    vals = partition(f, ids, plan).pool.values
-    nz = np.flatnonzero(vals)
-    pmap = np.full(a.nnz, -1, np.int64)
-    pmap[vals[nz].astype(np.int64) - 1] = nz
-    if (pmap < 0).any():
-        raise DimensionMismatch("A has entries outside the filled pattern")
-    return pmap
+    of A (CSC order), as recorded by ``partition`` (``BlockGrid.a_pos``).
+    Refactorizations with new values on A's pattern then only move A's entries
+    to the device (Engine.bind_matrix / refactor_host)."""
+    return partition(f, a, plan).a_pos
 
 
 def partition(f: FilledPattern, a: CscMatrix, plan: BlockingPlan) -> BlockGrid:
@@ -165,10 +162,15 @@ def partition(f: FilledPattern, a: CscMatrix, plan: BlockingPlan) -> BlockGrid:
     row_idx = np.empty(nnzf, np.int64)
     values = np.empty(nnzf, np.float64)
     block_nnz = np.empty((p, p), np.int64)
+    a_pos = np.empty(len(ari), np.int64)
     rc = lib.lbk_partition_fill(n, P(fcp, i64), P(fri, i64), P(acp, i64), P(ari, i64), P(av, _native.c_f64p),
                                 p, P(pos, i64), nblocks, P(table, i64), P(col_ptr, i64), P(row_idx, i64),
-                                P(values, _native.c_f64p), P(block_nnz, i64))
+                                P(values, _native.c_f64p), P(block_nnz, i64), P(a_pos, i64))
     _native.check_host(rc, "partition")
+    # the grid is an input (factorize never mutates it, factorize.py:265); read-only
+    # pooled values guarantee that the fill entries stay 0.0, which lets the device
+    # path upload only A's values (a_pos)
+    values.flags.writeable = False
     pool = GridPool(table=table, col_ptr=col_ptr, row_idx=row_idx, values=values)
     blocks = {}
     for b in range(nblocks):
@@ -177,7 +179,7 @@ def partition(f: FilledPattern, a: CscMatrix, plan: BlockingPlan) -> BlockGrid:
                                        row_idx=row_idx[eo:eo + nz], values=values[eo:eo + nz])
     value_max = float(np.max(np.abs(av))) if a.nnz else 0.0
     return BlockGrid(n=n, p=p, plan=plan, blocks=blocks, block_nnz=block_nnz,
-                     nnz_filled=f.nnz_filled, value_max=value_max, pool=pool)
+                     nnz_filled=f.nnz_filled, value_max=value_max, pool=pool, a_pos=a_pos)
 
 
 class TaskView(NamedTuple):

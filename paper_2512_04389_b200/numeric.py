@@ -85,6 +85,9 @@ def _dev():
     d(lib, "lbk_stream", vp, [vp])
     d(lib, "lbk_work_ptrs", C.c_int, [vp, C.POINTER(vp), C.POINTER(vp), C.POINTER(vp)])
     d(lib, "lbk_block_layout", C.c_int, [vp, i64p])
+    d(lib, "lbk_set_export", C.c_int, [vp, C.c_int64, i64p, i64p, st])
+    d(lib, "lbk_num_out", C.c_int64, [vp])
+    d(lib, "lbk_export_zero_counts", C.c_int, [vp, i64p, st])
     _native._dev = lib
     return lib
 
@@ -142,6 +145,35 @@ def pinned_empty(nbytes_or_count, dtype=np.float64):
 
 class _PinnedArray(np.ndarray):
     _owner = None
+
+
+_PINNED_FREE: dict = {}  # (count, dtype) -> page-locked arrays no longer referenced by any result
+_PINNED_KEEP = 2
+
+
+class _Recycle:
+    """Owner of a recycled page-locked array: when the last view of it dies (e.g. the
+    LUFactors built on it), the array returns to the free list instead of being
+    unpinned - cudaHostAlloc of gigabytes costs far more than a factorization."""
+
+    def __init__(self, key, arr):
+        self.key, self.arr = key, arr
+
+    def __del__(self):
+        free = _PINNED_FREE.setdefault(self.key, [])
+        if len(free) < _PINNED_KEEP:
+            free.append(self.arr)
+
+
+def pinned_recycled(count, dtype=np.float64) -> np.ndarray:
+    """Page-locked array from the recycle list (allocated on a miss); returned to
+    the list when no view of it is alive any more."""
+    key = (int(count), np.dtype(dtype).str)
+    free = _PINNED_FREE.get(key)
+    arr = free.pop() if free else pinned_empty(count, dtype)
+    out = arr.view(_PinnedArray)
+    out._owner = _Recycle(key, arr)
+    return out
 
 
 class Engine:
@@ -218,6 +250,9 @@ class Engine:
         if rc:
             _native.raise_status(st, "lbk_plan")
         self.nnz = int(pl.values.shape[0])
+        self.nout = self.nnz  # output entries (enable_export: the LUFactors layout)
+        self.export = None
+        self.bound_a = None  # a_pos array bound with bind_matrix (refactorization input)
         info = np.zeros(14, np.int64)
         self.lib.lbk_plan_info(ctx, P(info, i64p))
         self.info = info
@@ -229,6 +264,61 @@ class Engine:
         self.dmma_flops_executed, self.exec_flops_executed = float(info[12]), float(info[13])
         self._resident = False
         self.generation = 0  # bumped by every factorization: device factors of LUFactors stay valid until then
+
+    def enable_export(self) -> None:
+        """Make every output of this engine the LUFactors layout of the reference's
+        export (factorize.py:370-384): off-diagonal blocks as stored, diagonal blocks
+        split into triu(d) then tril(d,-1)+I.  Structures are computed once here; a
+        factorization then returns values the blocks view without a host-side copy."""
+        if getattr(self, "export", None) is not None:
+            return
+        t = self.pool.table
+        cpool, rpool = self.pool.col_ptr, self.pool.row_idx
+        xref, xoff, shapes = [], [0], []
+        for b in range(self.pool.nblocks):
+            bi, bj, nr, nc, nz, cpo, eo = (int(x) for x in t[:, b])
+            cp = cpool[cpo:cpo + nc + 1]
+            ri = rpool[eo:eo + nz]
+            if bi != bj:
+                xref.append(np.arange(eo, eo + nz, dtype=np.int64))
+                shapes.append((cp, ri, None, None))
+                xoff.append(xoff[-1] + nz)
+                continue
+            m = nr
+            cols = np.repeat(np.arange(m, dtype=np.int64), np.diff(cp))
+            up = ri <= cols
+            ucp = np.zeros(m + 1, np.int64)
+            np.cumsum(np.bincount(cols[up], minlength=m), out=ucp[1:])
+            lo = ~up
+            lcp = np.zeros(m + 1, np.int64)
+            np.cumsum(np.bincount(cols[lo], minlength=m) + 1, out=lcp[1:])
+            unit = lcp[:-1]
+            lref = np.empty(lcp[-1], np.int64)
+            lrow = np.empty(lcp[-1], np.int64)
+            other = np.ones(lcp[-1], bool)
+            other[unit] = False
+            lref[unit] = -1
+            lrow[unit] = np.arange(m)
+            lref[other] = eo + np.flatnonzero(lo)
+            lrow[other] = ri[lo]
+            xref.append(eo + np.flatnonzero(up))
+            xref.append(lref)
+            shapes.append((ucp, ri[up], lcp, lrow))
+            xoff.append(xoff[-1] + int(up.sum()) + len(lref))
+        xr = np.concatenate(xref) if xref else np.zeros(0, np.int64)
+        xo = np.asarray(xoff, np.int64)
+        st = _native.LbkStatus()
+        if self.lib.lbk_set_export(self.ctx, len(xr), P(xr, i64p), P(xo, i64p), C.byref(st)):
+            _native.raise_status(st, "lbk_set_export")
+        self.export = (xo, shapes)
+        self.nout = int(len(xr))
+
+    def export_zero_counts(self) -> np.ndarray:
+        zc = np.zeros(self.pool.nblocks, np.int64)
+        st = _native.LbkStatus()
+        if self.lib.lbk_export_zero_counts(self.ctx, P(zc, i64p), C.byref(st)):
+            _native.raise_status(st, "lbk_export_zero_counts")
+        return zc
 
     def solve(self, b) -> np.ndarray:
         """x = U^-1 L^-1 b[perm_global] on the device-resident factors of the
@@ -407,7 +497,7 @@ class Engine:
         return lv, it
 
     def download(self):
-        vals = np.empty(self.nnz, np.float64)
+        vals = np.empty(self.nout, np.float64)
         perms = np.empty(max(self.n_diag_rows, 1), np.int32)
         st = _native.LbkStatus()
         if self.lib.lbk_download(self.ctx, P(vals, f64p), P(perms, i32p), C.byref(st)):
@@ -517,6 +607,54 @@ def build_factors(grid, pool: GridPool, values: np.ndarray, perms_pool: np.ndarr
     return LUFactors(n=grid.n, plan=grid.plan, l_blocks=lb, u_blocks=ub, perms=perms)
 
 
+def _ro(a: np.ndarray) -> np.ndarray:
+    v = a.view()
+    v.flags.writeable = False
+    return v
+
+
+def _perm_list(grid, perms_pool):
+    spans = np.diff(grid.plan.positions)
+    perms = []
+    off = 0
+    for i in range(grid.p):
+        s = int(spans[i])
+        if perms_pool is not None and len(perms_pool):
+            perms.append(perms_pool[off:off + s].astype(np.int64))
+        else:
+            perms.append(np.arange(s))
+        off += s
+    return perms
+
+
+def build_factors_export(grid, eng, out: np.ndarray, zero_counts: np.ndarray, perms_pool) -> LUFactors:
+    """LUFactors over the export-layout output of ``eng`` (Engine.enable_export):
+    block values are views of ``out`` (which they keep alive), structures are the
+    cached read-only export structures; blocks holding exact zeros are compacted
+    like the reference's export (factorize.py:179-192)."""
+    xo, shapes = eng.export
+    t = eng.pool.table
+    lb, ub = {}, {}
+    for b in range(eng.pool.nblocks):
+        bi, bj, nr, nc = (int(x) for x in t[:4, b])
+        seg = out[xo[b]:xo[b + 1]]
+        cp, ri, lcp, lrow = shapes[b]
+        z = zero_counts[b] != 0
+        if bi != bj:
+            blk = _drop_zeros(nr, nc, cp, ri, seg) if z else SparseBlock(nr, nc, _ro(cp), _ro(ri), seg)
+            (lb if bi > bj else ub)[(bi, bj)] = blk
+            continue
+        nu = len(ri)
+        uv, lv = seg[:nu], seg[nu:]
+        if z:
+            ub[(bi, bj)] = _drop_zeros(nr, nr, cp, ri, uv)
+            lb[(bi, bj)] = _drop_zeros(nr, nr, lcp, lrow, lv)
+        else:
+            ub[(bi, bj)] = SparseBlock(nr, nr, _ro(cp), _ro(ri), uv)
+            lb[(bi, bj)] = SparseBlock(nr, nr, _ro(lcp), _ro(lrow), lv)
+    return LUFactors(n=grid.n, plan=grid.plan, l_blocks=lb, u_blocks=ub, perms=_perm_list(grid, perms_pool))
+
+
 def _block_from_tile(d: np.ndarray) -> SparseBlock:
     """Dense tile -> CSC dropping exact zeros (factorize.py:179-192)."""
     cols, rows = np.nonzero(d.T)
@@ -587,22 +725,38 @@ def factorize(grid, tree, workers: int = 1, pivot_tol: float = DEFAULT_PIVOT_TOL
     """
     if workers < 1:
         raise DimensionMismatch(f"workers must be >= 1, got {workers}")
-    for dense in (False, True):
-        eng = engine_for(grid, tree, device=device, dense=dense, chunk=chunk, dense_threshold=dense_threshold)
-        vals_in = np.ascontiguousarray(eng.pool.values, dtype=np.float64)
-        out = np.empty(eng.nnz, np.float64)
-        perms = np.empty(max(eng.n_diag_rows, 1), np.int32)
-        st = eng.run_host(vals_in, out, perms, pivot_tol, static_pivot)
-        if st.code == _native.LBK_ERR_PIVOT_SWAP and not dense:
-            continue
+    eng = engine_for(grid, tree, device=device, dense=False, chunk=chunk, dense_threshold=dense_threshold)
+    eng.enable_export()
+    out = pinned_recycled(eng.nout)
+    perms = np.empty(max(eng.n_diag_rows, 1), np.int32)
+    a_pos = getattr(grid, "a_pos", None)
+    if a_pos is not None and eng.pool is getattr(grid, "pool", None) and not eng.pool.values.flags.writeable:
+        # a grid built by partition(): its read-only pool holds A's values at a_pos and
+        # exact zeros (the fill) elsewhere, so only A's nnz values travel to the device
+        if eng.bound_a is not a_pos:
+            eng.bind_matrix(a_pos)
+            eng.bound_a = a_pos
+            eng.a_stage = pinned_empty(len(a_pos))
+        np.take(eng.pool.values, a_pos, out=eng.a_stage)
+        st = eng.refactor_host(eng.a_stage, out, perms, pivot_tol, static_pivot)
+    else:  # foreign (e.g. reference-built) grid: the whole pooled value array
+        st = eng.run_host(np.ascontiguousarray(eng.pool.values, dtype=np.float64), out, perms, pivot_tol,
+                          static_pivot)
+    if st.code != _native.LBK_ERR_PIVOT_SWAP:
         _native.raise_status(st, "factorize")
-        if dense:
-            lu = build_factors_full(grid, eng.pool, eng.download_work(), perms[: eng.n_diag_rows])
-        else:
-            lu = build_factors(grid, eng.pool, out, perms[: eng.n_diag_rows])
+        lu = build_factors_export(grid, eng, out, eng.export_zero_counts(), perms[: eng.n_diag_rows])
         lu._device = (eng, eng.generation)
         return lu
-    raise DeviceError("unreachable")  # pragma: no cover
+    # a row swap inside a diagonal block whose block row is stored compressed:
+    # the reference's dense-scratch semantics on full-rectangle blocks (still on the device)
+    eng = engine_for(grid, tree, device=device, dense=True, chunk=chunk, dense_threshold=dense_threshold)
+    vals_in = np.ascontiguousarray(eng.pool.values, dtype=np.float64)
+    out = np.empty(eng.nnz, np.float64)
+    st = eng.run_host(vals_in, out, perms, pivot_tol, static_pivot)
+    _native.raise_status(st, "factorize")
+    lu = build_factors_full(grid, eng.pool, eng.download_work(), perms[: eng.n_diag_rows])
+    lu._device = (eng, eng.generation)
+    return lu
 
 
 # --- validation (host, like the reference) -------------------------------------
