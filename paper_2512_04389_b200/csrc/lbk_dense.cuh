@@ -52,6 +52,8 @@ struct GemmTask {
 struct GemmItem {
   int32_t task;
   int32_t m0, n0;
+  int32_t nkc;     // < 0: every GBK-chunk of the inner dimension; else the number of listed chunks
+  int64_t kc_off;  // offset of the chunk list in P.kchunks (chunks whose L rows x U columns hold entries)
 };
 
 struct DenseItem {
@@ -111,11 +113,14 @@ __device__ __forceinline__ void gemm_map_item(const GemmItem it, const GemmTask*
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  const int nk = (K + GBK - 1) / GBK;
+  // inner-dimension chunks: all of them, or (k-chunk skipping) only those in which the
+  // tile's L rows and U columns both hold pattern entries - the others multiply exact zeros
+  const int nk = it.nkc < 0 ? (K + GBK - 1) / GBK : it.nkc;
+  const int32_t* kcl = it.nkc < 0 ? nullptr : P.kchunks + it.kc_off;
   auto stageA = [&](int s) { return sm + s * (GBK * SA + GBN * SB); };
   auto stageB = [&](int s) { return sm + s * (GBK * SA + GBN * SB) + GBK * SA; };
   auto load = [&](int s, int kt) {
-    const int k0 = kt * GBK;
+    const int k0 = (kcl ? kcl[kt] : kt) * GBK;
     double* As = stageA(s);
     double* Bs = stageB(s);
 #pragma unroll

@@ -213,6 +213,7 @@ struct lbk_ctx {
   DevBuf<Item> items;
   DevBuf<GemmTask> gtasks;
   DevBuf<GemmItem> gitems;
+  DevBuf<int32_t> kchunks;
   DevBuf<DenseItem> ditems;
   DevBuf<TileItem> titems;
   DevBuf<XTask> xtasks;
@@ -323,6 +324,7 @@ DevPools pools(lbk_ctx* c) {
   P.rlist = c->rlist.p;
   P.clist = c->clist.p;
   P.maps = c->maps.p;
+  P.kchunks = c->kchunks.p;
   P.perm = c->perm.p;
   P.colmax = c->colmax.p;
   P.bmax = c->bmax.p;
@@ -833,6 +835,48 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       return v;
     };
     auto tile_like = [&](int64_t b) { return hb[b].store != STORE_SPARSE; };
+    // pattern occupancy of a FULL/RECT block in its stored (compressed) coordinates:
+    // lmask[c] = 128-row tiles holding entries of stored column c (as an SSSSM L operand),
+    // umask[r] = 64-column tiles holding entries of stored row r (as a U operand)
+    std::map<int64_t, std::vector<uint64_t>> lmask_c, umask_c;
+    std::vector<int32_t> hkch;
+    auto stored_pos = [&](int64_t b, bool rows_dim) {
+      const BlockDev& d = hb[b];
+      const int n = rows_dim ? d.nrows : d.ncols;
+      std::vector<int32_t> pos(n);
+      if (d.store == STORE_RECT) {
+        std::fill(pos.begin(), pos.end(), -1);
+        const std::vector<int32_t>& lst = rows_dim ? Rl[b] : Cl[b];
+        for (size_t q = 0; q < lst.size(); ++q) pos[lst[q]] = static_cast<int32_t>(q);
+      } else {
+        for (int q = 0; q < n; ++q) pos[q] = q;
+      }
+      return pos;
+    };
+    auto lmask = [&](int64_t b) -> const std::vector<uint64_t>& {
+      auto it = lmask_c.find(b);
+      if (it != lmask_c.end()) return it->second;
+      std::vector<uint64_t> m(hb[b].nC, 0);
+      const std::vector<int32_t> rp = stored_pos(b, true), cpn = stored_pos(b, false);
+      const int64_t* scp = colptr + T_cp[b];
+      const int64_t* sri = rowidx + T_ent[b];
+      for (int col = 0; col < hb[b].ncols; ++col)
+        for (int64_t e = scp[col]; e < scp[col + 1]; ++e)
+          m[cpn[col]] |= 1ull << std::min(rp[sri[e]] / GBM, 63);
+      return lmask_c.emplace(b, std::move(m)).first->second;
+    };
+    auto umask = [&](int64_t b) -> const std::vector<uint64_t>& {
+      auto it = umask_c.find(b);
+      if (it != umask_c.end()) return it->second;
+      std::vector<uint64_t> m(hb[b].nR, 0);
+      const std::vector<int32_t> rp = stored_pos(b, true), cpn = stored_pos(b, false);
+      const int64_t* scp = colptr + T_cp[b];
+      const int64_t* sri = rowidx + T_ent[b];
+      for (int col = 0; col < hb[b].ncols; ++col)
+        for (int64_t e = scp[col]; e < scp[col + 1]; ++e)
+          m[rp[sri[e]]] |= 1ull << std::min(cpn[col] / GBN, 63);
+      return umask_c.emplace(b, std::move(m)).first->second;
+    };
     for (int64_t t = 0; t < ntasks; ++t) {
       if (!c->mask.empty() && !c->mask[t]) continue;  // another rank's task (owner-computes)
       const int kind = kinds[t];
@@ -949,12 +993,46 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           }
           const int32_t task = static_cast<int32_t>(gtasks.size());
           c->route[t] = 1;
-          c->dmma_flops += 2.0 * hb[lb].nR * static_cast<double>(gt.K) * hb[ub].nC;
           gtasks.push_back(gt);
           const int slack = c->defer.empty() ? 0 : c->defer[t];
           auto& dst = slack >= 3 ? gemE[lv] : slack == 2 ? gemD[lv] : gem[lv];
+          // k-chunk skipping: per GBK-chunk of the inner index, the 128-row tiles of L and the
+          // 64-column tiles of U holding pattern entries (bit per tile, saturating at 63)
+          // (dense-scratch mode: row swaps move the support, so every chunk runs)
+          const int nkch = (gt.K + GBK - 1) / GBK;
+          std::vector<uint64_t> chL(nkch, ~0ull), chU(nkch, ~0ull);
+          if (!all_full) {
+            const std::vector<uint64_t>& lm = lmask(lb);
+            const std::vector<uint64_t>& um = umask(ub);
+            std::fill(chL.begin(), chL.end(), 0);
+            std::fill(chU.begin(), chU.end(), 0);
+            for (int32_t k = 0; k < gt.K; ++k) {
+              chL[k / GBK] |= lm[kid ? k : kl[k]];
+              chU[k / GBK] |= um[kid ? k : ku[k]];
+            }
+          }
+          std::vector<int32_t> act;
           for (int32_t n0 = 0; n0 < hb[ub].nC; n0 += GBN)
-            for (int32_t m0 = 0; m0 < hb[lb].nR; m0 += GBM) dst.push_back(GemmItem{task, m0, n0});
+            for (int32_t m0 = 0; m0 < hb[lb].nR; m0 += GBM) {
+              const uint64_t bm = 1ull << std::min(m0 / GBM, 63), bn = 1ull << std::min(n0 / GBN, 63);
+              act.clear();
+              int64_t klen = 0;
+              for (int q = 0; q < nkch; ++q)
+                if ((chL[q] & bm) && (chU[q] & bn)) {
+                  act.push_back(q);
+                  klen += std::min(GBK, gt.K - q * GBK);
+                }
+              if (act.empty()) continue;  // the tile's product is structurally zero
+              GemmItem gi{task, m0, n0, -1, 0};
+              if (static_cast<int>(act.size()) < nkch) {
+                gi.nkc = static_cast<int32_t>(act.size());
+                gi.kc_off = static_cast<int64_t>(hkch.size());
+                hkch.insert(hkch.end(), act.begin(), act.end());
+              }
+              dst.push_back(gi);
+              c->dmma_flops += 2.0 * std::min(GBM, hb[lb].nR - m0) * static_cast<double>(klen) *
+                               std::min(GBN, hb[ub].nC - n0);
+            }
           continue;
         }
         acc_len[lv] = std::max(acc_len[lv], hb[tgt].nrows);
@@ -1358,6 +1436,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     LBK_CUDA(c->items.upload(gall), st);
     LBK_CUDA(c->gtasks.upload(gtasks), st);
     LBK_CUDA(c->gitems.upload(mall), st);
+    LBK_CUDA(c->kchunks.upload(hkch.empty() ? std::vector<int32_t>(1, 0) : hkch), st);
     LBK_CUDA(c->ditems.upload(dall), st);
     LBK_CUDA(c->titems.upload(tall), st);
     LBK_CUDA(c->xtasks.upload(xtasks), st);

@@ -141,6 +141,50 @@ __device__ __forceinline__ void trail16(const double (&l)[16], int c0, int ce, T
   }
 }
 
+
+#ifndef LBK_TILE_DMMA
+#define LBK_TILE_DMMA 1  // trailing updates inside the tile LU / TRSM routines on the FP64 tensor cores
+#endif
+
+// C[r0 + i, c0 + j] -= sum_{k < 16} A[r0 + i + k * lda] * B[k + (c0 + j) * ldb]  (i < nr, j < nc; all in
+// shared memory, column-major).  The rank-16 trailing update of the blocked tile routines on DMMA
+// (m8n8k4): 8x8 output tiles dealt over the 8 warps, up to 8 tiles per warp with independent
+// accumulators; operands outside the range read as zero.  Replaces ~200 FMAs and ~240 shared loads per
+// thread (shared-memory bound) by <= 32 DMMAs per warp.  Callers fence with __syncthreads on both sides.
+__device__ __noinline__ void mma_sub_k16(double* C, int ldc, const double* A, int lda, const double* B, int ldb,
+                                         int r0, int nr, int c0, int nc) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int tr = (nr + 7) >> 3, ntile = tr * ((nc + 7) >> 3);
+  if (warp >= ntile) return;
+  double acc[8][2];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = 0.0;
+#pragma unroll
+  for (int k4 = 0; k4 < 16; k4 += 4) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int tile = warp + 8 * q;
+      if (tile < ntile) {  // warp-uniform
+        const int i = (tile % tr) * 8 + g, j = (tile / tr) * 8 + g;
+        const double a = i < nr ? A[r0 + i + (k4 + t) * lda] : 0.0;
+        const double b = j < nc ? B[k4 + t + (c0 + j) * ldb] : 0.0;
+        dmma(acc[q][0], acc[q][1], a, b);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int tile = warp + 8 * q;
+    if (tile < ntile) {
+      const int i = (tile % tr) * 8 + g, j = (tile / tr) * 8 + 2 * t;
+      if (i < nr) {
+        if (j < nc) C[r0 + i + (c0 + j) * ldc] -= acc[q][0];
+        if (j + 1 < nc) C[r0 + i + (c0 + j + 1) * ldc] -= acc[q][1];
+      }
+    }
+  }
+}
+
 // X (smem, XTP) <- X U^{-1} for columns [0, nc); U upper in smem (XTP), rinv[j] =
 // 1/u_jj.  Blocked by 16 columns: the panel solve needs no communication
 // between rows (threads 0..63 own one row each), the trailing update runs on
@@ -173,6 +217,9 @@ __device__ void tile_right_solve_blk(double* X, const double* U, const double* r
     __syncthreads();
     const int pe = pb + PB;
     if (pe >= nc) break;
+#if LBK_TILE_DMMA
+    mma_sub_k16(X, XTP, X + pb * XTP, XTP, U + pb, XTP, 0, XT, pe, nc - pe);
+#else
     {
       const int r = tid & (XT - 1);
       double l[PB];
@@ -181,6 +228,7 @@ __device__ void tile_right_solve_blk(double* X, const double* U, const double* r
       trail16(l, pe + (tid >> 6), nc, [&](int c) { return X + c * XTP + r; },
               [&](int c) { return U + c * XTP + pb; });
     }
+#endif
     __syncthreads();
   }
 }
@@ -207,6 +255,9 @@ __device__ void tile_left_solve_blk(double* X, const double* Lm, int nr) {
     __syncthreads();
     const int pe = pb + PB;
     if (pe >= nr) break;
+#if LBK_TILE_DMMA
+    mma_sub_k16(X, XTP, Lm + pb * XTP, XTP, X + pb, XTP, pe, nr - pe, 0, XT);
+#else
     {
       // X[r, c] -= sum_k L[r, pb + k] X[pb + k, c] for the R = nr - pe rows below
       // the panel: work units (row, group of 4 columns) dealt over all 256
@@ -228,6 +279,7 @@ __device__ void tile_left_solve_blk(double* X, const double* Lm, int nr) {
         for (int j = 0; j < 4; ++j) X[(c0 + j) * XTP + r] = a4[j];
       }
     }
+#endif
     __syncthreads();
   }
 }
@@ -311,7 +363,10 @@ __device__ void tile_lu64_blocked(double* T, int n, double* Dd, double* urow, lo
     }
     __syncthreads();
     if (prof) { const long long t1 = clock64(); if (tid == 0) prof[1] += t1 - t0; t0 = t1; }
-    // (3) A22 -= L21 U12: work units (row, group of 4 columns) dealt over all 256 threads
+    // (3) A22 -= L21 U12 (tensor cores, or work units (row, group of 4 columns) dealt over all 256 threads)
+#if LBK_TILE_DMMA
+    mma_sub_k16(T, XTP, T + pb * XTP, XTP, T + pb, XTP, pe, n - pe, pe, n - pe);
+#else
     {
       const int R = n - pe, CG = (n - pe + 3) / 4;
 #pragma unroll 1
@@ -331,6 +386,7 @@ __device__ void tile_lu64_blocked(double* T, int n, double* Dd, double* urow, lo
           if (c0 + j < n) T[(c0 + j) * XTP + r] = a4[j];
       }
     }
+#endif
     __syncthreads();
     if (prof) { const long long t1 = clock64(); if (tid == 0) prof[2] += t1 - t0; t0 = t1; }
   }

@@ -305,6 +305,16 @@ class Engine:
             xref.append(lref)
             shapes.append((ucp, ri[up], lcp, lrow))
             xoff.append(xoff[-1] + int(up.sum()) + len(lref))
+        # per block: (key, L/U/diag, rows, cols, x0, split, x1, read-only structures) for build_factors_export
+        recs = []
+        for b in range(self.pool.nblocks):
+            bi, bj, nr, nc = (int(x) for x in t[:4, b])
+            cp, ri, lcp, lrow = shapes[b]
+            x0, x1 = xoff[b], xoff[b + 1]
+            kind = 0 if bi > bj else (1 if bi < bj else 2)
+            recs.append(((bi, bj), kind, nr, nc, x0, x0 + len(ri), x1, _ro(cp), _ro(ri),
+                         None if lcp is None else _ro(lcp), None if lrow is None else _ro(lrow)))
+        self.export_recs = recs
         xr = np.concatenate(xref) if xref else np.zeros(0, np.int64)
         xo = np.asarray(xoff, np.int64)
         st = _native.LbkStatus()
@@ -632,26 +642,20 @@ def build_factors_export(grid, eng, out: np.ndarray, zero_counts: np.ndarray, pe
     block values are views of ``out`` (which they keep alive), structures are the
     cached read-only export structures; blocks holding exact zeros are compacted
     like the reference's export (factorize.py:179-192)."""
-    xo, shapes = eng.export
-    t = eng.pool.table
     lb, ub = {}, {}
-    for b in range(eng.pool.nblocks):
-        bi, bj, nr, nc = (int(x) for x in t[:4, b])
-        seg = out[xo[b]:xo[b + 1]]
-        cp, ri, lcp, lrow = shapes[b]
-        z = zero_counts[b] != 0
-        if bi != bj:
-            blk = _drop_zeros(nr, nc, cp, ri, seg) if z else SparseBlock(nr, nc, _ro(cp), _ro(ri), seg)
-            (lb if bi > bj else ub)[(bi, bj)] = blk
-            continue
-        nu = len(ri)
-        uv, lv = seg[:nu], seg[nu:]
-        if z:
-            ub[(bi, bj)] = _drop_zeros(nr, nr, cp, ri, uv)
-            lb[(bi, bj)] = _drop_zeros(nr, nr, lcp, lrow, lv)
+    zb = set(np.flatnonzero(zero_counts).tolist())
+    for b, (key, kind, nr, nc, x0, xs, x1, cp, ri, lcp, lrow) in enumerate(eng.export_recs):
+        if b in zb:
+            if kind == 2:
+                ub[key] = _drop_zeros(nr, nr, cp, ri, out[x0:xs])
+                lb[key] = _drop_zeros(nr, nr, lcp, lrow, out[xs:x1])
+            else:
+                (lb if kind == 0 else ub)[key] = _drop_zeros(nr, nc, cp, ri, out[x0:x1])
+        elif kind == 2:
+            ub[key] = SparseBlock(nr, nr, cp, ri, out[x0:xs])
+            lb[key] = SparseBlock(nr, nr, lcp, lrow, out[xs:x1])
         else:
-            ub[(bi, bj)] = SparseBlock(nr, nr, _ro(cp), _ro(ri), uv)
-            lb[(bi, bj)] = SparseBlock(nr, nr, _ro(lcp), _ro(lrow), lv)
+            (lb if kind == 0 else ub)[key] = SparseBlock(nr, nc, cp, ri, out[x0:x1])
     return LUFactors(n=grid.n, plan=grid.plan, l_blocks=lb, u_blocks=ub, perms=_perm_list(grid, perms_pool))
 
 
@@ -737,8 +741,11 @@ def factorize(grid, tree, workers: int = 1, pivot_tol: float = DEFAULT_PIVOT_TOL
             eng.bind_matrix(a_pos)
             eng.bound_a = a_pos
             eng.a_stage = pinned_empty(len(a_pos))
-        np.take(eng.pool.values, a_pos, out=eng.a_stage)
-        st = eng.refactor_host(eng.a_stage, out, perms, pivot_tol, static_pivot)
+            eng.a_staged_from = None
+        if eng.a_staged_from is not eng.pool.values:  # read-only values: the staged copy stays valid
+            np.take(eng.pool.values, a_pos, out=eng.a_stage)
+            eng.a_staged_from = eng.pool.values
+        st = eng.refactor_host(eng.a_stage, out, perms, pivot_tol, static_pivot)  # H2D of A's values inside
     else:  # foreign (e.g. reference-built) grid: the whole pooled value array
         st = eng.run_host(np.ascontiguousarray(eng.pool.values, dtype=np.float64), out, perms, pivot_tol,
                           static_pivot)

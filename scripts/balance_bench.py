@@ -81,6 +81,8 @@ def main():
     ap.add_argument("--tau", type=float, default=0.1)
     ap.add_argument("--check", action="store_true", help="also solve and report ||Ax-b||/||b||")
     ap.add_argument("--out", default=None, help="JSON lines output")
+    ap.add_argument("--grid", default=None,
+                    help="irregular-plan variants 'steps:max_nums', e.g. 1,2,4:1,3,7 (blocking.py:49-114 knobs)")
     ap.add_argument("--taus", default=None,
                     help="also sweep the density tag on the irregular plan, e.g. 0.05,0.1,0.25,0.5,off")
     args = ap.parse_args()
@@ -95,6 +97,12 @@ def main():
         sizes = [int(x) for x in args.sizes.split(",")] if args.sizes else [b for b in PANGULU_SIZES if b <= a.n]
         plans = [("irregular", M.irregular_plan(curve, a.n))] + [(f"regular_{b}", M.regular_plan(a.n, b))
                                                                  for b in sizes]
+        if args.grid:
+            st_s, mx_s = args.grid.split(":")
+            for stp in (int(x) for x in st_s.split(",")):
+                for mx in (int(x) for x in mx_s.split(",")):
+                    if (stp, mx) != (2, 3):  # the defaults are the "irregular" row
+                        plans.append((f"irregular_s{stp}_m{mx}", M.irregular_plan(curve, a.n, stp, mx)))
         sel = min(M.pangulu_size_select(a.n, f.nnz_filled), a.n)
         if f"regular_{sel}" not in [p[0] for p in plans]:
             plans.append((f"regular_{sel}", M.regular_plan(a.n, sel)))

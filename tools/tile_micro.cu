@@ -87,8 +87,11 @@ int main() {
       cudaDeviceSynchronize();
     }
     cudaMemcpy(h, cyc, sizeof(h), cudaMemcpyDeviceToHost);
-    printf("%-22s %8lld cycles/call (%.2f us at 1.965 GHz)  err=%s\n", names[k], h[0], h[0] / 1965.0,
-           cudaGetErrorString(cudaGetLastError()));
+    double o[256], sum = 0.0;
+    cudaMemcpy(o, out, sizeof(o), cudaMemcpyDeviceToHost);
+    for (int i = 0; i < 256; ++i) sum += o[i] * (1.0 + 1e-3 * i);
+    printf("%-22s %8lld cycles/call (%.2f us at 1.965 GHz)  checksum %.15e err=%s\n", names[k], h[0], h[0] / 1965.0,
+           sum, cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
 }
