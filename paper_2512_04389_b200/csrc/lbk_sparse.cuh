@@ -15,6 +15,12 @@
 namespace lbk {
 
 // C(k,j) -= L(k,i) U(i,j); Gustavson by target column (factorize.py:307-325).
+// Latency hiding: the U entries of a column are read 32 at a time (lane q holds
+// entry e0 + q: its row r, value u and L column bounds Lcp[r], Lcp[r+1], all in
+// one round of loads), and the first 32 L entries of the next nonzero U entry
+// are loaded before the current one is applied, so the warp no longer waits on
+// three dependent global loads per U entry.  Updates into the accumulator are
+// still applied one U entry at a time, in the column's order (deterministic).
 __device__ void ssssm_item(const Item& it, const DevPools& P, double* acc) {
   const BlockDev L = P.blk[it.a], U = P.blk[it.b], C = P.blk[it.c];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -33,13 +39,46 @@ __device__ void ssssm_item(const Item& it, const DevPools& P, double* acc) {
     const int c0 = Ccp[c], c1 = Ccp[c + 1];
     for (int e = c0 + lane; e < c1; e += 32) acc[Cr[e]] = 0.0;
     __syncwarp();
-    for (int e = u0; e < u1; ++e) {
-      const double u = Uv[e];
-      if (u == 0.0) continue;  // exact-zero operand: no contribution (warp-uniform)
-      const int r = Ur[e];
-      const int l0 = Lcp[r], l1 = Lcp[r + 1];
-      for (int f = l0 + lane; f < l1; f += 32) acc[Lr[f]] = fma(Lv[f], u, acc[Lr[f]]);
-      __syncwarp();
+    for (int e0 = u0; e0 < u1; e0 += 32) {
+      const int cnt = min(32, u1 - e0);
+      double mu = 0.0;
+      int ml0 = 0, ml1 = 0;
+      if (lane < cnt) {
+        mu = Uv[e0 + lane];
+        if (mu != 0.0) {  // exact-zero operand: no contribution
+          const int r = Ur[e0 + lane];
+          ml0 = Lcp[r];
+          ml1 = Lcp[r + 1];
+        }
+      }
+      // prefetch registers (pr, pv): the first 32 L entries of the next entry
+      int pr = -1;
+      double pv = 0.0;
+      {
+        const int l0 = __shfl_sync(0xffffffffu, ml0, 0), l1 = __shfl_sync(0xffffffffu, ml1, 0);
+        if (l0 + lane < l1) {
+          pr = Lr[l0 + lane];
+          pv = Lv[l0 + lane];
+        }
+      }
+      for (int q = 0; q < cnt; ++q) {
+        const double u = __shfl_sync(0xffffffffu, mu, q);
+        const int l0 = __shfl_sync(0xffffffffu, ml0, q), l1 = __shfl_sync(0xffffffffu, ml1, q);
+        const int cr = pr;
+        const double cv = pv;
+        // next entry's loads in flight while this one is applied
+        const int qn = q + 1 < cnt ? q + 1 : q;
+        const int n0 = __shfl_sync(0xffffffffu, ml0, qn), n1 = __shfl_sync(0xffffffffu, ml1, qn);
+        pr = -1;
+        if (q + 1 < cnt && n0 + lane < n1) {
+          pr = Lr[n0 + lane];
+          pv = Lv[n0 + lane];
+        }
+        if (u == 0.0) continue;  // warp-uniform
+        if (cr >= 0) acc[cr] = fma(cv, u, acc[cr]);
+        for (int f = l0 + 32 + lane; f < l1; f += 32) acc[Lr[f]] = fma(Lv[f], u, acc[Lr[f]]);
+        __syncwarp();
+      }
     }
     for (int e = c0 + lane; e < c1; e += 32) Cv[e] -= acc[Cr[e]];
     __syncwarp();
@@ -83,16 +122,46 @@ __device__ void gessm_item(const Item& it, const DevPools& P, double* acc) {
         __syncwarp();
       }
     } else {
+      // sparse L_ii: the column bounds of 32 entries per round of loads, the first 32
+      // entries of the next column prefetched while the current one is applied
       const int32_t* dpos = P.diag_csc + D.dg;
-      for (int e = x0; e < x1; ++e) {
-        const int k = Xr[e];
-        const double xk = acc[k];
-        const int f1 = Dcp[k + 1];
-        for (int f = dpos[k] + 1 + lane; f < f1; f += 32) {
-          const int q = Dr[f];
-          acc[q] = dsub_mul(acc[q], Dv[f], xk);
+      for (int e0 = x0; e0 < x1; e0 += 32) {
+        const int cnt = min(32, x1 - e0);
+        int mk = 0, mf0 = 0, mf1 = 0;
+        if (lane < cnt) {
+          mk = Xr[e0 + lane];
+          mf0 = dpos[mk] + 1;
+          mf1 = Dcp[mk + 1];
         }
-        __syncwarp();
+        int pq = -1;
+        double pd = 0.0;
+        {
+          const int f0 = __shfl_sync(0xffffffffu, mf0, 0), f1 = __shfl_sync(0xffffffffu, mf1, 0);
+          if (f0 + lane < f1) {
+            pq = Dr[f0 + lane];
+            pd = Dv[f0 + lane];
+          }
+        }
+        for (int q = 0; q < cnt; ++q) {
+          const int k = __shfl_sync(0xffffffffu, mk, q);
+          const int f0 = __shfl_sync(0xffffffffu, mf0, q), f1 = __shfl_sync(0xffffffffu, mf1, q);
+          const int cq = pq;
+          const double cd = pd;
+          const int qn = q + 1 < cnt ? q + 1 : q;
+          const int n0 = __shfl_sync(0xffffffffu, mf0, qn), n1 = __shfl_sync(0xffffffffu, mf1, qn);
+          pq = -1;
+          if (q + 1 < cnt && n0 + lane < n1) {
+            pq = Dr[n0 + lane];
+            pd = Dv[n0 + lane];
+          }
+          const double xk = acc[k];
+          if (cq >= 0) acc[cq] = dsub_mul(acc[cq], cd, xk);
+          for (int f = f0 + 32 + lane; f < f1; f += 32) {
+            const int r = Dr[f];
+            acc[r] = dsub_mul(acc[r], Dv[f], xk);
+          }
+          __syncwarp();
+        }
       }
     }
     for (int e = x0 + lane; e < x1; e += 32) Xv[e] = acc[Xr[e]];
@@ -134,17 +203,48 @@ __device__ void tstrf_item(const Item& it, const DevPools& P, double* acc) {
       const int32_t* Drp = P.csr_ptr + D.rp;
       const int32_t* Dcc = P.csr_col + D.csr;
       const int32_t* Dcpos = P.csr_pos + D.csr;
-      for (int e = r0; e < r1; ++e) {
-        const int k = Xcc[e];
-        const double xk = __ddiv_rn(acc[k], Dv[Dcsc[k]]);
-        __syncwarp();
-        if (lane == 0) acc[k] = xk;
-        const int g1 = Drp[k + 1];
-        for (int g = Drow[k] + 1 + lane; g < g1; g += 32) {
-          const int j = Dcc[g];
-          acc[j] = dsub_mul(acc[j], xk, Dv[Dcpos[g]]);
+      for (int e0 = r0; e0 < r1; e0 += 32) {
+        const int cnt = min(32, r1 - e0);
+        int mk = 0, mg0 = 0, mg1 = 0;
+        double mdiag = 1.0;
+        if (lane < cnt) {
+          mk = Xcc[e0 + lane];
+          mdiag = Dv[Dcsc[mk]];
+          mg0 = Drow[mk] + 1;
+          mg1 = Drp[mk + 1];
         }
-        __syncwarp();
+        int pj = -1;
+        double pu = 0.0;
+        {
+          const int g0 = __shfl_sync(0xffffffffu, mg0, 0), g1 = __shfl_sync(0xffffffffu, mg1, 0);
+          if (g0 + lane < g1) {
+            pj = Dcc[g0 + lane];
+            pu = Dv[Dcpos[g0 + lane]];
+          }
+        }
+        for (int q = 0; q < cnt; ++q) {
+          const int k = __shfl_sync(0xffffffffu, mk, q);
+          const double dkk = __shfl_sync(0xffffffffu, mdiag, q);
+          const int g0 = __shfl_sync(0xffffffffu, mg0, q), g1 = __shfl_sync(0xffffffffu, mg1, q);
+          const int cj = pj;
+          const double cu = pu;
+          const int qn = q + 1 < cnt ? q + 1 : q;
+          const int n0 = __shfl_sync(0xffffffffu, mg0, qn), n1 = __shfl_sync(0xffffffffu, mg1, qn);
+          pj = -1;
+          if (q + 1 < cnt && n0 + lane < n1) {
+            pj = Dcc[n0 + lane];
+            pu = Dv[Dcpos[n0 + lane]];
+          }
+          const double xk = __ddiv_rn(acc[k], dkk);
+          __syncwarp();
+          if (lane == 0) acc[k] = xk;
+          if (cj >= 0) acc[cj] = dsub_mul(acc[cj], xk, cu);
+          for (int g = g0 + 32 + lane; g < g1; g += 32) {
+            const int j = Dcc[g];
+            acc[j] = dsub_mul(acc[j], xk, Dv[Dcpos[g]]);
+          }
+          __syncwarp();
+        }
       }
     }
     for (int e = r0 + lane; e < r1; e += 32) Xv[Xcpos[e]] = acc[Xcc[e]];

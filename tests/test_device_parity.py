@@ -35,8 +35,11 @@ def stacked(blocks, keys):
             np.concatenate([blocks[k].values for k in keys]))
 
 
+@pytest.mark.parametrize("dt", [0.1, None], ids=["dmma", "csc"])
 @pytest.mark.parametrize("idx", SMALL_IDS)
-def test_small_cases_vs_reference(idx):
+def test_small_cases_vs_reference(idx, dt):
+    """dt=None: every block stays CSC, so the sparse kernels (ssssm/gessm/tstrf/getrf_item,
+    lbk_sparse.cuh) run every task."""
     d = load_small(idx)
     n = int(d["n"])
     a = M.CscMatrix(n, d["a_col_ptr"], d["a_row_idx"], d["a_values"]).check()
@@ -46,10 +49,10 @@ def test_small_cases_vs_reference(idx):
     zp = d["zero_pivot"].tolist()
     if zp != [-1, -1]:
         with pytest.raises(M.ZeroPivot) as ei:
-            M.factorize(g, t, static_pivot=sp_)
+            M.factorize(g, t, static_pivot=sp_, dense_threshold=dt)
         assert [ei.value.block, ei.value.col] == zp
         return
-    f = M.factorize(g, t, static_pivot=sp_)
+    f = M.factorize(g, t, static_pivot=sp_, dense_threshold=dt)
     assert np.array_equal(f.perm_global(), d["perm_global"])
     amax = max(np.abs(d["a_values"]).max(), 1.0)
     for tag, blocks in (("L", f.l_blocks), ("U", f.u_blocks)):
@@ -83,13 +86,27 @@ def pipeline(a, bs=None):
     return g, M.dependency_levels(g)
 
 
+_ORACLE = {}
+
+
+def oracle_export(name, a, g, t):
+    """Every factor value of the oracle's serial run on the same grid (pinned to the reference in
+    tests/test_oracle_golden.py), cached per case."""
+    if name not in _ORACLE:
+        og = OS.Grid(a.n, g.p, g.plan.positions, g.blocks, g.block_nnz, g.value_max)
+        state, _ = ON.factorize(og, t)
+        _ORACLE[name] = ON.export(state)
+    return _ORACLE[name]
+
+
+@pytest.mark.parametrize("dt", [0.1, None], ids=["dmma", "csc"])
 @pytest.mark.parametrize("name", sorted(NAMED))
-def test_named_cases_vs_reference(name):
+def test_named_cases_vs_reference(name, dt):
     rec = CASES[name]
     mk, bs = NAMED[name]
     a = mk()
     g, t = pipeline(a, bs)
-    f = M.factorize(g, t)
+    f = M.factorize(g, t, dense_threshold=dt)
     z = np.load(os.path.join(GOLDEN, f"case_{name}.npz"))
     amax = float(np.abs(a.values).max())
     for tag, blocks in (("L", f.l_blocks), ("U", f.u_blocks)):
@@ -102,6 +119,21 @@ def test_named_cases_vs_reference(name):
         assert np.array_equal(nnz, bk[:, 2])  # identical exported structure per block
         sums = np.array([np.abs(blocks[(int(bi), int(bj))].values).sum() for bi, bj, _ in bk])
         np.testing.assert_allclose(sums, z[tag + "_blocks_abssum"], rtol=1e-10)
+        if tag + "_blocks_proj" in z:  # a +-1 projection of every value of the reference's block
+            w = [np.where(((np.arange(len(blocks[(int(bi), int(bj))].values), dtype=np.uint64)
+                            * np.uint64(0x9E3779B97F4A7C15)) >> np.uint64(40)) & np.uint64(1), 1.0, -1.0)
+                 for bi, bj, _ in bk]
+            proj = np.array([np.dot(wq, blocks[(int(bi), int(bj))].values) for wq, (bi, bj, _) in zip(w, bk)])
+            np.testing.assert_allclose(proj, z[tag + "_blocks_proj"], rtol=1e-9, atol=1e-10 * amax)
+    # all values against the oracle's run on the same grid
+    lb, ub = oracle_export(name, a, g, t)
+    for blocks, ob in ((f.l_blocks, lb), (f.u_blocks, ub)):
+        assert set(blocks) == set(ob)
+        for k, want in ob.items():
+            got = blocks[k]
+            assert np.array_equal(got.row_idx, want.row_idx) and np.array_equal(got.col_ptr, want.col_ptr), k
+            scale = max(float(np.abs(want.values).max(initial=0.0)), 1e-3 * amax)
+            assert float(np.abs(got.values - want.values).max(initial=0.0)) <= 1e-10 * scale, k
     b = a.to_scipy() @ np.ones(a.n)
     x = M.solve(f, b)
     relres = float(np.linalg.norm(a.to_scipy() @ x - b) / np.linalg.norm(b))
