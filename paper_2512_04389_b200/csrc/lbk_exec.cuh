@@ -143,7 +143,7 @@ __device__ __forceinline__ void trail16(const double (&l)[16], int c0, int ce, T
 
 
 #ifndef LBK_TILE_DMMA
-#define LBK_TILE_DMMA 1  // trailing updates inside the tile LU / TRSM routines on the FP64 tensor cores
+#define LBK_TILE_DMMA 0  // 1: trailing updates inside the tile LU / TRSM routines on DMMA (measured slower)
 #endif
 
 // C[r0 + i, c0 + j] -= sum_{k < 16} A[r0 + i + k * lda] * B[k + (c0 + j) * ldb]  (i < nr, j < nc; all in
@@ -156,31 +156,54 @@ __device__ __noinline__ void mma_sub_k16(double* C, int ldc, const double* A, in
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int tr = (nr + 7) >> 3, ntile = tr * ((nc + 7) >> 3);
   if (warp >= ntile) return;
+  // this warp's tiles warp, warp + 8, ...: fragment offsets computed once (-1: outside the range)
+  int oa[8], ob[8];
+  int ti = warp % tr, tj = warp / tr;  // tile coordinates, advanced by 8 tiles per slot
+  const int step_j = 8 / tr, step_i = 8 % tr;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int i = ti * 8 + g, j = tj * 8 + g;
+    const bool live = warp + 8 * q < ntile;
+    oa[q] = live && i < nr ? r0 + i + t * lda : -1;
+    ob[q] = live && j < nc ? t + (c0 + j) * ldb : -1;
+    ti += step_i;
+    tj += step_j;
+    if (ti >= tr) {
+      ti -= tr;
+      ++tj;
+    }
+  }
   double acc[8][2];
 #pragma unroll
   for (int q = 0; q < 8; ++q) acc[q][0] = acc[q][1] = 0.0;
+  const int nq = (ntile - warp + 7) >> 3;  // tiles of this warp (warp-uniform)
 #pragma unroll
   for (int k4 = 0; k4 < 16; k4 += 4) {
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const int tile = warp + 8 * q;
-      if (tile < ntile) {  // warp-uniform
-        const int i = (tile % tr) * 8 + g, j = (tile / tr) * 8 + g;
-        const double a = i < nr ? A[r0 + i + (k4 + t) * lda] : 0.0;
-        const double b = j < nc ? B[k4 + t + (c0 + j) * ldb] : 0.0;
+      if (q < nq) {
+        const double a = oa[q] >= 0 ? A[oa[q] + k4 * lda] : 0.0;
+        const double b = ob[q] >= 0 ? B[ob[q] + k4] : 0.0;
         dmma(acc[q][0], acc[q][1], a, b);
       }
     }
   }
+  ti = warp % tr;
+  tj = warp / tr;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    const int tile = warp + 8 * q;
-    if (tile < ntile) {
-      const int i = (tile % tr) * 8 + g, j = (tile / tr) * 8 + 2 * t;
+    if (q < nq) {
+      const int i = ti * 8 + g, j = tj * 8 + 2 * t;
       if (i < nr) {
         if (j < nc) C[r0 + i + (c0 + j) * ldc] -= acc[q][0];
         if (j + 1 < nc) C[r0 + i + (c0 + j + 1) * ldc] -= acc[q][1];
       }
+    }
+    ti += step_i;
+    tj += step_j;
+    if (ti >= tr) {
+      ti -= tr;
+      ++tj;
     }
   }
 }
@@ -284,6 +307,55 @@ __device__ void tile_left_solve_blk(double* X, const double* Lm, int nr) {
   }
 }
 
+
+#ifndef LBK_PANEL4
+#define LBK_PANEL4 0  // 1: tile-LU panels on 4 warps, 2 threads per row (measured slower)
+#endif
+
+// Panel [pb, pb + 16) of the n x n tile T (smem, XTP) factored by threads 0..127:
+// thread (row r = t / 2, half h = t % 2) keeps the row's 16 panel entries in
+// registers and updates the 8 columns of its half, plus column jj + 1 (the next
+// multiplier's operand, so both threads of a pair hold it); the pivot row is
+// published through a double-buffered shared row (prow[2][16]) and one 128-thread
+// named barrier per column.  Same arithmetic per entry as the one-warp panel
+// (l = d * rcp_nr(u), fma updates in column order), a quarter of its issue per warp.
+__device__ __forceinline__ void bar_panel() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+__device__ __noinline__ void panel16_4w(double* T, int pb, int n, double* Dd, double* prow) {
+  constexpr int PB = 16;
+  const int tid = threadIdx.x, r = tid >> 1, h = tid & 1;
+  double x[PB];
+#pragma unroll
+  for (int i = 0; i < PB; ++i) x[i] = T[(pb + i) * XTP + r];
+#pragma unroll
+  for (int jj = 0; jj < PB; ++jj) {
+    const int j = pb + jj;
+    if (j >= n) break;
+    double* pr = prow + (jj & 1) * PB;
+    if (r == j) {  // the pivot row's pair publishes its current entries (column jj from both)
+#pragma unroll
+      for (int i = jj; i < PB; ++i)
+        if (i == jj || (i >> 3) == h) pr[i] = x[i];
+    }
+    bar_panel();
+    const double rinv = rcp_nr(pr[jj]);
+    if (r > j && r < n) {
+      const double d = x[jj];
+      if (h == 0) Dd[j * XTP + r] = fabs(d);
+      const double l = d * rinv;
+      x[jj] = l;
+#pragma unroll
+      for (int i = jj + 1; i < PB; ++i)
+        if ((i >> 3) == h || i == jj + 1) x[i] = fma(-l, pr[i], x[i]);
+    }
+  }
+  if (r >= pb && r < n) {
+#pragma unroll
+    for (int i = 0; i < PB; ++i)
+      if ((i >> 3) == h) T[(pb + i) * XTP + r] = x[i];
+  }
+}
+
 // LU (no exchange) of the n x n (n <= 64) tile in smem T (column-major, XTP
 // stride), blocked by 16-column panels.  Per panel: (1) the 64 x 16 panel is
 // factored by threads 0..63 (thread r holds row r's 16 panel entries in
@@ -295,10 +367,12 @@ __device__ void tile_left_solve_blk(double* X, const double* Lm, int nr) {
 __device__ void tile_lu64_blocked(double* T, int n, double* Dd, double* urow, long long* prof = nullptr) {
   const int tid = threadIdx.x;
   constexpr int PB = 16;
-  (void)urow;
   long long t0 = prof ? clock64() : 0;
 #pragma unroll 1
   for (int pb = 0; pb < n; pb += PB) {
+#if LBK_PANEL4
+    if (tid < 128) panel16_4w(T, pb, n, Dd, urow);
+#else
     if (tid < 32) {
       // warp 0 holds rows lane and lane + 32 of the panel; the pivot row is
       // broadcast with shuffles (no barrier), every lane forms 1/u_jj itself
@@ -343,6 +417,7 @@ __device__ void tile_lu64_blocked(double* T, int n, double* Dd, double* urow, lo
         if (rb >= pb) T[(pb + i) * XTP + rb] = pc[i];
       }
     }
+#endif
     if (prof) { __syncthreads(); const long long t1 = clock64(); if (tid == 0) prof[0] += t1 - t0; t0 = t1; }
     __syncthreads();
     const int pe = min(n, pb + PB);
