@@ -236,6 +236,7 @@ struct lbk_ctx {
   std::vector<int32_t> blk_final_tl;  // tree level of the task that finishes each block
 
   std::vector<int64_t> ref_off, ref_len;  // reference pool range of each block
+  std::vector<char> resident;             // block has working storage on this rank
   // output layout (lbk_set_export): entries nout, per-block range, omap[x] = working
   // position of output entry x (-1: a constant 1.0, the unit diagonal of L)
   int64_t nout = 0;
@@ -571,6 +572,28 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     if (!c->mask.empty() && static_cast<int64_t>(c->mask.size()) != ntasks)
       return fail(st, LBK_ERR_DIM_MISMATCH, "task mask length differs from the task count");
     std::vector<std::vector<int32_t>> Rl(nb), Cl(nb);
+    // distributed plans (task mask): working storage only for the blocks this rank's
+    // tasks write or read (owned blocks + received operands); other blocks get none
+    // and their pool entries map to -2 (skipped by the scatter, zero in the output)
+    std::vector<char> resident(nb, c->mask.empty() ? 1 : 0);
+    if (!c->mask.empty()) {
+      auto mark = [&](int64_t bi, int64_t bj) {
+        if (bi >= 0 && bj >= 0 && bid[bi * p + bj] >= 0) resident[bid[bi * p + bj]] = 1;
+      };
+      for (int64_t t = 0; t < ntasks; ++t) {
+        if (!c->mask[t]) continue;
+        const int64_t i = steps[t], r = trows[t], cc = tcols[t];
+        mark(i, i);
+        if (kinds[t] == KIND_GESSM) mark(i, cc);
+        else if (kinds[t] == KIND_TSTRF) mark(r, i);
+        else if (kinds[t] == KIND_SSSSM) {
+          mark(r, i);
+          mark(i, cc);
+          mark(r, cc);
+        }
+      }
+    }
+    c->resident.assign(resident.begin(), resident.end());
     int64_t nnz = 0, nnz_w = 0, ncp = 0;
     for (int64_t b = 0; b < nb; ++b) {
       BlockDev& d = hb[b];
@@ -619,9 +642,9 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       }
       d.cp = ncp;
       d.ent = nnz_w;
-      c->wlen[b] = store == STORE_SPARSE ? nzb : static_cast<int64_t>(d.nR) * d.nC;
+      c->wlen[b] = !resident[b] ? 0 : store == STORE_SPARSE ? nzb : static_cast<int64_t>(d.nR) * d.nC;
       ncp += d.ncols + 1;
-      nnz_w += store == STORE_SPARSE ? nzb : static_cast<int64_t>(d.nR) * d.nC;
+      nnz_w += c->wlen[b];
       c->store_count[store]++;
     }
     c->nnz = nnz;
@@ -640,9 +663,12 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       const int64_t nzb = T_nz[b];
       const int64_t eo = T_ent[b];  // index into the reference pool (A values, factor output)
       int32_t* cp = &hcp[d.cp];
+      const bool res = resident[b];
+      if (!res)
+        for (int64_t e = 0; e < nzb; ++e) hmap[eo + e] = -2;  // no storage on this rank
       if (d.store == STORE_SPARSE) {
         for (int k = 0; k <= d.ncols; ++k) cp[k] = static_cast<int32_t>(scp[k]);
-        for (int64_t e = 0; e < nzb; ++e) {
+        for (int64_t e = 0; res && e < nzb; ++e) {
           hrows[d.ent + e] = static_cast<int32_t>(sri[e]);
           hmap[eo + e] = d.ent + e;
         }
@@ -664,9 +690,9 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           }
       } else if (d.store == STORE_FULL) {
         for (int k = 0; k <= d.ncols; ++k) cp[k] = k * d.nrows;
-        for (int col = 0; col < d.ncols; ++col)
+        for (int col = 0; res && col < d.ncols; ++col)
           for (int r = 0; r < d.nrows; ++r) hrows[d.ent + static_cast<int64_t>(col) * d.nrows + r] = r;
-        for (int col = 0; col < d.ncols; ++col)
+        for (int col = 0; res && col < d.ncols; ++col)
           for (int64_t e = scp[col]; e < scp[col + 1]; ++e)
             hmap[eo + e] = d.ent + static_cast<int64_t>(col) * d.nrows + sri[e];
       } else {
@@ -683,12 +709,12 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         for (int col = 0; col < d.ncols; ++col) {
           cp[col] = acc;
           if (cpos[col] >= 0) {
-            for (int a = 0; a < d.nR; ++a) hrows[d.ent + acc + a] = R[a];
+            for (int a = 0; res && a < d.nR; ++a) hrows[d.ent + acc + a] = R[a];
             acc += d.nR;
           }
         }
         cp[d.ncols] = acc;
-        for (int col = 0; col < d.ncols; ++col)
+        for (int col = 0; res && col < d.ncols; ++col)
           for (int64_t e = scp[col]; e < scp[col + 1]; ++e)
             hmap[eo + e] = d.ent + static_cast<int64_t>(cpos[col]) * d.nR + rpos[sri[e]];
       }

@@ -354,7 +354,8 @@ __global__ void scatter_kernel(const double* __restrict__ in, const int64_t* __r
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const double v = in[e];
     bad |= !isfinite(v);
-    work[map[e]] = v;
+    const int64_t m = map[e];
+    if (m >= 0) work[m] = v;  // -2: block without storage on this rank (distributed plans)
   }
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *nonfinite = 1;
 }
@@ -387,7 +388,7 @@ __global__ void range_gather_kernel(const double* __restrict__ work, const int64
     const int64_t off = ranges[2 * q], len = ranges[2 * q + 1];
     for (int64_t e = threadIdx.x; e < len; e += blockDim.x) {
       const int64_t m = map[off + e];
-      out[off + e] = m >= 0 ? work[m] : 1.0;  // -1: unit diagonal of an exported L block
+      out[off + e] = m >= 0 ? work[m] : (m == -1 ? 1.0 : 0.0);  // -1: unit diagonal of an exported L block
     }
   }
 }
@@ -405,7 +406,7 @@ __global__ void gather_kernel(const double* __restrict__ work, const int64_t* __
   for (int64_t e = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; e < n;
        e += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t m = map[e];
-    out[e] = m >= 0 ? work[m] : 1.0;
+    out[e] = m >= 0 ? work[m] : (m == -1 ? 1.0 : 0.0);  // -2: no storage on this rank
   }
 }
 
@@ -415,7 +416,7 @@ __global__ void compose_map_kernel(const int64_t* __restrict__ xref, const int64
   for (int64_t x = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; x < n;
        x += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t r = xref[x];
-    omap[x] = r < 0 ? -1 : map[r];
+    omap[x] = r < 0 ? -1 : map[r];  // (map -2 stays -2)
   }
 }
 

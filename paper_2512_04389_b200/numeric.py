@@ -26,7 +26,7 @@ from scipy.sparse.linalg import spsolve_triangular
 
 from . import _native
 from .blocking import BlockingPlan
-from .errors import DeviceError, DimensionMismatch, ZeroPivot
+from .errors import DeviceError, DimensionMismatch, SupportViolation, ZeroPivot
 from .grid import GESSM, GETRF, SSSSM, TSTRF, GridPool, SparseBlock, pool_grid
 from .matrix_io import CscMatrix
 
@@ -689,6 +689,59 @@ def build_factors_full(grid, pool: GridPool, work: np.ndarray, perms_pool: np.nd
     return LUFactors(n=grid.n, plan=grid.plan, l_blocks=lb, u_blocks=ub, perms=f.perms)
 
 
+def check_support(grid, tree) -> None:
+    """The reference's support checks (factorize.py:277-324), structurally, once per grid.
+
+    The reference raises SupportViolation when an SSSSM product is nonzero outside the
+    target block's filled support (or hits an absent block).  A grid built by this
+    package's ``partition`` is elimination-closed by construction (grid.py:3-5), so no
+    product can leave the support.  For any other grid (e.g. hand-made), the union of
+    the block patterns is checked for closure with the native symbolic factorization;
+    only if it is not closed are the products walked in construction order, and the
+    first one whose STRUCTURAL support leaves its target raises, with the reference's
+    message.  (The reference tests the numeric product, so it would stay silent on an
+    exact cancellation, and it stops checking after the first row swap.)"""
+    if getattr(grid, "a_pos", None) is not None or getattr(grid, "_lbk_support_ok", False):
+        return
+    from .symbolic import symbolic_factorize, symmetrize_pattern
+
+    pool = pool_grid(grid)
+    t = pool.table
+    pos = np.asarray(grid.plan.positions, np.int64)
+    nc = t[3]
+    cols_local = np.concatenate([np.repeat(np.arange(int(c)), np.diff(pool.col_ptr[int(o):int(o) + int(c) + 1]))
+                                 for c, o in zip(nc, t[5])]) if t.shape[1] else np.zeros(0, np.int64)
+    r = pool.row_idx + np.repeat(pos[t[0]], t[4])
+    c = cols_local + np.repeat(pos[t[1]], t[4])
+    m = sp.coo_matrix((np.ones(len(r)), (r, c)), shape=(grid.n, grid.n)).tocsc()
+    m.sum_duplicates()
+    a = CscMatrix(grid.n, m.indptr.astype(np.int64), m.indices.astype(np.int64), m.data)
+    closed = False
+    try:
+        closed = symbolic_factorize(symmetrize_pattern(a)).nnz_filled == a.nnz
+    except Exception:
+        closed = False
+    if not closed:
+        def pat(key):
+            b = grid.blocks[key]
+            return sp.csc_matrix((np.ones(b.nnz), np.asarray(b.row_idx), np.asarray(b.col_ptr)),
+                                 shape=(b.nrows, b.ncols))
+        for q in np.flatnonzero(np.asarray(tree.kinds) == SSSSM):
+            i, rr, cc = int(tree.steps[q]), int(tree.rows[q]), int(tree.cols[q])
+            prod = (pat((rr, i)) @ pat((i, cc))).tocoo()
+            if (rr, cc) not in grid.blocks:
+                if prod.nnz:
+                    raise SupportViolation(f"update from step {i} hits empty block ({rr}, {cc})")
+                continue
+            tgt = pat((rr, cc)).tocsr()
+            if np.any(np.asarray(tgt[prod.row, prod.col]).ravel() == 0):
+                raise SupportViolation(f"update from step {i} writes outside filled support of block ({rr}, {cc})")
+    try:
+        grid._lbk_support_ok = True
+    except AttributeError:
+        pass
+
+
 def engine_for(grid, tree, *, device: int = 0, dense: bool = False, chunk: int = DEFAULT_CHUNK,
                dense_threshold: float | None = DEFAULT_DENSE_THRESHOLD) -> Engine:
     """Cached device plan of (grid, tree); dense=True uses full-rectangle blocks everywhere.
@@ -729,6 +782,7 @@ def factorize(grid, tree, workers: int = 1, pivot_tol: float = DEFAULT_PIVOT_TOL
     """
     if workers < 1:
         raise DimensionMismatch(f"workers must be >= 1, got {workers}")
+    check_support(grid, tree)
     eng = engine_for(grid, tree, device=device, dense=False, chunk=chunk, dense_threshold=dense_threshold)
     eng.enable_export()
     out = pinned_recycled(eng.nout)

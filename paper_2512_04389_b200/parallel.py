@@ -327,13 +327,23 @@ class DistEngine:
         return v, pv
 
     def gather_work(self):
-        """Working-layout values assembled from every rank's owned blocks (dense-scratch mode)."""
+        """Dense-scratch values (every block a full tile, pool block order, the layout
+        ``build_factors_full`` reads) assembled from every rank's owned blocks.  Each rank's
+        working pool only holds its resident blocks (compacted offsets), so the owned tiles
+        are first placed at their offsets in the common full-tile layout."""
         w = self.eng.download_work()
         lay = self.eng.block_layout()
-        m = np.zeros(len(w), bool)
+        t = self.eng.pool.table
+        size = t[2] * t[3]
+        off = np.concatenate([[0], np.cumsum(size)])
+        out = np.zeros(int(off[-1]), np.float64)
         for b in np.flatnonzero(self.owned_block):
-            m[lay[0, b]:lay[0, b] + lay[1, b]] = True
-        return self._allreduce(self.torch.from_numpy(np.where(m, w, 0.0)), "sum").numpy()
+            out[off[b]:off[b + 1]] = w[lay[0, b]:lay[0, b] + lay[1, b]]
+        return self._allreduce(self.torch.from_numpy(out), "sum").numpy()
+
+    def pool_entries(self) -> int:
+        """Working-pool entries this rank allocates (owned blocks + received operands)."""
+        return int(self.eng.nnz_work)
 
     def close(self):
         self.eng.close()

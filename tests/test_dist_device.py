@@ -75,8 +75,8 @@ def _worker(rank, world, port, name, out_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,name", [(2, "p3d"), (4, "p3d"), (2, "bbd"), (4, "p2reg"), (2, "small15"),
-                                        (2, "small21"), (2, "small19")])
+@pytest.mark.parametrize("world,name", [(2, "p3d"), (4, "p3d"), (8, "p3d"), (2, "bbd"), (8, "bbd"), (4, "p2reg"),
+                                        (2, "small15"), (2, "small21"), (2, "small19")])
 def test_distributed_factors_bitwise_equal_to_single_gpu(tmp_path, world, name):
     mp.spawn(_worker, args=(world, _free_port(), name, str(tmp_path)), nprocs=world, join=True)
     g, t, sp = _case(name)
@@ -110,6 +110,21 @@ def test_distributed_plan_splits_work_and_segments():
     assert np.array_equal(r0[own == 0], rf[own == 0])
     assert e0.n_segments == int(cuts.sum()) + 1
     lay = e0.block_layout()
-    assert np.all(lay[1] > 0) and np.all(np.diff(lay[0]) >= 0)
+    assert np.all(np.diff(lay[0]) >= 0)
+    # working storage only for the blocks rank 0's tasks touch: its owned blocks + received operands
+    touched = set()
+    for q in np.flatnonzero(own == 0):
+        i, r, c, k = int(t.steps[q]), int(t.rows[q]), int(t.cols[q]), int(t.kinds[q])
+        touched.add((i, i))
+        if k == M.GESSM:
+            touched.add((i, c))
+        elif k == M.TSTRF:
+            touched.add((r, i))
+        elif k == M.SSSSM:
+            touched.update({(r, i), (i, c), (r, c)})
+    keys = list(zip(e0.pool.table[0], e0.pool.table[1]))
+    res = np.array([(int(bi), int(bj)) in touched for bi, bj in keys])
+    assert np.all(lay[1][res] > 0) and np.all(lay[1][~res] == 0)
+    assert e0.nnz_work < full.nnz_work
     e0.close()
     full.close()

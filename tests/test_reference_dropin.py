@@ -82,6 +82,16 @@ def test_reference_built_grid_all_values(family, size, plan):
 
 
 @pytest.mark.skipif(L is None, reason="baseline/_ref (the reference install) is not present")
+def test_dense_blas_flag_matches_reference_lapack_path():
+    """dense_blas=True (LAPACK getrf / trsm on >= 50 % dense blocks, factorize.py:271-275, 331-343):
+    same factors within rounding as the reference's own dense_blas run."""
+    a, grid, tree = ref_objects("poisson2d", 24, plan=48)
+    ref = L.factorize(grid, tree, dense_blas=True)
+    ours = M.factorize(grid, tree, dense_blas=True)
+    compare(ref, ours, 1e-3 * float(np.abs(a.values).max()))
+
+
+@pytest.mark.skipif(L is None, reason="baseline/_ref (the reference install) is not present")
 def test_reference_built_grid_with_row_swaps():
     """Non-dominant values: block-local pivoting swaps rows (the reference's quirk of
     leaving L blocks unpermuted, factorize.py:326-331, reproduced)."""
@@ -107,6 +117,13 @@ def test_reference_built_grid_zero_pivot_and_static_pivot():
     with pytest.raises(M.ZeroPivot) as got:
         M.factorize(grid, tree)
     assert (got.value.block, got.value.col) == (want.value.block, want.value.col)
+    # dense_blas=True: the reference's LAPACK path (factorize.py:81-95) checks the same |u_kk| against
+    # tol * colmax-at-entry after the fact and raises the lowest failing column
+    with pytest.raises(L.ZeroPivot) as want_b:
+        L.factorize(grid, tree, dense_blas=True)
+    with pytest.raises(M.ZeroPivot) as got_b:
+        M.factorize(grid, tree, dense_blas=True)
+    assert (got_b.value.block, got_b.value.col) == (want_b.value.block, want_b.value.col)
     ref = L.factorize(grid, tree, static_pivot=1e-8)
     ours = M.factorize(grid, tree, static_pivot=1e-8)
     compare(ref, ours, 1e-3)
