@@ -107,7 +107,12 @@ void lbk_destroy(lbk_ctx* ctx);
  *   rectangle holds >= tau of its entries becomes a compressed dense tile
  *   (SSSSM/GESSM/TSTRF on FP64 tensor cores); other blocks stay CSC;
  * flags bit 1: dense-scratch mode — every block a full tile, true row swaps
- *   (the reference's dense scratch, factorize.py:265). */
+ *   (the reference's dense scratch, factorize.py:265);
+ * flags bit 2: segment-refined levels — banded diagonal blocks are swept per
+ *   independent segment, and updates into them, their sweeps and the panels
+ *   reading them wait only for the segments involved (the reference's block
+ *   DAG, grid.py:223-378, refined; bitwise the same factors).  Such a plan
+ *   rejects static pivoting (LBK_ERR_BAD_ARG): plan without bit 2 for it. */
 int lbk_plan(lbk_ctx* ctx, int64_t n, int64_t p, const int64_t* positions, int64_t nblocks,
              const int64_t* table, const int64_t* col_ptr, const int64_t* row_idx, int64_t ntasks,
              const int8_t* kinds, const int32_t* steps, const int32_t* rows, const int32_t* cols,

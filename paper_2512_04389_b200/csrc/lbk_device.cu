@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "../../include/lbk.h"
+#include <limits>
 #include <map>
 
 #include "lbk_common.cuh"
@@ -237,6 +238,7 @@ struct lbk_ctx {
 
   std::vector<int64_t> ref_off, ref_len;  // reference pool range of each block
   std::vector<char> resident;             // block has working storage on this rank
+  bool refined = false;                   // segment-refined levels (lbk_plan flags bit 2)
   // output layout (lbk_set_export): entries nout, per-block range, omap[x] = working
   // position of output entry x (-1: a constant 1.0, the unit diagonal of L)
   int64_t nout = 0;
@@ -562,7 +564,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       if (kinds[t] == KIND_GETRF) fb = bid[i * p + i];
       else if (kinds[t] == KIND_GESSM) fb = bid[i * p + tcols[t]];
       else if (kinds[t] == KIND_TSTRF) fb = bid[trows[t] * p + i];
-      if (fb >= 0) c->blk_final_tl[fb] = tlevels[t];
+      if (fb >= 0) c->blk_final_tl[fb] = tlevels[t];  // (refined plans: reset below)
     }
 
     c->dext.clear();
@@ -796,9 +798,183 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       for (int r = 0; r < d.ncols; ++r) v[r] = r;
       return v;
     };
+    // ---- banded diagonal blocks: independent segments --------------------------------
+    // A FULL diagonal block whose filled pattern lies in a band <= BAND_MAX is swept
+    // segment by segment (X_BAND); a segment boundary at s when no entry couples
+    // [.., s) with [s, ..) (block-diagonal bodies inside one block), segments >= 64.
+    struct BandInfo {
+      int bl = 0, bu = 0;
+      std::vector<std::pair<int32_t, int32_t>> seg;  // [s0, s1)
+      std::vector<int32_t> segof;                    // local index -> segment
+      std::vector<int32_t> lev;                      // refined launch level of each segment
+    };
+    std::map<int64_t, BandInfo> band;
+    if (!all_full && dense_on && c->use_exec)
+      for (int64_t b = 0; b < nb; ++b) {
+        const int m = static_cast<int>(T_nr[b]);
+        if (T_bi[b] != T_bj[b] || hb[b].store != STORE_FULL || m <= 2 * XT || m > 32767) continue;
+        int bl = 0, bu = 0;
+        const int64_t* scp = colptr + T_cp[b];
+        const int64_t* sri = rowidx + T_ent[b];
+        for (int col = 0; col < m; ++col)
+          for (int64_t e = scp[col]; e < scp[col + 1]; ++e) {
+            const int r = static_cast<int>(sri[e]);
+            bl = std::max(bl, r - col);
+            bu = std::max(bu, col - r);
+          }
+        if (bl > BAND_MAX || bu > BAND_MAX) continue;
+        BandInfo bi;
+        bi.bl = bl;
+        bi.bu = bu;
+        std::vector<int> lo(m, m);  // lowest row/col index coupled to index x from the other side
+        for (int col = 0; col < m; ++col)
+          for (int64_t e = scp[col]; e < scp[col + 1]; ++e) {
+            const int r = static_cast<int>(sri[e]);
+            lo[std::max(r, col)] = std::min(lo[std::max(r, col)], std::min(r, col));
+          }
+        std::vector<int> sufmin(m + 1, m);
+        for (int x = m - 1; x >= 0; --x) sufmin[x] = std::min(sufmin[x + 1], lo[x]);
+        bi.segof.assign(m, 0);
+        int s0 = 0;
+        for (int s1 = 1; s1 <= m; ++s1)
+          if (s1 == m || (sufmin[s1] >= s1 && s1 - s0 >= 64)) {
+            for (int x = s0; x < s1; ++x) bi.segof[x] = static_cast<int32_t>(bi.seg.size());
+            bi.seg.push_back({s0, s1});
+            s0 = s1;
+          }
+        bi.lev.assign(bi.seg.size(), -1);
+        band.emplace(b, std::move(bi));
+      }
+    // ---- refined ASAP levels ----------------------------------------------------------
+    // The reference's DAG (grid.py:223-378) orders whole blocks.  Inside a banded
+    // diagonal block the segments are independent sub-LUs, so: an update into the block
+    // waits only for the last update into the segments its product rows reach, each
+    // segment's sweep only for those updates, and a panel (GESSM / TSTRF) only for the
+    // segments its rows / columns read.  Every per-entry operation order is unchanged
+    // (the ascending-step chain is kept per segment), so the factors are bitwise the same;
+    // the chain of coupled band blocks of a bordered-block-diagonal matrix falls apart into
+    // short per-body chains.  Off for distributed plans (their cuts follow tree levels),
+    // static pivoting (the exact single-CTA GETRF factors whole blocks) and the tile path.
+    const bool refine = (flags & 4) != 0 && c->mask.empty() && c->use_exec && !all_full && !band.empty() &&
+                        std::getenv("LBK_NO_REFINE") == nullptr;
+    std::vector<int32_t> rlev(tlevels, tlevels + ntasks);
+    std::vector<int8_t> rdefer;
+    c->refined = refine;
+    if (refine) {
+      constexpr int32_t NONE = std::numeric_limits<int32_t>::max();
+      std::vector<int32_t> lastlv(nb, -1), lastid(nb, -1), minsucc(ntasks, NONE);
+      std::map<int64_t, std::vector<int32_t>> slastlv, slastid;
+      for (auto& kv : band) {
+        slastlv[kv.first].assign(kv.second.seg.size(), -1);
+        slastid[kv.first].assign(kv.second.seg.size(), -1);
+      }
+      std::vector<int32_t> getrf_of(p, -1), gessm_of(p, -1), tstrf_of(p, -1);
+      auto pred = [&](int32_t& lvl, int32_t plv, int32_t pid, std::vector<int32_t>& ps) {
+        lvl = std::max(lvl, plv + 1);
+        if (pid >= 0) ps.push_back(pid);
+      };
+      // segments of band block d reached by the rows (rows = true) / columns of block x
+      auto segs_of = [&](int64_t d, int64_t x, bool rows_dim) {
+        const BandInfo& bi = band.at(d);
+        std::vector<char> hit(bi.seg.size(), 0);
+        const int64_t* scp = colptr + T_cp[x];
+        const int64_t* sri = rowidx + T_ent[x];
+        if (rows_dim) {
+          for (int64_t e = 0; e < T_nz[x]; ++e) hit[bi.segof[sri[e]]] = 1;
+        } else {
+          for (int col = 0; col < T_nc[x]; ++col)
+            if (scp[col + 1] > scp[col]) hit[bi.segof[col]] = 1;
+        }
+        return hit;
+      };
+      std::vector<int32_t> ps;
+      for (int64_t t = 0; t < ntasks; ++t) {
+        const int kind = kinds[t];
+        const int64_t i = steps[t], r = trows[t], cc = tcols[t];
+        const int64_t d = bid[i * p + i];
+        const bool dband = band.count(d) != 0;
+        int32_t lvl = 0;
+        ps.clear();
+        if (kind == KIND_GETRF) {
+          getrf_of[i] = static_cast<int32_t>(t);
+          if (dband) {
+            BandInfo& bi = band.at(d);
+            auto& sl = slastlv[d];
+            auto& si = slastid[d];
+            for (size_t q = 0; q < bi.seg.size(); ++q) {
+              bi.lev[q] = sl[q] + 1;
+              if (si[q] >= 0) minsucc[si[q]] = std::min(minsucc[si[q]], bi.lev[q]);
+              lvl = std::max(lvl, bi.lev[q]);
+            }
+          } else {
+            pred(lvl, lastlv[d], lastid[d], ps);
+          }
+        } else if (kind == KIND_GESSM || kind == KIND_TSTRF) {
+          const int64_t x = kind == KIND_GESSM ? bid[i * p + cc] : bid[r * p + i];
+          if (kind == KIND_GESSM) gessm_of[cc] = static_cast<int32_t>(t);
+          else tstrf_of[r] = static_cast<int32_t>(t);
+          if (dband) {
+            const std::vector<char> hit = segs_of(d, x, kind == KIND_GESSM);
+            const BandInfo& bi = band.at(d);
+            for (size_t q = 0; q < hit.size(); ++q)
+              if (hit[q]) lvl = std::max(lvl, bi.lev[q] + 1);
+          } else {
+            lvl = std::max(lvl, rlev[getrf_of[i]] + 1);
+          }
+          pred(lvl, lastlv[x], lastid[x], ps);
+        } else {  // SSSSM(r, cc, i)
+          const int64_t tgt = bid[r * p + cc];
+          if (tgt < 0 || costs[t] == 0) {  // skipped at run time (zero work): not a writer
+            rlev[t] = 0;
+            continue;
+          }
+          lvl = std::max(rlev[tstrf_of[r]], rlev[gessm_of[cc]]) + 1;
+          if (band.count(tgt)) {
+            const std::vector<char> hit = segs_of(tgt, bid[r * p + i], true);  // product rows = L's rows
+            auto& sl = slastlv[tgt];
+            auto& si = slastid[tgt];
+            for (size_t q = 0; q < hit.size(); ++q)
+              if (hit[q]) pred(lvl, sl[q], si[q], ps);
+            for (int32_t pid : ps) minsucc[pid] = std::min(minsucc[pid], lvl);
+            for (size_t q = 0; q < hit.size(); ++q)
+              if (hit[q]) {
+                sl[q] = lvl;
+                si[q] = static_cast<int32_t>(t);
+              }
+            rlev[t] = lvl;
+            continue;
+          }
+          pred(lvl, lastlv[tgt], lastid[tgt], ps);
+          lastlv[tgt] = lvl;
+          for (int32_t pid : ps) minsucc[pid] = std::min(minsucc[pid], lvl);
+          lastid[tgt] = static_cast<int32_t>(t);
+          rlev[t] = lvl;
+          continue;
+        }
+        for (int32_t pid : ps) minsucc[pid] = std::min(minsucc[pid], lvl);
+        rlev[t] = lvl;
+      }
+      // lookahead slack of the updates under the refined levels (numeric.defer_flags semantics)
+      rdefer.assign(ntasks, 0);
+      for (int64_t t = 0; t < ntasks; ++t)
+        if (kinds[t] == KIND_SSSSM && minsucc[t] != NONE)
+          rdefer[t] = static_cast<int8_t>(std::clamp(minsucc[t] - rlev[t], 0, 100));
+    }
+    const int32_t* tlev = rlev.data();
+    if (refine)  // the level after which each block is final (streamed output)
+      for (int64_t t = 0; t < ntasks; ++t) {
+        const int64_t i = steps[t];
+        int64_t fb = -1;
+        if (kinds[t] == KIND_GETRF) fb = bid[i * p + i];
+        else if (kinds[t] == KIND_GESSM) fb = bid[i * p + tcols[t]];
+        else if (kinds[t] == KIND_TSTRF) fb = bid[trows[t] * p + i];
+        if (fb >= 0) c->blk_final_tl[fb] = tlev[t];
+      }
     // ---- per-level work lists ------------------------------------------------------
     int32_t nlevels = 0;
-    for (int64_t t = 0; t < ntasks; ++t) nlevels = std::max(nlevels, tlevels[t] + 1);
+    for (int64_t t = 0; t < ntasks; ++t) nlevels = std::max(nlevels, tlev[t] + 1);
+    for (auto& kv : band)
+      for (int32_t l : kv.second.lev) nlevels = std::max(nlevels, l + 1);
     std::vector<std::vector<Item>> gen(nlevels);
     std::vector<int32_t> acc_len(nlevels, 1);
     std::vector<std::vector<GemmItem>> gem(nlevels), gemD(nlevels), gemE(nlevels);
@@ -907,15 +1083,23 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       if (!c->mask.empty() && !c->mask[t]) continue;  // another rank's task (owner-computes)
       const int kind = kinds[t];
       const int64_t i = steps[t], r = trows[t], cc = tcols[t];
-      const int32_t lv = tlevels[t];
+      const int32_t lv = tlev[t];
       const int64_t dblk = bid[i * p + i];
       Item it{};
       it.kind = kind;
       if (kind == KIND_GETRF) {
         if (hb[dblk].store == STORE_FULL) {
           // tiled multi-CTA GETRF (no-swap speculation, verified); the exact
-          // single-CTA variant is kept for dense-scratch / static pivoting
-          tgetrf[lv].push_back(dblk);
+          // single-CTA variant is kept for dense-scratch / static pivoting.
+          // Refined band blocks: listed at every level holding one of their segments.
+          if (refine && band.count(dblk)) {
+            std::vector<int32_t> ls = band.at(dblk).lev;
+            std::sort(ls.begin(), ls.end());
+            ls.erase(std::unique(ls.begin(), ls.end()), ls.end());
+            for (int32_t l : ls) tgetrf[l].push_back(dblk);
+          } else {
+            tgetrf[lv].push_back(dblk);
+          }
           c->route[t] = 3;
           DenseItem d{0, static_cast<int32_t>(dblk), static_cast<int32_t>(i), all_full ? 1 : 0, 0,
                       static_cast<int32_t>(i)};
@@ -1020,7 +1204,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           const int32_t task = static_cast<int32_t>(gtasks.size());
           c->route[t] = 1;
           gtasks.push_back(gt);
-          const int slack = c->defer.empty() ? 0 : c->defer[t];
+          const int slack = refine ? rdefer[t] : c->defer.empty() ? 0 : c->defer[t];
           auto& dst = slack >= 3 ? gemE[lv] : slack == 2 ? gemD[lv] : gem[lv];
           // k-chunk skipping: per GBK-chunk of the inner index, the 128-row tiles of L and the
           // 64-column tiles of U holding pattern entries (bit per tile, saturating at 63)
@@ -1110,6 +1294,15 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         gemD[lv].clear();
         gemE[lv].clear();
       }
+      // longest tiles first (LPT): the block scheduler hands out CTAs in index order,
+      // so the long inner loops start early and the level's tail is made of short tiles
+      // (items write disjoint output tiles: the order does not touch the floating point)
+      for (auto* v : {&gem[lv], &gemD[lv], &gemE[lv]})
+        std::stable_sort(v->begin(), v->end(), [&](const GemmItem& x, const GemmItem& y) {
+          const int32_t kx = x.nkc >= 0 ? x.nkc : (gtasks[x.task].K + GBK - 1) / GBK;
+          const int32_t ky = y.nkc >= 0 ? y.nkc : (gtasks[y.task].K + GBK - 1) / GBK;
+          return kx > ky;
+        });
       L.gemm_off = static_cast<int64_t>(mall.size());
       L.ngemm = static_cast<int32_t>(gem[lv].size());
       mall.insert(mall.end(), gem[lv].begin(), gem[lv].end());
@@ -1209,46 +1402,22 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           const int64_t b = tgetrf[lv][q];
           const int m = hb[b].nrows, nt = (m + XT - 1) / XT;
           const int32_t stp = static_cast<int32_t>(T_bi[b]);
-          if (!all_full && m > 2 * XT) {
-            // banded diagonal block: one sweeping task instead of the tile DAG
-            int bl = 0, bu = 0;
-            const int64_t* scp = colptr + T_cp[b];
-            const int64_t* sri = rowidx + T_ent[b];
-            for (int col = 0; col < m; ++col)
-              for (int64_t e = scp[col]; e < scp[col + 1]; ++e) {
-                const int r = static_cast<int>(sri[e]);
-                bl = std::max(bl, r - col);
-                bu = std::max(bu, col - r);
-              }
-            if (bl <= BAND_MAX && bu <= BAND_MAX && m <= 32767) {
-              std::vector<int> band_tasks;
-              // independent segments: cut before column s when no entry couples
-              // [.., s) with [s, ..) (block-diagonal bodies inside one block)
-              std::vector<int> lo(m, m);  // lowest row/col index coupled to index x from the other side
-              for (int col = 0; col < m; ++col)
-                for (int64_t e = scp[col]; e < scp[col + 1]; ++e) {
-                  const int r = static_cast<int>(sri[e]);
-                  const int a0 = std::min(r, col), a1 = std::max(r, col);
-                  lo[a1] = std::min(lo[a1], a0);
-                }
-              // segment boundary at s iff min over x >= s of lo[x] >= s
-              std::vector<int> sufmin(m + 1, m);
-              for (int x = m - 1; x >= 0; --x) sufmin[x] = std::min(sufmin[x + 1], lo[x]);
-              int s0 = 0;
-              for (int s1 = 1; s1 <= m; ++s1) {
-                const bool boundary = s1 == m || (sufmin[s1] >= s1 && s1 - s0 >= 64);
-                if (boundary) {
-                  band_tasks.push_back(X.add(X_BAND, b, s0, bl, bu, s1 - s0, stp, 0, {}));
-                  s0 = s1;
-                }
-              }
-              if (merge_next) {
-                const int done = X.add(X_NOP, b, b, 0, 0, 0, stp, 0, band_tasks);
-                coldone[b].assign(nt, done);
-                rowdone[b].assign(nt, done);
-              }
-              continue;
+          if (band.count(b)) {
+            // banded diagonal block: one sweeping task per independent segment instead of
+            // the tile DAG (refined plans: only the segments whose level is this one)
+            const BandInfo& bi = band.at(b);
+            std::vector<int> band_tasks;
+            for (size_t q = 0; q < bi.seg.size(); ++q) {
+              if (refine && bi.lev[q] != lv) continue;
+              const int s0 = bi.seg[q].first, s1 = bi.seg[q].second;
+              band_tasks.push_back(X.add(X_BAND, b, s0, bi.bl, bi.bu, s1 - s0, stp, 0, {}));
             }
+            if (merge_next) {
+              const int done = X.add(X_NOP, b, b, 0, 0, 0, stp, 0, band_tasks);
+              coldone[b].assign(nt, done);
+              rowdone[b].assign(nt, done);
+            }
+            continue;
           }
           // column maxima at GETRF entry: tasks over (column tile, row chunk of
           // COLMAX_ROWS); every first write into column tile c waits for all of
@@ -1727,6 +1896,8 @@ bool same(double a, double b) { return a == b || (std::isnan(a) && std::isnan(b)
 
 int build_graph(lbk_ctx* c, double pivot_tol, double static_eps, lbk_status* st) {
   const int ns = nsegments(c);
+  if (c->refined && !std::isnan(static_eps))
+    return fail(st, LBK_ERR_BAD_ARG, "static pivoting needs a plan without segment-refined levels (lbk_plan flags bit 2)");
   if (static_cast<int>(c->graphs.size()) == ns && same(c->g_tol, pivot_tol) && same(c->g_eps, static_eps)) return 0;
   drop_graphs(c);
   for (int s = 0; s < ns; ++s) {
@@ -1867,6 +2038,8 @@ int factorize_host_impl(lbk_ctx* c, const double* a_values, bool a_is_pool, doub
   cudaPointerAttributes pa{};
   const bool pinned = cudaPointerGetAttributes(&pa, lu_values) == cudaSuccess && pa.type == cudaMemoryTypeHost;
   (void)cudaGetLastError();
+  if (c->refined && !std::isnan(static_eps))
+    return fail(st, LBK_ERR_BAD_ARG, "static pivoting needs a plan without segment-refined levels (lbk_plan flags bit 2)");
   if (pinned && nsegments(c) == 1 && c->nnz >= (int64_t{1} << 24)) {
     // streamed output: every block's factor values are copied to the host while
     // later levels still run (one graph per output buffer)
@@ -2235,6 +2408,8 @@ void lbk_host_free(void* ptr) {
 // out_ms[nlevels x 5] = level, DMMA SSSSM, panel solves, tiled GETRF, CSC kernel.
 int lbk_level_times(lbk_ctx* c, double pivot_tol, double static_eps, float* out_ms, lbk_status* st) {
   LBK_CUDA(cudaSetDevice(c->device), st);
+  if (c->refined && !std::isnan(static_eps))
+    return fail(st, LBK_ERR_BAD_ARG, "static pivoting needs a plan without segment-refined levels (lbk_plan flags bit 2)");
   const size_t nl = c->levels.size();
   std::vector<cudaEvent_t> ev(1 + nl * 13);
   for (auto& e : ev) LBK_CUDA(cudaEventCreate(&e), st);

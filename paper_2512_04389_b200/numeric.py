@@ -186,13 +186,15 @@ class Engine:
     def __init__(self, grid, tree, *, device: int = 0, chunk: int = DEFAULT_CHUNK, pool: GridPool | None = None,
                  dense: bool = False, dense_threshold: float | None = DEFAULT_DENSE_THRESHOLD,
                  dense_kernels: bool = True, mask: np.ndarray | None = None, cuts: np.ndarray | None = None,
-                 lookahead: bool = True):
+                 lookahead: bool = True, refine: bool = True):
         """dense=True: dense-scratch mode (every block a full tile, true row swaps).
         dense_threshold: tau of the compressed-tile tag (see include/lbk.h lbk_plan);
         None / dense_kernels=False keeps every block CSC (sparse kernels only).
         mask (int8 per task) / cuts (int8 per tree level): distributed plans
         (parallel.DistEngine) — run only the masked tasks, and split the graph
-        into segments after the cut levels."""
+        into segments after the cut levels.
+        refine: segment-level scheduling of banded diagonal blocks (lbk_plan flags bit 2;
+        such a plan cannot run static pivoting — use refine=False for that)."""
         self.lib = _dev()
         self.grid = grid
         self.tree = tree
@@ -245,7 +247,7 @@ class Engine:
         rc = self.lib.lbk_plan(ctx, grid.n, grid.p, P(pos, i64p), pl.nblocks, P(t, i64p), P(cp, i64p),
                                P(ri, i64p), len(k), P(k, i8p), P(s, i32p), P(r, i32p), P(c, i32p),
                                P(lv, i32p), P(co, i64p), int(chunk),
-                               (1 if (use_tiles or dense) else 0) | (2 if dense else 0),
+                               (1 if (use_tiles or dense) else 0) | (2 if dense else 0) | (4 if refine else 0),
                                float(dense_threshold if use_tiles else 1.0), C.byref(st))
         if rc:
             _native.raise_status(st, "lbk_plan")
@@ -743,7 +745,7 @@ def check_support(grid, tree) -> None:
 
 
 def engine_for(grid, tree, *, device: int = 0, dense: bool = False, chunk: int = DEFAULT_CHUNK,
-               dense_threshold: float | None = DEFAULT_DENSE_THRESHOLD) -> Engine:
+               dense_threshold: float | None = DEFAULT_DENSE_THRESHOLD, refine: bool = True) -> Engine:
     """Cached device plan of (grid, tree); dense=True uses full-rectangle blocks everywhere.
 
     One plan per (device, dense, chunk, dense_threshold) and grid: a call with a different
@@ -756,14 +758,15 @@ def engine_for(grid, tree, *, device: int = 0, dense: bool = False, chunk: int =
             grid._lbk_engines = cache
         except AttributeError:
             pass
-    key = (device, dense, chunk, dense_threshold)
+    key = (device, dense, chunk, dense_threshold, refine)
     eng = cache.get(key)
     if eng is not None and eng.tree is not tree:
         eng.close()
         eng = None
     if eng is None:
         cache.pop(key, None)
-        eng = Engine(grid, tree, device=device, chunk=chunk, dense=dense, dense_threshold=dense_threshold)
+        eng = Engine(grid, tree, device=device, chunk=chunk, dense=dense, dense_threshold=dense_threshold,
+                     refine=refine)
         cache[key] = eng
     return eng
 
@@ -783,7 +786,9 @@ def factorize(grid, tree, workers: int = 1, pivot_tol: float = DEFAULT_PIVOT_TOL
     if workers < 1:
         raise DimensionMismatch(f"workers must be >= 1, got {workers}")
     check_support(grid, tree)
-    eng = engine_for(grid, tree, device=device, dense=False, chunk=chunk, dense_threshold=dense_threshold)
+    # static pivoting runs the exact whole-block GETRF: no segment-refined levels for it
+    eng = engine_for(grid, tree, device=device, dense=False, chunk=chunk, dense_threshold=dense_threshold,
+                     refine=static_pivot is None)
     eng.enable_export()
     out = pinned_recycled(eng.nout)
     perms = np.empty(max(eng.n_diag_rows, 1), np.int32)
