@@ -268,6 +268,10 @@ struct lbk_ctx {
   std::vector<int32_t> dext;       // per diagonal block, per 64-col chunk: (row hi, row lo) of its pattern
   std::vector<int64_t> dext_off;   // per block: offset into dext (diagonal blocks)
   DevBuf<int32_t> sdext;
+  // banded FULL diagonal blocks (from lbk_plan): bandwidths and segments for the band solve
+  std::vector<int32_t> band_bl, band_bu, band_seg;
+  std::vector<int64_t> band_off;
+  DevBuf<int32_t> sbandseg;
   DevBuf<SolveStep> sfw, sbw;
   DevBuf<SolveUpd> ufw, ubw;
   DevBuf<int32_t> sbstart, tistep, titile;
@@ -409,6 +413,8 @@ int lbk_create(lbk_ctx** out, int device, lbk_status* st) {
     e = cudaFuncSetAttribute(solve_diag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_SMEM);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(solve_upd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_SMEM);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(solve_band_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, MAX_SMEM);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(tile_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (2 * XREG + XT) * sizeof(double));
@@ -845,6 +851,19 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         bi.lev.assign(bi.seg.size(), -1);
         band.emplace(b, std::move(bi));
       }
+    c->band_bl.assign(nb, -1);
+    c->band_bu.assign(nb, -1);
+    c->band_off.assign(nb, -1);
+    c->band_seg.clear();
+    for (const auto& kv : band) {
+      c->band_bl[kv.first] = kv.second.bl;
+      c->band_bu[kv.first] = kv.second.bu;
+      c->band_off[kv.first] = static_cast<int64_t>(c->band_seg.size());
+      for (const auto& sg : kv.second.seg) {
+        c->band_seg.push_back(sg.first);
+        c->band_seg.push_back(sg.second);
+      }
+    }
     // ---- refined ASAP levels ----------------------------------------------------------
     // The reference's DAG (grid.py:223-378) orders whole blocks.  Inside a banded
     // diagonal block the segments are independent sub-LUs, so: an update into the block
@@ -2282,6 +2301,7 @@ int build_solve(lbk_ctx* c, lbk_status* st) {
     const BlockDev& D = c->hblk[bid[i * p + i]];
     const int64_t span = c->pos[i + 1] - c->pos[i];
     if (D.store != STORE_FULL || span <= XT) continue;
+    if (c->band_bl.size() == static_cast<size_t>(nb) && c->band_bl[bid[i * p + i]] >= 0) continue;  // band solve
     tinv_off[i] = ntinv;
     const int64_t nt = (span + XT - 1) / XT;
     for (int64_t t = 0; t < nt; ++t) {
@@ -2310,6 +2330,22 @@ int build_solve(lbk_ctx* c, lbk_status* st) {
       S.span = static_cast<int32_t>(c->pos[i + 1] - c->pos[i]);
       S.tinv = tinv_off[i];
       S.ext = c->dext_off[bid[i * p + i]];
+      const int64_t db = bid[i * p + i];
+      S.bl = S.bu = -1;
+      S.nseg = 0;
+      S.seg_off = 0;
+      if (c->band_bl.size() == static_cast<size_t>(nb) && c->band_bl[db] >= 0) {
+        S.bl = c->band_bl[db];
+        S.bu = c->band_bu[db];
+        S.seg_off = c->band_off[db];
+        const int64_t next = [&] {  // segments of this block: up to the next block's offset
+          int64_t e = static_cast<int64_t>(c->band_seg.size());
+          for (int64_t b2 = 0; b2 < nb; ++b2)
+            if (c->band_off[b2] > c->band_off[db]) e = std::min(e, c->band_off[b2]);
+          return e;
+        }();
+        S.nseg = static_cast<int32_t>((next - S.seg_off) / 2);
+      }
       maxspan = std::max<int64_t>(maxspan, S.span);
       std::vector<SolveUpd>* out = dir == 0 ? &uf : &ub;
       S.upd_off = static_cast<int64_t>(out->size());
@@ -2340,6 +2376,7 @@ int build_solve(lbk_ctx* c, lbk_status* st) {
   LBK_CUDA(c->tistep.upload(tistep), st);
   LBK_CUDA(c->sdext.upload(c->dext.empty() ? std::vector<int32_t>(2, 0) : c->dext), st);
   LBK_CUDA(c->titile.upload(titile), st);
+  LBK_CUDA(c->sbandseg.upload(c->band_seg.empty() ? std::vector<int32_t>(2, 0) : c->band_seg), st);
   LBK_CUDA(c->stinv.alloc(std::max<int64_t>(ntinv, 1)), st);
   c->n_tinv = static_cast<int64_t>(tistep.size());
   DevPools P = pools(c);
@@ -2355,7 +2392,11 @@ int build_solve(lbk_ctx* c, lbk_status* st) {
     for (size_t q = 0; q < steps.size(); ++q) {
       const SolveStep& S = steps[q];
       const size_t sm = (static_cast<size_t>((S.span + 1) & ~1) + SOLVE_CHUNK * 65) * sizeof(double);
-      if (S.tinv >= 0) {
+      if (S.bl >= 0 && S.nseg > 0) {
+        const int W = std::max(S.bl, S.bu) + 1;
+        solve_band_kernel<<<S.nseg, 256, (BAND_SOLVE_ROWS * (W + 1) + BAND_MAX) * sizeof(double), s0>>>(
+            P, (dir == 0 ? c->sfw.p : c->sbw.p), static_cast<int>(q), c->sv.p, dir, c->sbandseg.p);
+      } else if (S.tinv >= 0) {
         const int nch = (S.span + XT - 1) / XT, rpc = ((nch + SOLVE_CL - 1) / SOLVE_CL) * XT;
         solve_diag_cluster_kernel<<<SOLVE_CL, 256, (rpc + 7 * XT) * sizeof(double), s0>>>(
             P, (dir == 0 ? c->sfw.p : c->sbw.p), static_cast<int>(q), c->sv.p, dir, c->stinv.p, c->sdext.p);

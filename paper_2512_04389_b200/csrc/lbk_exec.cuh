@@ -364,9 +364,13 @@ __device__ __noinline__ void panel16_4w(double* T, int pb, int n, double* Dd, do
 // (3) A22 -= L21 U12 by all 256 threads.  Every column is scaled only after
 // all updates from the columns left of it, so |d_rj| staged in Dd (r > j) is
 // the value the reference's pivot search sees.  Ends with a CTA barrier.
+#ifndef LBK_LU_PB
+#define LBK_LU_PB 16  // panel width of the 64x64 tile LU
+#endif
 __device__ void tile_lu64_blocked(double* T, int n, double* Dd, double* urow, long long* prof = nullptr) {
   const int tid = threadIdx.x;
-  constexpr int PB = 16;
+  constexpr int PB = LBK_LU_PB;
+  static_assert(PB == 16 || !LBK_PANEL4, "the 4-warp panel is 16 columns wide");
   long long t0 = prof ? clock64() : 0;
 #pragma unroll 1
   for (int pb = 0; pb < n; pb += PB) {

@@ -40,7 +40,76 @@ struct SolveStep {
   int64_t upd_off;
   int64_t tinv;   // FULL diagonal blocks: offset of its inverse 64x64 diagonal tiles (-1: none)
   int64_t ext;    // offset of the per-chunk (row hi, row lo) pattern extents
+  int32_t bl, bu; // banded FULL diagonal block: bandwidths (-1: not banded)
+  int32_t nseg;   // its independent segments
+  int64_t seg_off;  // offset of their (s0, s1) pairs
 };
+
+constexpr int BAND_SOLVE_ROWS = 1024;  // rows of a segment staged per chunk
+
+// Banded FULL diagonal block (the filled pattern within |r - c| <= bl / bu, e.g. the
+// bodies of a bordered-block-diagonal matrix): one CTA per independent segment stages
+// the band of up to 1,024 rows into shared memory (row-oriented: the sweep reads
+// contiguous entries) and one thread sweeps it, carrying the last bw solution values
+// across chunks.  Forward: x_r = y_r - sum_q L(r, r-q) x_{r-q} (unit lower);
+// backward: x_r = (y_r - sum_q U(r, r+q) x_{r+q}) / U(r, r).  Same row operations as the
+// dense chunked solve restricted to the band (entries outside it are exact zeros).
+__global__ void __launch_bounds__(256) solve_band_kernel(DevPools P, const SolveStep* __restrict__ steps, int s,
+                                                        double* __restrict__ v, int upper,
+                                                        const int32_t* __restrict__ segs) {
+  extern __shared__ double sm[];
+  const SolveStep S = steps[s];
+  const BlockDev D = P.blk[S.diag];
+  const int s0 = segs[S.seg_off + 2 * blockIdx.x], s1 = segs[S.seg_off + 2 * blockIdx.x + 1];
+  const int bw = upper ? S.bu : S.bl, W = bw + 1, ld = D.nR;
+  const double* G = P.vals + D.ent;
+  double* band = sm;                              // [BAND_SOLVE_ROWS][W]
+  double* ys = sm + BAND_SOLVE_ROWS * W;          // [BAND_SOLVE_ROWS]
+  double* carry = ys + BAND_SOLVE_ROWS;           // last bw solved values of the previous chunk
+  const int m = s1 - s0, nch = (m + BAND_SOLVE_ROWS - 1) / BAND_SOLVE_ROWS;
+  for (int q = 0; q < nch; ++q) {
+    const int cq = upper ? nch - 1 - q : q;
+    const int r0 = s0 + cq * BAND_SOLVE_ROWS, rn = min(BAND_SOLVE_ROWS, s1 - r0);
+    for (int idx = threadIdx.x; idx < rn * W; idx += blockDim.x) {
+      const int r = r0 + idx / W, k = idx % W;
+      const int c = upper ? r + k : r - k;  // (r, c): U(r, r + k) / L(r, r - k)
+      band[idx] = (c >= s0 && c < s1) ? G[static_cast<size_t>(c) * ld + r] : 0.0;
+    }
+    for (int r = threadIdx.x; r < rn; r += blockDim.x) ys[r] = v[S.off + r0 + r];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      if (!upper) {
+        for (int r = 0; r < rn; ++r) {
+          double acc = ys[r];
+          for (int k = 1; k <= bw; ++k) {
+            const int rr = r - k;
+            const double xk = rr >= 0 ? ys[rr] : (r0 + rr >= s0 ? carry[bw + rr] : 0.0);
+            acc = fma(-band[r * W + k], xk, acc);
+          }
+          ys[r] = acc;
+        }
+      } else {
+        for (int r = rn - 1; r >= 0; --r) {
+          double acc = ys[r];
+          for (int k = 1; k <= bw; ++k) {
+            const int rr = r + k;
+            const double xk = rr < rn ? ys[rr] : (r0 + rr < s1 ? carry[rr - rn] : 0.0);
+            acc = fma(-band[r * W + k], xk, acc);
+          }
+          ys[r] = acc / band[r * W];
+        }
+      }
+      // the values the next chunk reaches back to
+      for (int k = 0; k < bw; ++k) {
+        if (!upper) carry[k] = rn - bw + k >= 0 ? ys[rn - bw + k] : 0.0;
+        else carry[k] = k < rn ? ys[k] : 0.0;
+      }
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < rn; r += blockDim.x) v[S.off + r0 + r] = ys[r];
+    __syncthreads();
+  }
+}
 
 constexpr int SOLVE_CL = 8;  // CTAs per cluster of the diagonal solve
 

@@ -35,6 +35,10 @@ CASES = {
     "arrow": (lambda: generate("arrowhead", 1000, b=100), None, {}),
     "randspd": (lambda: generate("random_spd", 3000, bandwidth=20, density=0.3), None, {}),
     "p3d12_csc": (lambda: G.poisson3d(12, "nd"), None, {"dense_threshold": None}),
+    # banded diagonal blocks solved per segment (solve_band_kernel), bodies longer than one
+    # 1,024-row staging chunk, and one 2,500-row segment per block
+    "bbd_bigbody": (lambda: G.bbd(30000, 600, 10, seed=2), None, {}),
+    "tridiag_reg": (lambda: generate("tridiagonal", 5000), 2500, {}),
 }
 
 
