@@ -365,12 +365,15 @@ __device__ __noinline__ void panel16_4w(double* T, int pb, int n, double* Dd, do
 // all updates from the columns left of it, so |d_rj| staged in Dd (r > j) is
 // the value the reference's pivot search sees.  Ends with a CTA barrier.
 #ifndef LBK_LU_PB
-#define LBK_LU_PB 16  // panel width of the 64x64 tile LU
+#define LBK_LU_PB 8  // panel width of the 64x64 tile LU (8: C2 167.3 -> 161.6 ms vs 16, profiles/r2_lu_pb_ab.txt)
+#endif
+#ifndef LBK_A22_4X4
+#define LBK_A22_4X4 1  // trailing update of the tile LU in 4 x 4 register tiles
 #endif
 __device__ void tile_lu64_blocked(double* T, int n, double* Dd, double* urow, long long* prof = nullptr) {
   const int tid = threadIdx.x;
   constexpr int PB = LBK_LU_PB;
-  static_assert(PB == 16 || !LBK_PANEL4, "the 4-warp panel is 16 columns wide");
+  static_assert(PB == 16 || (!LBK_PANEL4 && !LBK_TILE_DMMA), "the 4-warp panel and the DMMA update are 16 wide");
   long long t0 = prof ? clock64() : 0;
 #pragma unroll 1
   for (int pb = 0; pb < n; pb += PB) {
@@ -445,6 +448,42 @@ __device__ void tile_lu64_blocked(double* T, int n, double* Dd, double* urow, lo
     // (3) A22 -= L21 U12 (tensor cores, or work units (row, group of 4 columns) dealt over all 256 threads)
 #if LBK_TILE_DMMA
     mma_sub_k16(T, XTP, T + pb * XTP, XTP, T + pb, XTP, pe, n - pe, pe, n - pe);
+#elif LBK_A22_4X4
+    {
+      // 4 x 4 register tiles: rows pe + rg + i * RG (consecutive threads -> consecutive rows:
+      // conflict-free L / C accesses), columns pe + 4 cg + j (U loads broadcast in a warp);
+      // 8 shared loads per 16 FMA instead of 5 per 4
+      const int R = n - pe, RG = (R + 3) / 4, CG = (R + 3) / 4;
+      if (tid < RG * CG) {
+        const int rg = tid % RG, c0 = pe + 4 * (tid / RG);
+        int rr[4];
+        double a[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          rr[i] = pe + rg + i * RG;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            a[i][j] = (rr[i] < n && c0 + j < n) ? T[(c0 + j) * XTP + rr[i]] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < PB; ++k) {
+          double l[4], u[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) l[i] = T[(pb + k) * XTP + min(rr[i], XT - 1)];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) u[j] = T[min(c0 + j, XT - 1) * XTP + pb + k];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) a[i][j] = fma(-l[i], u[j], a[i][j]);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (rr[i] < n && c0 + j < n) T[(c0 + j) * XTP + rr[i]] = a[i][j];
+      }
+    }
 #else
     {
       const int R = n - pe, CG = (n - pe + 3) / 4;

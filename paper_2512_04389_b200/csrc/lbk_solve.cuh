@@ -47,6 +47,36 @@ struct SolveStep {
 
 constexpr int BAND_SOLVE_ROWS = 1024;  // rows of a segment staged per chunk
 
+// One thread's sweep over a staged chunk of a band segment (solve_band_kernel).  The last
+// B solution values live in registers (win[k-1] = x at distance k), so each row costs one
+// FMA on the dependency chain: the terms of the older values are summed first.  The
+// backward sweep multiplies by the reciprocal of U(r, r) (formed off the chain).
+// nb = the band width when it is below the template bound (B = 8 / 15 buckets).
+template <int B>
+__device__ __forceinline__ void band_sweep(double* ys, const double* band, int W, int rn, int upper,
+                                           const double* carry, int before, int after, int nb = B) {
+  double win[B > 0 ? B : 1];
+#pragma unroll
+  for (int k = 0; k < B; ++k) {  // values of the previous chunk (0 outside the segment)
+    if (!upper) win[k] = (k < nb && k < before) ? carry[nb - 1 - k] : 0.0;
+    else win[k] = (k < nb && k < after) ? carry[k] : 0.0;
+  }
+  for (int q = 0; q < rn; ++q) {
+    const int r = upper ? rn - 1 - q : q;
+    const double* br = band + r * W;
+    double acc = ys[r];
+#pragma unroll
+    for (int k = B; k >= 2; --k)
+      if (k <= nb) acc = fma(-br[k], win[k - 1], acc);
+    double x = B >= 1 && nb >= 1 ? fma(-br[1], win[0], acc) : acc;
+    if (upper) x *= 1.0 / br[0];
+#pragma unroll
+    for (int k = B - 1; k >= 1; --k) win[k] = win[k - 1];
+    if (B > 0) win[0] = x;
+    ys[r] = x;
+  }
+}
+
 // Banded FULL diagonal block (the filled pattern within |r - c| <= bl / bu, e.g. the
 // bodies of a bordered-block-diagonal matrix): one CTA per independent segment stages
 // the band of up to 1,024 rows into shared memory (row-oriented: the sweep reads
@@ -78,28 +108,16 @@ __global__ void __launch_bounds__(256) solve_band_kernel(DevPools P, const Solve
     for (int r = threadIdx.x; r < rn; r += blockDim.x) ys[r] = v[S.off + r0 + r];
     __syncthreads();
     if (threadIdx.x == 0) {
-      if (!upper) {
-        for (int r = 0; r < rn; ++r) {
-          double acc = ys[r];
-          for (int k = 1; k <= bw; ++k) {
-            const int rr = r - k;
-            const double xk = rr >= 0 ? ys[rr] : (r0 + rr >= s0 ? carry[bw + rr] : 0.0);
-            acc = fma(-band[r * W + k], xk, acc);
-          }
-          ys[r] = acc;
-        }
-      } else {
-        for (int r = rn - 1; r >= 0; --r) {
-          double acc = ys[r];
-          for (int k = 1; k <= bw; ++k) {
-            const int rr = r + k;
-            const double xk = rr < rn ? ys[rr] : (r0 + rr < s1 ? carry[rr - rn] : 0.0);
-            acc = fma(-band[r * W + k], xk, acc);
-          }
-          ys[r] = acc / band[r * W];
-        }
+      switch (bw) {
+        case 0: band_sweep<0>(ys, band, W, rn, upper, carry, r0 - s0, s1 - r0 - rn); break;
+        case 1: band_sweep<1>(ys, band, W, rn, upper, carry, r0 - s0, s1 - r0 - rn); break;
+        case 2: band_sweep<2>(ys, band, W, rn, upper, carry, r0 - s0, s1 - r0 - rn); break;
+        case 3: band_sweep<3>(ys, band, W, rn, upper, carry, r0 - s0, s1 - r0 - rn); break;
+        case 4: band_sweep<4>(ys, band, W, rn, upper, carry, r0 - s0, s1 - r0 - rn); break;
+        case 5: case 6: case 7: case 8: band_sweep<8>(ys, band, W, rn, upper, carry, r0 - s0, s1 - r0 - rn, bw); break;
+        default: band_sweep<15>(ys, band, W, rn, upper, carry, r0 - s0, s1 - r0 - rn, bw); break;
       }
-      // the values the next chunk reaches back to
+      // the values the next chunk reaches back to (forward: the last bw rows, backward: the first)
       for (int k = 0; k < bw; ++k) {
         if (!upper) carry[k] = rn - bw + k >= 0 ? ys[rn - bw + k] : 0.0;
         else carry[k] = k < rn ? ys[k] : 0.0;
