@@ -104,6 +104,10 @@ constexpr int NBRANCH = 3;
 // Builds one level's tile-DAG for the persistent executor: tasks get a
 // priority key (elimination sub-step first); flush() orders them by key
 // (topological within every DAG) and emits counters and successor lists.
+#ifndef LBK_CHAIN_TRSM
+#define LBK_CHAIN_TRSM 0  // 1: the diagonal LU task also solves the next step's two update operands (measured slower: the two solves then run one after the other instead of on two CTAs)
+#endif
+
 struct ExecBuilder {
   std::vector<XTask> t;
   std::vector<int64_t> key;
@@ -149,7 +153,7 @@ struct ExecBuilder {
       for (int i = n - 1; i >= 0; --i) {
         int64_t m = 0;
         for (int s2 : fwd[i]) m = std::max(m, rank[s2]);
-        rank[i] = m + cost_of(t[i].type);
+        rank[i] = m + cost_of(t[i].type) + (t[i].chain ? cost_of(X_TRSM_L) + cost_of(X_TRSM_U) : 0);
       }
       std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return rank[x] > rank[y]; });
     }
@@ -1463,8 +1467,20 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           bool fused = false;
           std::vector<std::vector<int>> colw(nt), roww(nt);  // writers of each tile column's L / row's U part
           for (int kb = 0; kb < nt; ++kb) {
-            const int g = fused ? X.add(X_GETRF_UPD, b, b, kb, kb, kb - 1, stp, kb * 4, fused_deps)
-                                : X.add(X_GETRF, b, b, kb, kb, kb, stp, kb * 4, prev(kb, kb, {}));
+            // chain: this step's LU task also solves L(kb+1, kb) and U(kb, kb+1), the operands
+            // of the next diagonal update (both tiles present), so the critical chain has one
+            // task and one handoff per step instead of three and two
+            const bool chain = LBK_CHAIN_TRSM && kb + 1 < nt && occ[q][static_cast<size_t>(kb) * nt + kb + 1] &&
+                               occ[q][static_cast<size_t>(kb + 1) * nt + kb];
+            std::vector<int> gdeps = fused ? fused_deps : prev(kb, kb, {});
+            if (chain) {
+              const std::vector<int> dl = prev(kb + 1, kb, {}), du = prev(kb, kb + 1, {});
+              gdeps.insert(gdeps.end(), dl.begin(), dl.end());
+              gdeps.insert(gdeps.end(), du.begin(), du.end());
+            }
+            const int g = fused ? X.add(X_GETRF_UPD, b, b, kb, kb, kb - 1, stp, kb * 4, gdeps)
+                                : X.add(X_GETRF, b, b, kb, kb, kb, stp, kb * 4, gdeps);
+            X.t[g].chain = chain ? 1 : 0;
             fused = false;
             colw[kb].push_back(g);
             roww[kb].push_back(g);
@@ -1473,7 +1489,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
             for (int r = kb + 1; r < nt; ++r) {
               lt[r] = -1;
               if (!occ[q][static_cast<size_t>(kb) * nt + r]) continue;
-              lt[r] = X.add(X_TRSM_L, b, b, r, kb, kb, stp, kb * 4 + 1, prev(r, kb, {g}));
+              lt[r] = (chain && r == kb + 1) ? g : X.add(X_TRSM_L, b, b, r, kb, kb, stp, kb * 4 + 1, prev(r, kb, {g}));
               colw[kb].push_back(lt[r]);
               L_(r, kb) = lt[r];
               fin_deps.push_back(lt[r]);
@@ -1481,7 +1497,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
             for (int cc = kb + 1; cc < nt; ++cc) {
               ut[cc] = -1;
               if (!occ[q][static_cast<size_t>(cc) * nt + kb]) continue;
-              ut[cc] = X.add(X_TRSM_U, b, b, kb, cc, kb, stp, kb * 4 + 1, prev(kb, cc, {g}));
+              ut[cc] = (chain && cc == kb + 1) ? g : X.add(X_TRSM_U, b, b, kb, cc, kb, stp, kb * 4 + 1, prev(kb, cc, {g}));
               roww[kb].push_back(ut[cc]);
               L_(kb, cc) = ut[cc];
             }
@@ -1616,6 +1632,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         }
         for (const XTask& x : X.t) {  // executed flops of the tile tasks (full 64-tiles)
           const double t3 = 64.0 * 64.0 * 64.0;
+          if (x.chain) c->exec_flops += 2 * t3;  // the two solved tiles of the chain
           c->exec_flops += x.type == X_GETRF_UPD                                     ? 2 * t3 + 2 * t3 / 3
                            : x.type == X_PG_FUSED || x.type == X_PT_FUSED              ? 3 * t3
                            : x.type == X_GEMM || x.type == X_PG_UPD || x.type == X_PT_UPD ? 2 * t3

@@ -63,7 +63,7 @@ enum XType : int8_t {
 
 struct XTask {
   int8_t type;
-  int8_t pad0;
+  int8_t chain;  // X_GETRF / X_GETRF_UPD: then also solve L(r+1, r) and U(r, r+1) (the next step's update operands)
   int16_t r, c, k;
   int16_t pad1;
   int32_t a;     // block the task writes
@@ -208,6 +208,53 @@ __device__ __noinline__ void mma_sub_k16(double* C, int ldc, const double* A, in
   }
 }
 
+
+#ifndef LBK_TRSM_PB
+#define LBK_TRSM_PB 16  // panel width of the tile triangular solves
+#endif
+#ifndef LBK_TRSM_4X4
+#define LBK_TRSM_4X4 1  // their trailing updates in 4 x 4 register tiles
+#endif
+
+// C[r, c] -= sum_{k < PB} A[r, k] B[k, c] for rows [r0, r0 + R) x columns [c0, c0 + Cn) of
+// 64-tiles in shared memory (column-major, XTP): A(r, k) = A[k * XTP + r], B(k, c) =
+// B[c * XTP + k], C(r, c) = C[c * XTP + r].  4 x 4 register tiles (rows rg + i * RG:
+// consecutive threads read consecutive rows; columns 4 cg + j: B loads broadcast within a
+// warp), 8 shared loads per 16 FMA.
+template <int PB>
+__device__ __forceinline__ void trail_4x4(double* C, const double* A, const double* B, int r0, int R, int c0,
+                                          int Cn) {
+  const int RG = (R + 3) >> 2, CG = (Cn + 3) >> 2;
+  for (int u = threadIdx.x; u < RG * CG; u += blockDim.x) {
+    const int rg = u % RG, cb = c0 + 4 * (u / RG);
+    int rr[4];
+    double a[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      rr[i] = rg + i * RG < R ? r0 + rg + i * RG : -1;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) a[i][j] = (rr[i] >= 0 && cb + j < c0 + Cn) ? C[(cb + j) * XTP + rr[i]] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < PB; ++k) {
+      double l[4], w[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) l[i] = A[k * XTP + (rr[i] >= 0 ? rr[i] : 0)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) w[j] = B[min(cb + j, XT - 1) * XTP + k];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) a[i][j] = fma(-l[i], w[j], a[i][j]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (rr[i] >= 0 && cb + j < c0 + Cn) C[(cb + j) * XTP + rr[i]] = a[i][j];
+  }
+}
+
 // X (smem, XTP) <- X U^{-1} for columns [0, nc); U upper in smem (XTP), rinv[j] =
 // 1/u_jj.  Blocked by 16 columns: the panel solve needs no communication
 // between rows (threads 0..63 own one row each), the trailing update runs on
@@ -216,7 +263,8 @@ __device__ __noinline__ void mma_sub_k16(double* C, int ldc, const double* A, in
 template <bool kCheck>
 __device__ void tile_right_solve_blk(double* X, const double* U, const double* rinv, double* Dd, int nc) {
   const int tid = threadIdx.x;
-  constexpr int PB = 16;
+  constexpr int PB = LBK_TRSM_PB;
+  static_assert(PB == 16 || !LBK_TILE_DMMA, "the DMMA update is 16 deep");
 #pragma unroll 1
   for (int pb = 0; pb < nc; pb += PB) {
     if (tid < XT) {
@@ -242,8 +290,11 @@ __device__ void tile_right_solve_blk(double* X, const double* U, const double* r
     if (pe >= nc) break;
 #if LBK_TILE_DMMA
     mma_sub_k16(X, XTP, X + pb * XTP, XTP, U + pb, XTP, 0, XT, pe, nc - pe);
+#elif LBK_TRSM_4X4
+    trail_4x4<PB>(X, X + pb * XTP, U + pb, 0, XT, pe, nc - pe);
 #else
     {
+      static_assert(PB == 16, "trail16 is 16 deep");
       const int r = tid & (XT - 1);
       double l[PB];
 #pragma unroll
@@ -260,7 +311,8 @@ __device__ void tile_right_solve_blk(double* X, const double* U, const double* r
 // c < 64 owns column c of the 16-row panel; the trailing rows on all 256 threads.
 __device__ void tile_left_solve_blk(double* X, const double* Lm, int nr) {
   const int tid = threadIdx.x;
-  constexpr int PB = 16;
+  constexpr int PB = LBK_TRSM_PB;
+  static_assert(PB == 16 || !LBK_TILE_DMMA, "the DMMA update is 16 deep");
 #pragma unroll 1
   for (int pb = 0; pb < nr; pb += PB) {
     if (tid < XT) {
@@ -280,6 +332,8 @@ __device__ void tile_left_solve_blk(double* X, const double* Lm, int nr) {
     if (pe >= nr) break;
 #if LBK_TILE_DMMA
     mma_sub_k16(X, XTP, Lm + pb * XTP, XTP, X + pb, XTP, pe, nr - pe, 0, XT);
+#elif LBK_TRSM_4X4
+    trail_4x4<PB>(X, Lm + pb * XTP, X + pb, pe, nr - pe, 0, XT);
 #else
     {
       // X[r, c] -= sum_k L[r, pb + k] X[pb + k, c] for the R = nr - pe rows below
@@ -911,6 +965,24 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       store_tile(G, m, T0, n, n);
       flush_colmax(T1, n, n, false, P.bmax + A.dg + k0, T2);
       stamp(ph, 2);
+      if (tk.chain) {
+        // the critical chain of the diagonal block continues through L(k+1, k) and U(k, k+1):
+        // solve them here with the factored tile still in shared memory (no handoff, no reload)
+        const int r0 = k0 + XT, nr = min(XT, m - r0);
+        __syncthreads();
+        load_tile(T1, P.vals + A.ent + static_cast<size_t>(k0) * m + r0, m, nr, n);  // L tile (r0, k0)
+        if (threadIdx.x < XT) rinv[threadIdx.x] = threadIdx.x < n ? 1.0 / T0[threadIdx.x * XTP + threadIdx.x] : 1.0;
+        __syncthreads();
+        tile_right_solve_blk<true>(T1, T0, rinv, T2, n);
+        store_tile(P.vals + A.ent + static_cast<size_t>(k0) * m + r0, m, T1, nr, n);
+        flush_colmax(T2, nr, n, true, P.bmax + A.dg + k0, T1);
+        __syncthreads();
+        load_tile(T1, P.vals + A.ent + static_cast<size_t>(r0) * m + k0, m, n, nr);  // U tile (k0, r0)
+        __syncthreads();
+        tile_left_solve_blk(T1, T0, n);
+        store_tile(P.vals + A.ent + static_cast<size_t>(r0) * m + k0, m, T1, n, nr);
+        stamp(ph, 3);
+      }
       break;
     }
     case X_TRSM_L: {  // rows of tile (r,k) in registers, U_kk in smem
