@@ -266,7 +266,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--levels-out", default=None, help="write per-level device times + work to this .npz")
-    ap.add_argument("--dense-threshold", type=float, default=0.1,
+    ap.add_argument("--dense-threshold", type=float, default=0.05,
                     help="compressed-tile density tag for the FP64 DMMA kernels; <0 = CSC kernels only")
     ap.add_argument("--plan", default="irregular", help="irregular | selector | regular:<block size>")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent replicas instead of 2D block-cyclic")

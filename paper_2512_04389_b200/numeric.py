@@ -34,8 +34,11 @@ DEFAULT_PIVOT_TOL = 1e-12
 DEFAULT_CHUNK = 8
 # compressed-tile tag: a block whose nonempty-rows x nonempty-columns rectangle
 # holds >= this fraction of entries runs on the DMMA kernels (the reference's
-# own dense tag is 0.5 of the FULL block, factorize.py:274)
-DEFAULT_DENSE_THRESHOLD = 0.1
+# own dense tag is 0.5 of the FULL block, factorize.py:274).  0.05: at 0.1 the 74
+# blocks of C4 that stayed CSC cost 620 ms of its 1,464 ms; as compressed tiles
+# they add 2 % executed flops and the factorization takes 907 ms
+# (profiles/r2_bench_c4_tau*.json); C2, C3 and C5 have no block below 0.1.
+DEFAULT_DENSE_THRESHOLD = 0.05
 
 P = _native.ptr
 i64p, i32p, i8p, f64p = _native.c_i64p, _native.c_i32p, _native.c_i8p, _native.c_f64p

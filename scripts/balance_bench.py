@@ -78,7 +78,7 @@ def main():
     ap.add_argument("matrices", nargs="+")
     ap.add_argument("--sizes", default=None, help="regular block sizes (default: PANGULU_SIZES <= n)")
     ap.add_argument("--repeats", type=int, default=3)
-    ap.add_argument("--tau", type=float, default=0.1)
+    ap.add_argument("--tau", type=float, default=0.05)
     ap.add_argument("--check", action="store_true", help="also solve and report ||Ax-b||/||b||")
     ap.add_argument("--out", default=None, help="JSON lines output")
     ap.add_argument("--grid", default=None,
