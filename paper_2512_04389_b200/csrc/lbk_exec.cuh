@@ -142,6 +142,10 @@ __device__ __forceinline__ void trail16(const double (&l)[16], int c0, int ce, T
 }
 
 
+#ifndef LBK_LATE_FLUSH
+#define LBK_LATE_FLUSH 1  // colmax flush of GETRF / TRSM_L tiles after their successors are released
+#endif
+
 #ifndef LBK_TILE_DMMA
 #define LBK_TILE_DMMA 0  // 1: trailing updates inside the tile LU / TRSM routines on DMMA (measured slower)
 #endif
@@ -963,7 +967,7 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       tile_lu64_blocked(T0, n, T1, rinv);
       stamp(ph, 1);
       store_tile(G, m, T0, n, n);
-      flush_colmax(T1, n, n, false, P.bmax + A.dg + k0, T2);
+      if (!LBK_LATE_FLUSH || tk.chain) flush_colmax(T1, n, n, false, P.bmax + A.dg + k0, T2);
       stamp(ph, 2);
       if (tk.chain) {
         // the critical chain of the diagonal block continues through L(k+1, k) and U(k, k+1):
@@ -998,7 +1002,7 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       stamp(ph, 1);
       store_tile(G, m, T0, nr, nk);
       stamp(ph, 2);
-      flush_colmax(T2, nr, nk, true, P.bmax + A.dg + k0, T1);
+      if (!LBK_LATE_FLUSH) flush_colmax(T2, nr, nk, true, P.bmax + A.dg + k0, T1);
       stamp(ph, 3);
       break;
     }
@@ -1127,6 +1131,28 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
 // kBandReg: the launch holds band sweeps of half-bandwidth 4 (BBD bodies),
 // run by the register-window sweep; its registers (> 128) allow one CTA per SM,
 // so levels without such sweeps use the plain instance at two CTAs per SM.
+// Late colmax flush: a GETRF tile and a TRSM_L tile release their successors as soon
+// as their tile is stored; the staged |d| maxima (still in shared memory) are folded
+// into bmax afterwards.  Only the pivot verdict (X_FINAL) reads bmax, so it alone is
+// released after the flush.  Takes the flush (~1-1.5 us) off the critical tile chain.
+__device__ __forceinline__ bool late_flush(const XTask& tk) {
+  return LBK_LATE_FLUSH && (((tk.type == X_GETRF || tk.type == X_GETRF_UPD) && !tk.chain) || tk.type == X_TRSM_L);
+}
+
+__device__ void run_late_flush(const XTask& tk, const DevPools& P, double* sm) {
+  double* T1 = sm + XREG;
+  double* T2 = sm + 2 * XREG;
+  const BlockDev A = P.blk[tk.a];
+  const int m = A.nrows;
+  if (tk.type == X_TRSM_L) {
+    const int k0 = tk.k * XT, r0 = tk.r * XT, nk = min(XT, m - k0), nr = min(XT, m - r0);
+    flush_colmax(T2, nr, nk, true, P.bmax + A.dg + k0, T1);
+  } else {
+    const int k0 = tk.r * XT, n = min(XT, m - k0);
+    flush_colmax(T1, n, n, false, P.bmax + A.dg + k0, T2);
+  }
+}
+
 template <bool kBandReg>
 __device__ __forceinline__ void exec_body(const XLevel& L, const DevPools& P, double pivot_tol) {
   extern __shared__ double sm[];
@@ -1155,11 +1181,21 @@ __device__ __forceinline__ void exec_body(const XLevel& L, const DevPools& P, do
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0 && L.trace) L.trace[8 * t + 7] = gtimer();
+    const bool late = late_flush(tk);
     {
       const int e0 = L.succ_ptr[t], e1 = L.succ_ptr[t + 1];
-      for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) atomicSub(L.deps + L.succ[e], 1);
+      for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x)
+        if (!late || L.tasks[L.succ[e]].type != X_FINAL) atomicSub(L.deps + L.succ[e], 1);
     }
     if (threadIdx.x == 0 && L.trace) L.trace[8 * t + 2] = gtimer();
+    if (late) {
+      run_late_flush(tk, P, sm);  // (flush_colmax ends with its atomics; fence + barrier below)
+      __threadfence();
+      __syncthreads();
+      const int e0 = L.succ_ptr[t], e1 = L.succ_ptr[t + 1];
+      for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x)
+        if (L.tasks[L.succ[e]].type == X_FINAL) atomicSub(L.deps + L.succ[e], 1);
+    }
   }
 }
 
