@@ -61,6 +61,7 @@ __device__ __forceinline__ void band_sweep(double* ys, const double* band, int W
     if (!upper) win[k] = (k < nb && k < before) ? carry[nb - 1 - k] : 0.0;
     else win[k] = (k < nb && k < after) ? carry[k] : 0.0;
   }
+#pragma unroll 4
   for (int q = 0; q < rn; ++q) {
     const int r = upper ? rn - 1 - q : q;
     const double* br = band + r * W;
@@ -69,7 +70,7 @@ __device__ __forceinline__ void band_sweep(double* ys, const double* band, int W
     for (int k = B; k >= 2; --k)
       if (k <= nb) acc = fma(-br[k], win[k - 1], acc);
     double x = B >= 1 && nb >= 1 ? fma(-br[1], win[0], acc) : acc;
-    if (upper) x *= 1.0 / br[0];
+    if (upper) x *= br[0];  // staged as 1 / U(r, r)
 #pragma unroll
     for (int k = B - 1; k >= 1; --k) win[k] = win[k - 1];
     if (B > 0) win[0] = x;
@@ -100,10 +101,26 @@ __global__ void __launch_bounds__(256) solve_band_kernel(DevPools P, const Solve
   for (int q = 0; q < nch; ++q) {
     const int cq = upper ? nch - 1 - q : q;
     const int r0 = s0 + cq * BAND_SOLVE_ROWS, rn = min(BAND_SOLVE_ROWS, s1 - r0);
-    for (int idx = threadIdx.x; idx < rn * W; idx += blockDim.x) {
-      const int r = r0 + idx / W, k = idx % W;
-      const int c = upper ? r + k : r - k;  // (r, c): U(r, r + k) / L(r, r - k)
-      band[idx] = (c >= s0 && c < s1) ? G[static_cast<size_t>(c) * ld + r] : 0.0;
+    // staged column by column: column c holds L(c + q, c) (forward) / U(c - q, c) (backward),
+    // q = 0..bw, contiguous in the column-major tile -> one thread, up to 16 loads in flight
+    {
+      const int cb = upper ? r0 : r0 - bw, ce = upper ? r0 + rn + bw : r0 + rn;
+      for (int c = cb + static_cast<int>(threadIdx.x); c < ce; c += blockDim.x) {
+        double vq[BAND_MAX + 1];
+#pragma unroll
+        for (int q = 0; q <= BAND_MAX; ++q) {
+          const int r = upper ? c - q : c + q;
+          vq[q] = (q < W && c >= s0 && c < s1 && r >= s0 && r < s1) ? G[static_cast<size_t>(c) * ld + r] : 0.0;
+        }
+        if (upper) vq[0] = 1.0 / vq[0];  // the backward sweep multiplies by 1 / U(c, c)
+#pragma unroll
+        for (int q = 0; q <= BAND_MAX; ++q) {
+          const int r = upper ? c - q : c + q;
+          if (q < W && r >= r0 && r < r0 + rn) band[(r - r0) * W + q] = vq[q];
+        }
+      }
+      // (every slot (r, k) of the chunk has its column in [cb, ce): columns outside the
+      // segment write their zeros there too)
     }
     for (int r = threadIdx.x; r < rn; r += blockDim.x) ys[r] = v[S.off + r0 + r];
     __syncthreads();
@@ -346,7 +363,13 @@ __global__ void __launch_bounds__(256) solve_upd_kernel(DevPools P, const SolveU
   const SolveUpd it = items[blockIdx.x];
   const BlockDev B = P.blk[it.blk];
   const int tid = threadIdx.x;
-  for (int c = tid; c < B.ncols; c += blockDim.x) ys[c] = v[it.src_off + c];
+  const int32_t* cl = B.store == STORE_RECT ? P.clist + B.coff : nullptr;
+  // the source values this block reads: a RECT block only its stored columns (compressed)
+  if (cl) {
+    for (int a = tid; a < B.nC; a += blockDim.x) ys[a] = v[it.src_off + cl[a]];
+  } else {
+    for (int c = tid; c < B.ncols; c += blockDim.x) ys[c] = v[it.src_off + c];
+  }
   __syncthreads();
   const double* G = P.vals + B.ent;
   const int a = it.r0 + tid;
@@ -361,7 +384,6 @@ __global__ void __launch_bounds__(256) solve_upd_kernel(DevPools P, const SolveU
   } else {
     // 64 rows x 4 column quarters per CTA: 4x shorter dependent load chains
     const int ar = it.r0 + (tid & 63), quarter = tid >> 6;
-    const int32_t* cl = B.store == STORE_RECT ? P.clist + B.coff : nullptr;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     if (ar < B.nR) {
       const int cq = (B.nC + 3) / 4, cb = quarter * cq, ce = min(B.nC, cb + cq);
@@ -369,10 +391,9 @@ __global__ void __launch_bounds__(256) solve_upd_kernel(DevPools P, const SolveU
       int c = cb;
       for (; c + 8 <= ce; c += 8) {
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          acc[q & 3] = fma(col[static_cast<size_t>(c + q) * B.nR], ys[cl ? cl[c + q] : c + q], acc[q & 3]);
+        for (int q = 0; q < 8; ++q) acc[q & 3] = fma(col[static_cast<size_t>(c + q) * B.nR], ys[c + q], acc[q & 3]);
       }
-      for (; c < ce; ++c) acc[0] = fma(col[static_cast<size_t>(c) * B.nR], ys[cl ? cl[c] : c], acc[0]);
+      for (; c < ce; ++c) acc[0] = fma(col[static_cast<size_t>(c) * B.nR], ys[c], acc[0]);
     }
     double* part = ys + ((B.ncols + 1) & ~1);  // 4 x 64 partial sums after the source segment
     part[quarter * 64 + (tid & 63)] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
