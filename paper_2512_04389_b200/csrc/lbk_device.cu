@@ -2415,8 +2415,12 @@ int build_solve(lbk_ctx* c, lbk_status* st) {
             P, (dir == 0 ? c->sfw.p : c->sbw.p), static_cast<int>(q), c->sv.p, dir, c->sbandseg.p);
       } else if (S.tinv >= 0) {
         const int nch = (S.span + XT - 1) / XT, rpc = ((nch + SOLVE_CL - 1) / SOLVE_CL) * XT;
-        solve_diag_cluster_kernel<<<SOLVE_CL, 256, (rpc + 7 * XT) * sizeof(double), s0>>>(
-            P, (dir == 0 ? c->sfw.p : c->sbw.p), static_cast<int>(q), c->sv.p, dir, c->stinv.p, c->sdext.p);
+        if (LBK_SOLVE_FLAGS)
+          solve_diag_flag_kernel<<<SOLVE_CL, 256, (rpc + 5 * XT + (nch + 1) / 2 + 1) * sizeof(double), s0>>>(
+              P, (dir == 0 ? c->sfw.p : c->sbw.p), static_cast<int>(q), c->sv.p, dir, c->stinv.p, c->sdext.p);
+        else
+          solve_diag_cluster_kernel<<<SOLVE_CL, 256, (rpc + 7 * XT) * sizeof(double), s0>>>(
+              P, (dir == 0 ? c->sfw.p : c->sbw.p), static_cast<int>(q), c->sv.p, dir, c->stinv.p, c->sdext.p);
       } else {
         solve_diag_kernel<<<1, 256, sm, s0>>>(P, (dir == 0 ? c->sfw.p : c->sbw.p), static_cast<int>(q), c->sv.p, dir);
       }

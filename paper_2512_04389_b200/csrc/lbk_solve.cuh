@@ -250,6 +250,125 @@ __global__ void __cluster_dims__(SOLVE_CL, 1, 1) __launch_bounds__(256)
   for (int r = r0 + tid; r < r1; r += blockDim.x) v[S.off + r] = y[r - r0];
 }
 
+#ifndef LBK_SOLVE_FLAGS
+#define LBK_SOLVE_FLAGS 0  // 1: dense diagonal solve with per-chunk flags in distributed shared memory + lookahead (measured slower: C2 solve 68 -> 85 ms)
+#endif
+
+__device__ __forceinline__ int ld_acquire_cluster(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cluster.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_cluster(int* p, int v) {
+  asm volatile("st.release.cluster.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Same solve as solve_diag_cluster_kernel, without a cluster barrier per chunk: the
+// owner of chunk c publishes x_c in its own row segment (y) and raises done[c]
+// (st.release.cluster); a consumer waits on that flag through distributed shared
+// memory (ld.acquire.cluster) and reads x_c from the owner's y.  Lookahead: a CTA that
+// owns the next chunk applies x_c to that chunk's rows first, forms and publishes x_next,
+// and only then applies x_c to the rest of its rows - the critical path per chunk is one
+// 64x64 update, one 64x64 matvec and one flag hop.  Every row still receives its updates
+// in chunk order, each the same 4-way partial-sum matvec as before.
+__global__ void __cluster_dims__(SOLVE_CL, 1, 1) __launch_bounds__(256)
+    solve_diag_flag_kernel(DevPools P, const SolveStep* __restrict__ steps, int s, double* __restrict__ v,
+                           int upper, const double* __restrict__ inv, const int32_t* __restrict__ ext) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  extern __shared__ double sm[];
+  const SolveStep S = steps[s];
+  const BlockDev D = P.blk[S.diag];
+  const int m = S.span, tid = threadIdx.x, q = static_cast<int>(cl.block_rank());
+  const int nch = (m + XT - 1) / XT, rpc = ((nch + SOLVE_CL - 1) / SOLVE_CL) * XT;
+  const int r0 = q * rpc, r1 = min(m, r0 + rpc);
+  double* y = sm;                 // my rows (x once solved)
+  double* xs = sm + rpc;          // the current chunk's solution
+  double* part = xs + XT;         // 256 matvec partial sums
+  int* done = reinterpret_cast<int*>(part + 4 * XT);  // per chunk: x published (own chunks)
+  for (int r = r0 + tid; r < r1; r += blockDim.x) y[r - r0] = v[S.off + r];
+  for (int c = tid; c < nch; c += blockDim.x) done[c] = 0;
+  const double* G = P.vals + D.ent;
+  const int ld = D.nR;
+  cl.sync();  // every CTA's flags are zero before anyone polls them
+  auto chunk = [&](int qq) { return upper ? nch - 1 - qq : qq; };
+  auto owner_of = [&](int c) { return (c * XT) / rpc; };
+  // x_c = Tinv_c r_c on the owner (its rows of chunk c are fully updated), then publish
+  auto solve_chunk = [&](int c) {
+    const int c0 = c * XT, cn = min(XT, m - c0);
+    const double* Ti = inv + S.tinv + static_cast<int64_t>(c) * 2 * XT * XT + (upper ? XT * XT : 0);
+    const int row = tid & (XT - 1), kq = (tid >> 6) * 16;
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (kq + k < cn) acc = fma(Ti[(kq + k) * XT + row], y[c0 - r0 + kq + k], acc);
+    part[tid] = acc;
+    __syncthreads();
+    double xv = 0.0;
+    if (tid < cn) xv = (part[tid] + part[XT + tid]) + (part[2 * XT + tid] + part[3 * XT + tid]);
+    __syncthreads();
+    if (tid < cn) y[c0 - r0 + tid] = xv;
+    __syncthreads();
+    if (tid == 0) st_release_cluster(done + c, 1);
+  };
+  // y[r - r0] -= L[r, c0:c0+cn] xs for r in [lo, hi) (rows of this CTA)
+  auto apply = [&](int c, int lo, int hi) {
+    const int c0 = c * XT, cn = min(XT, m - c0);
+    for (int r = lo + tid; r < hi; r += blockDim.x) {
+      const double* col = G + static_cast<size_t>(c0) * ld + r;
+      double a4[4] = {0.0, 0.0, 0.0, 0.0};
+      if (cn == XT) {
+#pragma unroll
+        for (int k = 0; k < XT; ++k) a4[k & 3] = fma(col[static_cast<size_t>(k) * ld], xs[k], a4[k & 3]);
+      } else {
+        for (int k = 0; k < cn; ++k) a4[k & 3] = fma(col[static_cast<size_t>(k) * ld], xs[k], a4[k & 3]);
+      }
+      y[r - r0] -= (a4[0] + a4[1]) + (a4[2] + a4[3]);
+    }
+  };
+  if (owner_of(chunk(0)) == q) solve_chunk(chunk(0));
+  for (int qq = 0; qq < nch; ++qq) {
+    const int c = chunk(qq), c0 = c * XT, cn = min(XT, m - c0), own = owner_of(c);
+    // rows this chunk reaches inside my range (banded patterns: a few)
+    const int lo = upper ? max(r0, ext[S.ext + 2 * c + 1]) : max(r0, c0 + cn);
+    const int hi = upper ? min(r1, c0) : min(r1, ext[S.ext + 2 * c]);
+    const bool need = lo < hi;
+    if (need) {
+      if (own == q) {
+        if (tid < XT) xs[tid] = tid < cn ? y[c0 - r0 + tid] : 0.0;
+      } else {
+        if (tid == 0) {
+          const int* f = cl.map_shared_rank(done, own) + c;
+          while (ld_acquire_cluster(f) == 0) {
+          }
+        }
+        __syncthreads();
+        const double* src = cl.map_shared_rank(y, own) + (c0 - own * rpc);
+        if (tid < XT) xs[tid] = tid < cn ? src[tid] : 0.0;
+      }
+      __syncthreads();
+    }
+    // lookahead: when the next chunk is mine, its rows get x_c first and it is solved and
+    // published before x_c reaches the rest of my rows
+    int n0 = m, n1 = m;
+    if (qq + 1 < nch && owner_of(chunk(qq + 1)) == q) {
+      n0 = chunk(qq + 1) * XT;
+      n1 = min(m, n0 + XT);
+      if (need) apply(c, max(lo, n0), min(hi, n1));
+      __syncthreads();
+      solve_chunk(chunk(qq + 1));
+    }
+    if (need) {
+      apply(c, lo, min(hi, n0));
+      apply(c, max(lo, n1), hi);
+    }
+    __syncthreads();
+  }
+  cl.sync();  // no CTA leaves while another may still read its rows
+  for (int r = r0 + tid; r < r1; r += blockDim.x) v[S.off + r] = y[r - r0];
+}
+
 struct SolveUpd {
   int32_t blk;      // factor block B_ki
   int32_t tgt_off;  // global offset of block row k
