@@ -238,7 +238,8 @@ def run_reference(args):
     fam, full, _ = R.FAMILIES[args.config]
     scope = ("the full configuration" if case.size == full else
              f"largest same-family instance with predicted run <= {budget:.1f}s and memory <= 0.8 x MemAvailable; "
-             f"full size {full} is infeasible within the bench budget (C2: > 1,930 s and > 62 GB, SURVEY.md 8d)")
+             f"full size {full} does not fit the bench budget (the full C2 reference run took 749 s on the GPU "
+             f"box's 16 host cores, 1.12 GFLOP/s: profiles/r2_ref_full_c2.jsonl)")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "GFLOP/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * med, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
