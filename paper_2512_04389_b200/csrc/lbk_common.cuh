@@ -62,6 +62,7 @@ struct DevPools {
   const int32_t* clist;     // RECT column lists
   const int32_t* maps;      // SSSSM gather/scatter maps of the DMMA path
   const int32_t* kchunks;   // SSSSM DMMA tiles: lists of active inner-dimension chunks
+  double* gemm_ws;          // split-K partial products of the DMMA SSSSM tiles
   int32_t* perm;            // per diagonal-block row: local permutation
   double* colmax;           // per diagonal-block column: max |entry| at GETRF entry
   unsigned long long* bmax; // per diagonal-block column: max |d_qc| over rows below c (bits)

@@ -54,7 +54,12 @@ struct GemmItem {
   int32_t m0, n0;
   int32_t nkc;     // < 0: every GBK-chunk of the inner dimension; else the number of listed chunks
   int64_t kc_off;  // offset of the chunk list in P.kchunks (chunks whose L rows x U columns hold entries)
+  int32_t ks, ke;  // split-K: this item's range of the tile's chunk sequence ([0, all) unsplit)
+  int32_t wslot;   // split-K: workspace slot of its partial product (-1: C -= product directly)
+  int32_t nsplit;  // reduce items: partial products of the tile, in slots wslot .. wslot + nsplit - 1
 };
+
+constexpr int GEMM_PART = GBM * GBN;  // doubles per split-K partial (thread-fragment order)
 
 struct DenseItem {
   int32_t kind;   // 0 exact GETRF, 1 GESSM strip, 2 TSTRF strip
@@ -91,19 +96,18 @@ __device__ __forceinline__ void cp_async_wait() {
 }
 
 // ------------------------------------------------------------- SSSSM ----
+__device__ __forceinline__ void gemm_epilogue(const double (&acc)[4][4][2], const GemmTask& tk, const DevPools& P,
+                                              int m0, int n0);
 __device__ __forceinline__ void gemm_map_item(const GemmItem it, const GemmTask* __restrict__ tasks, const DevPools& P,
                                               double* sm) {
   const GemmTask tk = tasks[it.task];
-  const BlockDev Lb = P.blk[tk.a], Ub = P.blk[tk.b], Cb = P.blk[tk.c];
+  const BlockDev Lb = P.blk[tk.a], Ub = P.blk[tk.b];
   const double* __restrict__ A = P.vals + Lb.ent;
   const double* __restrict__ B = P.vals + Ub.ent;
-  double* Cv = P.vals + Cb.ent;
-  const int lda = Lb.nR, ldb = Ub.nR, ldc = Cb.nR;
+  const int lda = Lb.nR, ldb = Ub.nR;
   const int M = Lb.nR, N = Ub.nC, K = tk.K;
   const int32_t* kL = tk.kL >= 0 ? P.maps + tk.kL : nullptr;
   const int32_t* kU = tk.kU >= 0 ? P.maps + tk.kU : nullptr;
-  const int32_t* rmap = tk.rmap >= 0 ? P.maps + tk.rmap : nullptr;
-  const int32_t* cmap = tk.cmap >= 0 ? P.maps + tk.cmap : nullptr;
   const int m0 = it.m0, n0 = it.n0;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t = lane & 3;
@@ -115,12 +119,13 @@ __device__ __forceinline__ void gemm_map_item(const GemmItem it, const GemmTask*
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   // inner-dimension chunks: all of them, or (k-chunk skipping) only those in which the
   // tile's L rows and U columns both hold pattern entries - the others multiply exact zeros
-  const int nk = it.nkc < 0 ? (K + GBK - 1) / GBK : it.nkc;
-  const int32_t* kcl = it.nkc < 0 ? nullptr : P.kchunks + it.kc_off;
+  const int nk = it.ke - it.ks;
+  const int32_t* kcl = (it.nkc < 0 ? nullptr : P.kchunks + it.kc_off);
+  const int kbase = it.ks;
   auto stageA = [&](int s) { return sm + s * (GBK * SA + GBN * SB); };
   auto stageB = [&](int s) { return sm + s * (GBK * SA + GBN * SB) + GBK * SA; };
   auto load = [&](int s, int kt) {
-    const int k0 = (kcl ? kcl[kt] : kt) * GBK;
+    const int k0 = (kcl ? kcl[kbase + kt] : kbase + kt) * GBK;
     double* As = stageA(s);
     double* Bs = stageB(s);
 #pragma unroll
@@ -169,6 +174,31 @@ __device__ __forceinline__ void gemm_map_item(const GemmItem it, const GemmTask*
     }
   }
   cp_async_wait<0>();
+  if (it.wslot >= 0) {  // split-K: the partial product goes to the workspace (thread-fragment order)
+    double* W = P.gemm_ws + static_cast<size_t>(it.wslot) * GEMM_PART + tid * 32;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        W[(i * 4 + j) * 2] = acc[i][j][0];
+        W[(i * 4 + j) * 2 + 1] = acc[i][j][1];
+      }
+    return;
+  }
+  gemm_epilogue(acc, tk, P, m0, n0);
+}
+
+// C(rows of L, cols of U) -= acc through the row / column scatter maps (a product row or
+// column outside the target's support only carries exact zeros and is skipped)
+__device__ __forceinline__ void gemm_epilogue(const double (&acc)[4][4][2], const GemmTask& tk, const DevPools& P,
+                                              int m0, int n0) {
+  const BlockDev Lb = P.blk[tk.a], Ub = P.blk[tk.b], Cb = P.blk[tk.c];
+  double* Cv = P.vals + Cb.ent;
+  const int ldc = Cb.nR, M = Lb.nR, N = Ub.nC;
+  const int32_t* rmap = tk.rmap >= 0 ? P.maps + tk.rmap : nullptr;
+  const int32_t* cmap = tk.cmap >= 0 ? P.maps + tk.cmap : nullptr;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = m0 + wm + i * 8 + g;
@@ -193,6 +223,29 @@ __global__ void __launch_bounds__(256) gemm_map_kernel(const GemmItem* __restric
                                                        const GemmTask* __restrict__ tasks, DevPools P) {
   extern __shared__ double sm[];
   gemm_map_item(items[blockIdx.x], tasks, P, sm);
+}
+
+// Split-K reduction: one CTA per tile sums its partial products in slot order (a fixed
+// order: deterministic) and applies the usual scatter epilogue.
+__global__ void __launch_bounds__(256) gemm_reduce_kernel(const GemmItem* __restrict__ items,
+                                                          const GemmTask* __restrict__ tasks, DevPools P) {
+  const GemmItem it = items[blockIdx.x];
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int sp = 0; sp < it.nsplit; ++sp) {
+    const double* W = P.gemm_ws + static_cast<size_t>(it.wslot + sp) * GEMM_PART + threadIdx.x * 32;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        acc[i][j][0] += W[(i * 4 + j) * 2];
+        acc[i][j][1] += W[(i * 4 + j) * 2 + 1];
+      }
+  }
+  gemm_epilogue(acc, tasks[it.task], P, it.m0, it.n0);
 }
 
 // Throttled variant for the deferred (off-critical-path) SSSSM updates: a

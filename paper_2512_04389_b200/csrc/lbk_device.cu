@@ -80,6 +80,8 @@ struct Level {
   int32_t ngemmD;
   int64_t gemmE_off;  // deferred SSSSM DMMA tiles with >= 3 levels of slack
   int32_t ngemmE;
+  int64_t gred_off;   // split-K reductions of the critical SSSSM tiles
+  int32_t ngred;
   int64_t panel_off;  // dense GESSM/TSTRF strips
   int32_t npanel;
   int32_t panel_smem;
@@ -104,6 +106,12 @@ constexpr int NBRANCH = 3;
 // Builds one level's tile-DAG for the persistent executor: tasks get a
 // priority key (elimination sub-step first); flush() orders them by key
 // (topological within every DAG) and emits counters and successor lists.
+#ifndef LBK_SPLITK
+#define LBK_SPLITK 1  // split-K for critical DMMA SSSSM launches with few tiles
+#endif
+constexpr int SPLITK_TILES = 2 * 148 * 2;  // fill ~2 waves of 2 CTAs per SM
+constexpr int SPLITK_MIN_CHUNKS = 4;       // inner chunks per part at least
+
 #ifndef LBK_CHAIN_TRSM
 #define LBK_CHAIN_TRSM 0  // 1: the diagonal LU task also solves the next step's two update operands (measured slower: the two solves then run one after the other instead of on two CTAs)
 #endif
@@ -219,6 +227,7 @@ struct lbk_ctx {
   DevBuf<GemmTask> gtasks;
   DevBuf<GemmItem> gitems;
   DevBuf<int32_t> kchunks;
+  DevBuf<double> gemm_ws;  // split-K partial products
   DevBuf<DenseItem> ditems;
   DevBuf<TileItem> titems;
   DevBuf<XTask> xtasks;
@@ -336,6 +345,7 @@ DevPools pools(lbk_ctx* c) {
   P.clist = c->clist.p;
   P.maps = c->maps.p;
   P.kchunks = c->kchunks.p;
+  P.gemm_ws = c->gemm_ws.p;
   P.perm = c->perm.p;
   P.colmax = c->colmax.p;
   P.bmax = c->bmax.p;
@@ -1256,10 +1266,11 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
                   klen += std::min(GBK, gt.K - q * GBK);
                 }
               if (act.empty()) continue;  // the tile's product is structurally zero
-              GemmItem gi{task, m0, n0, -1, 0};
+              GemmItem gi{task, m0, n0, -1, 0, 0, nkch, -1, 0};
               if (static_cast<int>(act.size()) < nkch) {
                 gi.nkc = static_cast<int32_t>(act.size());
                 gi.kc_off = static_cast<int64_t>(hkch.size());
+                gi.ke = gi.nkc;
                 hkch.insert(hkch.end(), act.begin(), act.end());
               }
               dst.push_back(gi);
@@ -1279,6 +1290,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     // ---- flatten ---------------------------------------------------------------------
     std::vector<Item> gall;
     std::vector<GemmItem> mall;
+    int64_t max_ws_slots = 0;  // split-K workspace slots (levels run one after another)
     std::vector<DenseItem> dall;
     std::vector<TileItem> tall;
     std::vector<XTask> xtasks;
@@ -1320,12 +1332,39 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       // longest tiles first (LPT): the block scheduler hands out CTAs in index order,
       // so the long inner loops start early and the level's tail is made of short tiles
       // (items write disjoint output tiles: the order does not touch the floating point)
+      // split-K for a critical launch with too few tiles to fill the GPU: a tile with enough
+      // inner chunks is cut into up to 8 parts writing partial products to a workspace, and
+      // a reduction launch adds them in slot order (deterministic) and scatters into C
+      std::vector<GemmItem> red;
+      if (LBK_SPLITK && !gem[lv].empty() && static_cast<int>(gem[lv].size()) < SPLITK_TILES) {
+        const int S = std::min(8, SPLITK_TILES / static_cast<int>(gem[lv].size()));
+        std::vector<GemmItem> out;
+        int32_t slots = 0;
+        for (const GemmItem& g0 : gem[lv]) {
+          const int nk = g0.ke - g0.ks;
+          const int parts = std::min(S, nk / SPLITK_MIN_CHUNKS);
+          if (parts < 2) {
+            out.push_back(g0);
+            continue;
+          }
+          GemmItem r = g0;
+          r.wslot = slots;
+          r.nsplit = parts;
+          red.push_back(r);
+          for (int q = 0; q < parts; ++q) {
+            GemmItem part = g0;
+            part.ks = g0.ks + static_cast<int32_t>((static_cast<int64_t>(nk) * q) / parts);
+            part.ke = g0.ks + static_cast<int32_t>((static_cast<int64_t>(nk) * (q + 1)) / parts);
+            part.wslot = slots++;
+            out.push_back(part);
+          }
+        }
+        gem[lv].swap(out);
+        max_ws_slots = std::max<int64_t>(max_ws_slots, slots);
+      }
       for (auto* v : {&gem[lv], &gemD[lv], &gemE[lv]})
-        std::stable_sort(v->begin(), v->end(), [&](const GemmItem& x, const GemmItem& y) {
-          const int32_t kx = x.nkc >= 0 ? x.nkc : (gtasks[x.task].K + GBK - 1) / GBK;
-          const int32_t ky = y.nkc >= 0 ? y.nkc : (gtasks[y.task].K + GBK - 1) / GBK;
-          return kx > ky;
-        });
+        std::stable_sort(v->begin(), v->end(),
+                         [&](const GemmItem& x, const GemmItem& y) { return x.ke - x.ks > y.ke - y.ks; });
       L.gemm_off = static_cast<int64_t>(mall.size());
       L.ngemm = static_cast<int32_t>(gem[lv].size());
       mall.insert(mall.end(), gem[lv].begin(), gem[lv].end());
@@ -1335,6 +1374,9 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       L.gemmE_off = static_cast<int64_t>(mall.size());
       L.ngemmE = static_cast<int32_t>(gemE[lv].size());
       mall.insert(mall.end(), gemE[lv].begin(), gemE[lv].end());
+      L.gred_off = static_cast<int64_t>(mall.size());
+      L.ngred = static_cast<int32_t>(red.size());
+      mall.insert(mall.end(), red.begin(), red.end());
       L.panel_off = static_cast<int64_t>(dall.size());
       L.npanel = static_cast<int32_t>(pan[lv].size());
       L.panel_smem = pan_smem[lv];
@@ -1667,6 +1709,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     LBK_CUDA(c->items.upload(gall), st);
     LBK_CUDA(c->gtasks.upload(gtasks), st);
     LBK_CUDA(c->gitems.upload(mall), st);
+    LBK_CUDA(c->gemm_ws.alloc(std::max<int64_t>(max_ws_slots, 1) * GEMM_PART), st);
     LBK_CUDA(c->kchunks.upload(hkch.empty() ? std::vector<int32_t>(1, 0) : hkch), st);
     LBK_CUDA(c->ditems.upload(dall), st);
     LBK_CUDA(c->titems.upload(tall), st);
@@ -1799,6 +1842,7 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
       cudaStreamWaitEvent(c->aux[0], c->fork, 0);
       rec(1, c->aux[0]);
       if (L.ngemm) gemm_map_kernel<<<L.ngemm, 256, GEMM_SMEM, c->aux[0]>>>(c->gitems.p + L.gemm_off, c->gtasks.p, P);
+      if (L.ngred) gemm_reduce_kernel<<<L.ngred, 256, 0, c->aux[0]>>>(c->gitems.p + L.gred_off, c->gtasks.p, P);
       if (inline_defer) {
         if (L.ngemmD)
           gemm_map_kernel<<<L.ngemmD, 256, GEMM_SMEM, c->aux[0]>>>(c->gitems.p + L.gemmD_off, c->gtasks.p, P);
