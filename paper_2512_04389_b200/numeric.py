@@ -163,9 +163,12 @@ class _Recycle:
         self.key, self.arr = key, arr
 
     def __del__(self):
-        free = _PINNED_FREE.setdefault(self.key, [])
-        if len(free) < _PINNED_KEEP:
-            free.append(self.arr)
+        try:
+            free = _PINNED_FREE.setdefault(self.key, [])
+            if len(free) < _PINNED_KEEP:
+                free.append(self.arr)
+        except Exception:  # pragma: no cover - interpreter shutdown
+            pass
 
 
 def pinned_recycled(count, dtype=np.float64) -> np.ndarray:
