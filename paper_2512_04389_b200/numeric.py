@@ -771,6 +771,11 @@ def engine_for(grid, tree, *, device: int = 0, dense: bool = False, chunk: int =
         eng = None
     if eng is None:
         cache.pop(key, None)
+        # one plan per grid and mode: the variant with the other `refine` setting (static pivoting
+        # toggled between calls) is released first, so C4-sized plans never coexist
+        other = cache.pop((device, dense, chunk, dense_threshold, not refine), None)
+        if other is not None:
+            other.close()
         eng = Engine(grid, tree, device=device, chunk=chunk, dense=dense, dense_threshold=dense_threshold,
                      refine=refine)
         cache[key] = eng
