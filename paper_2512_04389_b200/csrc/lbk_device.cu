@@ -24,6 +24,7 @@
 #include <vector>
 
 #include "../../include/lbk.h"
+#include <iterator>
 #include <limits>
 #include <map>
 
@@ -106,6 +107,10 @@ constexpr int NBRANCH = 3;
 // Builds one level's tile-DAG for the persistent executor: tasks get a
 // priority key (elimination sub-step first); flush() orders them by key
 // (topological within every DAG) and emits counters and successor lists.
+#ifndef LBK_TWO_PHASE
+#define LBK_TWO_PHASE 1  // GETRF_UPD / TRSM tiles load their target before their operands are ready
+#endif
+
 #ifndef LBK_SPLITK
 #define LBK_SPLITK 1  // split-K for critical DMMA SSSSM launches with few tiles
 #endif
@@ -119,8 +124,11 @@ constexpr int SPLITK_MIN_CHUNKS = 4;       // inner chunks per part at least
 struct ExecBuilder {
   std::vector<XTask> t;
   std::vector<int64_t> key;
-  std::vector<std::vector<int>> preds;
-  int add(int type, int64_t a, int64_t d, int r, int c, int k, int32_t step, int64_t prio, std::vector<int> deps) {
+  std::vector<std::vector<int>> preds, preds2;  // phase-1 / phase-2 dependencies
+  // deps2: dependencies the task waits for only after its phase-1 loads (the target tile of
+  // GETRF_UPD / TRSM is loaded while its operands are still being produced)
+  int add(int type, int64_t a, int64_t d, int r, int c, int k, int32_t step, int64_t prio, std::vector<int> deps,
+          std::vector<int> deps2 = {}) {
     XTask x{};
     x.type = static_cast<int8_t>(type);
     x.r = static_cast<int16_t>(r);
@@ -131,10 +139,22 @@ struct ExecBuilder {
     x.step = step;
     t.push_back(x);
     key.push_back(prio);
-    std::sort(deps.begin(), deps.end());
-    deps.erase(std::unique(deps.begin(), deps.end()), deps.end());
-    if (!deps.empty() && deps.front() < 0) deps.erase(deps.begin());
-    preds.push_back(std::move(deps));
+    auto clean = [](std::vector<int>& v) {
+      std::sort(v.begin(), v.end());
+      v.erase(std::unique(v.begin(), v.end()), v.end());
+      while (!v.empty() && v.front() < 0) v.erase(v.begin());
+    };
+    clean(deps);
+    clean(deps2);
+    if (!LBK_TWO_PHASE) {  // everything in phase 1
+      deps.insert(deps.end(), deps2.begin(), deps2.end());
+      deps2.clear();
+      clean(deps);
+    }
+    std::vector<int> d1;
+    std::set_difference(deps.begin(), deps.end(), deps2.begin(), deps2.end(), std::back_inserter(d1));
+    preds.push_back(std::move(d1));
+    preds2.push_back(std::move(deps2));
     return static_cast<int>(t.size()) - 1;
   }
   // Dequeue order = descending upward rank (longest cost path to the end of
@@ -155,8 +175,10 @@ struct ExecBuilder {
     {
       // insertion order is topological (deps always name earlier tasks)
       std::vector<std::vector<int>> fwd(n);
-      for (int i = 0; i < n; ++i)
+      for (int i = 0; i < n; ++i) {
         for (int p : preds[i]) fwd[p].push_back(i);
+        for (int p : preds2[i]) fwd[p].push_back(i);
+      }
       std::vector<int64_t> rank(n, 0);
       for (int i = n - 1; i >= 0; --i) {
         int64_t m = 0;
@@ -166,9 +188,12 @@ struct ExecBuilder {
       std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return rank[x] > rank[y]; });
     }
     for (int i = 0; i < n; ++i) pos[order[i]] = i;
+    // successor entries: (task << 1) | phase
     std::vector<std::vector<int>> out(n);
-    for (int i = 0; i < n; ++i)
-      for (int p : preds[i]) out[pos[p]].push_back(pos[i]);
+    for (int i = 0; i < n; ++i) {
+      for (int p : preds[i]) out[pos[p]].push_back(pos[i] << 1);
+      for (int p : preds2[i]) out[pos[p]].push_back((pos[i] << 1) | 1);
+    }
     L->exec_off = static_cast<int64_t>(tasks->size());
     L->nexec = n;
     L->band4 = 0;
@@ -179,6 +204,7 @@ struct ExecBuilder {
     for (int i = 0; i < n; ++i) {
       tasks->push_back(t[order[i]]);
       deps0->push_back(static_cast<int32_t>(preds[order[i]].size()));
+      deps0->push_back(static_cast<int32_t>(preds2[order[i]].size()));
       sptr->push_back(acc);
       for (int s2 : out[i]) succ->push_back(s2);
       acc += static_cast<int32_t>(out[i].size());
@@ -1505,7 +1531,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           // the last update of diagonal tile kb (GEMM(kb, kb, kb-1)) is fused into
           // its LU task: one handoff and one tile round trip less per step of
           // the critical chain
-          std::vector<int> fused_deps;
+          std::vector<int> fused_deps, fused_ops;
           bool fused = false;
           std::vector<std::vector<int>> colw(nt), roww(nt);  // writers of each tile column's L / row's U part
           for (int kb = 0; kb < nt; ++kb) {
@@ -1520,7 +1546,9 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
               gdeps.insert(gdeps.end(), dl.begin(), dl.end());
               gdeps.insert(gdeps.end(), du.begin(), du.end());
             }
-            const int g = fused ? X.add(X_GETRF_UPD, b, b, kb, kb, kb - 1, stp, kb * 4, gdeps)
+            // GETRF_UPD loads its target tile before the two operand tiles exist (phase 2)
+            const int g = fused ? X.add(X_GETRF_UPD, b, b, kb, kb, kb - 1, stp, kb * 4, gdeps,
+                                        chain ? std::vector<int>{} : fused_ops)
                                 : X.add(X_GETRF, b, b, kb, kb, kb, stp, kb * 4, gdeps);
             X.t[g].chain = chain ? 1 : 0;
             fused = false;
@@ -1531,7 +1559,8 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
             for (int r = kb + 1; r < nt; ++r) {
               lt[r] = -1;
               if (!occ[q][static_cast<size_t>(kb) * nt + r]) continue;
-              lt[r] = (chain && r == kb + 1) ? g : X.add(X_TRSM_L, b, b, r, kb, kb, stp, kb * 4 + 1, prev(r, kb, {g}));
+              lt[r] = (chain && r == kb + 1) ? g
+                                             : X.add(X_TRSM_L, b, b, r, kb, kb, stp, kb * 4 + 1, prev(r, kb, {g}), {g});
               colw[kb].push_back(lt[r]);
               L_(r, kb) = lt[r];
               fin_deps.push_back(lt[r]);
@@ -1539,7 +1568,8 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
             for (int cc = kb + 1; cc < nt; ++cc) {
               ut[cc] = -1;
               if (!occ[q][static_cast<size_t>(cc) * nt + kb]) continue;
-              ut[cc] = (chain && cc == kb + 1) ? g : X.add(X_TRSM_U, b, b, kb, cc, kb, stp, kb * 4 + 1, prev(kb, cc, {g}));
+              ut[cc] = (chain && cc == kb + 1) ? g
+                                               : X.add(X_TRSM_U, b, b, kb, cc, kb, stp, kb * 4 + 1, prev(kb, cc, {g}), {g});
               roww[kb].push_back(ut[cc]);
               L_(kb, cc) = ut[cc];
             }
@@ -1550,6 +1580,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
                 if (r == kb + 1 && cc == kb + 1) {
                   fused = true;
                   fused_deps = prev(r, cc, {lt[r], ut[cc]});
+                  fused_ops = {lt[r], ut[cc]};
                   continue;
                 }
                 const int t2 = X.add(X_GEMM, b, b, r, cc, kb, stp, kb * 4 + 2, prev(r, cc, {lt[r], ut[cc]}));
@@ -1802,7 +1833,7 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
     }
     scatter_kernel<<<148 * 8, 256, 0, s0>>>(c->vin.p, c->map.p, c->vals.p, c->nnz, c->dirty.p + 1);
   if (use_exec && c->n_exec) {
-    cudaMemcpyAsync(c->xdeps.p, c->xdeps0.p, c->n_exec * sizeof(int), cudaMemcpyDeviceToDevice, s0);
+    cudaMemcpyAsync(c->xdeps.p, c->xdeps0.p, 2 * c->n_exec * sizeof(int), cudaMemcpyDeviceToDevice, s0);
     cudaMemsetAsync(c->xheads.p, 0, c->levels.size() * sizeof(int), s0);
     if (c->ndiag_rows) {  // colmax/bmax accumulate with atomic max; perms start as identity
       cudaMemsetAsync(c->colmax.p, 0, c->ndiag_rows * sizeof(double), s0);
@@ -1873,7 +1904,7 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
         X.tasks = c->xtasks.p + L.exec_off;
         X.succ_ptr = c->xsptr.p + L.sptr_off;
         X.succ = c->xsucc.p + L.succ_off;
-        X.deps = c->xdeps.p + L.exec_off;
+        X.deps = c->xdeps.p + 2 * L.exec_off;
         X.head = c->xheads.p + l;
         X.ntasks = L.nexec;
         X.trace = (evs && c->xtrace.p) ? c->xtrace.p + 8 * L.exec_off : nullptr;

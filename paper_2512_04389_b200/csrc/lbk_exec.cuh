@@ -74,8 +74,8 @@ struct XTask {
 struct XLevel {
   const XTask* tasks;
   const int32_t* succ_ptr;
-  const int32_t* succ;
-  int* deps;   // working dependency counters (reset from a pristine copy per run)
+  const int32_t* succ;  // (successor << 1) | phase
+  int* deps;   // working dependency counters, two per task (phase 1, phase 2), reset per run
   int* head;   // task counter of this level
   int ntasks;
   unsigned long long* trace;  // optional: per task [dequeue, ready, done, phase 0..3, fenced] in ns (globaltimer)
@@ -917,9 +917,19 @@ __device__ void band_getrf(const BlockDev& A, const DevPools& P, double* sm, int
   }
 }
 
+// Phase-2 dependencies: a task that loaded its target tile waits here for its operands.
+__device__ __forceinline__ void wait_phase2(volatile int* d2) {
+  if (!d2) return;
+  if (threadIdx.x == 0) {
+    while (*d2 > 0) __nanosleep(LBK_SPIN_NS);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
 template <bool kBandReg>
 __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double pivot_tol,
-                         unsigned long long* ph = nullptr) {
+                         unsigned long long* ph = nullptr, volatile int* d2 = nullptr) {
   double* T0 = sm;                  // target tile (XTP stride)
   double* T1 = sm + XREG;           // operand tile (XTP stride) / DMMA A (XS stride)
   double* T2 = sm + 2 * XREG;       // DMMA B (XS stride)
@@ -954,6 +964,7 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       const int m = A.nrows, k0 = tk.r * XT, n = min(XT, m - k0);
       double* G = P.vals + A.ent + static_cast<size_t>(k0) * m + k0;
       load_tile(T0, G, m, n, n);
+      wait_phase2(d2);  // the operand tiles of the fused update
       if (tk.type == X_GETRF_UPD) {  // the last trailing update of this tile first
         const int u0 = tk.k * XT, nu = min(XT, m - u0);
         const double* base = P.vals + A.ent;
@@ -992,8 +1003,9 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
     case X_TRSM_L: {  // rows of tile (r,k) in registers, U_kk in smem
       const int m = A.nrows, k0 = tk.k * XT, r0 = tk.r * XT, nk = min(XT, m - k0), nr = min(XT, m - r0);
       double* G = P.vals + A.ent + static_cast<size_t>(k0) * m + r0;
+      load_tile(T0, G, m, nr, nk);  // the target first: its last update is done (phase 1)
+      wait_phase2(d2);              // the factored diagonal tile
       load_tile(T1, P.vals + A.ent + static_cast<size_t>(k0) * m + k0, m, nk, nk);
-      load_tile(T0, G, m, nr, nk);
       __syncthreads();
       stamp(ph, 0);
       if (threadIdx.x < XT) rinv[threadIdx.x] = threadIdx.x < nk ? 1.0 / T1[threadIdx.x * XTP + threadIdx.x] : 1.0;
@@ -1009,8 +1021,9 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
     case X_TRSM_U: {  // columns of tile (k,c) in registers, L_kk in smem
       const int m = A.nrows, k0 = tk.k * XT, c0 = tk.c * XT, nk = min(XT, m - k0), nc = min(XT, m - c0);
       double* G = P.vals + A.ent + static_cast<size_t>(c0) * m + k0;
+      load_tile(T0, G, m, nk, nc);  // the target first (phase 1)
+      wait_phase2(d2);              // the factored diagonal tile
       load_tile(T1, P.vals + A.ent + static_cast<size_t>(k0) * m + k0, m, nk, nk);
-      load_tile(T0, G, m, nk, nc);
       __syncthreads();
       tile_left_solve_blk(T0, T1, nk);
       store_tile(G, m, T0, nk, nc);
@@ -1162,7 +1175,7 @@ __device__ __forceinline__ void exec_body(const XLevel& L, const DevPools& P, do
       const int t = atomicAdd(L.head, 1);
       if (t < L.ntasks) {
         if (L.trace) L.trace[8 * t] = gtimer();
-        volatile int* dp = L.deps + t;
+        volatile int* dp = L.deps + 2 * t;  // phase-1 dependencies
         while (*dp > 0) __nanosleep(LBK_SPIN_NS);
         __threadfence();
         if (L.trace) L.trace[8 * t + 1] = gtimer();
@@ -1173,7 +1186,7 @@ __device__ __forceinline__ void exec_body(const XLevel& L, const DevPools& P, do
     const int t = s_t;
     if (t >= L.ntasks) break;
     const XTask tk = L.tasks[t];
-    run_task<kBandReg>(tk, P, sm, pivot_tol, L.trace ? L.trace + 8 * t + 3 : nullptr);
+    run_task<kBandReg>(tk, P, sm, pivot_tol, L.trace ? L.trace + 8 * t + 3 : nullptr, L.deps + 2 * t + 1);
     // every thread fences its own tile writes before the barrier, so the
     // successor releases after it are ordered behind all of them; the
     // releases are spread over the CTA (a GETRF tile has ~2x(tiles per
@@ -1184,8 +1197,10 @@ __device__ __forceinline__ void exec_body(const XLevel& L, const DevPools& P, do
     const bool late = late_flush(tk);
     {
       const int e0 = L.succ_ptr[t], e1 = L.succ_ptr[t + 1];
-      for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x)
-        if (!late || L.tasks[L.succ[e]].type != X_FINAL) atomicSub(L.deps + L.succ[e], 1);
+      for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        const int sx = L.succ[e];
+        if (!late || L.tasks[sx >> 1].type != X_FINAL) atomicSub(L.deps + 2 * (sx >> 1) + (sx & 1), 1);
+      }
     }
     if (threadIdx.x == 0 && L.trace) L.trace[8 * t + 2] = gtimer();
     if (late) {
@@ -1193,8 +1208,10 @@ __device__ __forceinline__ void exec_body(const XLevel& L, const DevPools& P, do
       __threadfence();
       __syncthreads();
       const int e0 = L.succ_ptr[t], e1 = L.succ_ptr[t + 1];
-      for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x)
-        if (L.tasks[L.succ[e]].type == X_FINAL) atomicSub(L.deps + L.succ[e], 1);
+      for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+        const int sx = L.succ[e];
+        if (L.tasks[sx >> 1].type == X_FINAL) atomicSub(L.deps + 2 * (sx >> 1) + (sx & 1), 1);
+      }
     }
   }
 }
