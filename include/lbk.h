@@ -207,10 +207,15 @@ int lbk_level_times(lbk_ctx* ctx, double pivot_tol, double static_eps, float* ou
 
 /* Persistent-executor timeline of one instrumented replay: trace[8 x n] =
  * dequeue / dependencies-met / done, four in-task phase stamps and the
- * all-writes-fenced time (ns, globaltimer) per tile task,
+ * time its phase-2 operands were complete (ns, globaltimer) per tile task,
  * info[6 x n] = type, block, r, c, k, level.  Pass NULL buffers to get *n. */
 int lbk_exec_trace(lbk_ctx* ctx, double pivot_tol, double static_eps, uint64_t* trace, int32_t* info,
                    int64_t* n, lbk_status* st);
+
+/* The executor's task DAG behind lbk_exec_trace (analysis tooling): per launch
+ * level, nexec + 1 local successor offsets in sptr and (local successor << 1 |
+ * phase) entries in succ.  Pass NULL buffers to get *nsptr / *nsucc. */
+int lbk_exec_graph(lbk_ctx* ctx, int32_t* sptr, int32_t* succ, int64_t* nsptr, int64_t* nsucc);
 
 /* ---- 2D block-cyclic distribution (north-star subsystem 5; no reference
  * counterpart: SPEC.md:14 scopes multi-process mapping out).  Owner-computes:

@@ -38,6 +38,7 @@ struct BlockDev {
   int64_t roff, coff;    // R / C list offsets (RECT), -1 otherwise
   int64_t dg;            // diagonal blocks: offset into the per-diagonal-row pools
   int64_t lvc, lvp;      // sparse diagonal GETRF: level-column / level-pointer offsets
+  int64_t xtb1;          // executor-tiled diagonal blocks: 1 + offset of the tile boundaries (0: uniform 64)
 };
 
 struct Item {  // generic (sparse) work item: `chunk` columns/rows of one task
@@ -67,6 +68,7 @@ struct DevPools {
   double* colmax;           // per diagonal-block column: max |entry| at GETRF entry
   unsigned long long* bmax; // per diagonal-block column: max |d_qc| over rows below c (bits)
   unsigned long long* err;  // [0] zero-pivot key, [1] swap key (block<<32 | col), min wins
+  const int32_t* xtb;       // tile boundaries of executor-tiled diagonal blocks (subtree-aligned)
 };
 
 __device__ __forceinline__ double dsub_mul(double x, double l, double u) {

@@ -121,6 +121,41 @@ constexpr int SPLITK_MIN_CHUNKS = 4;       // inner chunks per part at least
 #define LBK_CHAIN_TRSM 0  // 1: the diagonal LU task also solves the next step's two update operands (measured slower: the two solves then run one after the other instead of on two CTAs)
 #endif
 
+// Tile boundaries of a diagonal block for the executor (block-local CSC of its filled,
+// structurally symmetric pattern): at most XT columns per tile, and a new tile wherever a
+// new elimination subtree starts while the current tile holds an ancestor of earlier
+// columns.  Uniform 64-column tiles straddle subtree boundaries, so tile (k+1, k) is
+// nonempty for almost every k and the LU runs as one chain through all diagonal tiles;
+// with subtree-aligned tiles independent subtrees (nested-dissection leaves inside a
+// block) become independent tile chains.  Any partition is correct: only the schedule
+// and the operation order inside the tiles change (C2 model: sum of the blocks' critical
+// paths 148 -> 65 ms).  parent(j) = min{i > j : (i, j) in the pattern},
+// fd(j) = first column of j's subtree (contiguous when the order is a postorder).
+static std::vector<int32_t> subtree_tiles(int m, const int64_t* cp, const int64_t* ri, int T) {
+  std::vector<int32_t> par(m, -1), fd(m), b{0};
+  for (int j = 0; j < m; ++j) {
+    fd[j] = j;
+    for (int64_t e = cp[j]; e < cp[j + 1]; ++e) {
+      const int r = static_cast<int>(ri[e]);
+      if (r > j && (par[j] < 0 || r < par[j])) par[j] = r;
+    }
+  }
+  for (int j = 0; j < m; ++j)
+    if (par[j] >= 0) fd[par[j]] = std::min(fd[par[j]], fd[j]);
+  int s = 0, mfd = m;
+  for (int j = 1; j < m; ++j) {
+    mfd = std::min(mfd, fd[j - 1]);  // tile [s, j) holds an ancestor of a column < s iff mfd < s
+    const bool new_subtree = par[j - 1] != j;
+    if (j - s == T || (new_subtree && mfd < s)) {
+      b.push_back(j);
+      s = j;
+      mfd = m;
+    }
+  }
+  if (m > 0) b.push_back(m);
+  return b;
+}
+
 struct ExecBuilder {
   std::vector<XTask> t;
   std::vector<int64_t> key;
@@ -258,6 +293,7 @@ struct lbk_ctx {
   DevBuf<TileItem> titems;
   DevBuf<XTask> xtasks;
   DevBuf<int32_t> xsptr, xsucc, xdeps0;
+  DevBuf<int32_t> xtb;  // executor tile boundaries per tiled diagonal block (BlockDev::xtb1)
   DevBuf<int> xdeps, xheads;
   DevBuf<int32_t> perm0;  // identity permutation per diagonal row
   int64_t n_exec = 0;
@@ -376,6 +412,7 @@ DevPools pools(lbk_ctx* c) {
   P.colmax = c->colmax.p;
   P.bmax = c->bmax.p;
   P.err = c->err.p;
+  P.xtb = c->xtb.p;
   return P;
 }
 
@@ -1321,6 +1358,8 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     std::vector<TileItem> tall;
     std::vector<XTask> xtasks;
     std::vector<int32_t> xsucc_ptr, xsucc, xdeps0;
+    std::vector<int32_t> hxtb;            // executor tile boundaries (BlockDev::xtb1)
+    std::map<int64_t, int64_t> xtb_of;
     c->levels.clear();
     c->subs.clear();
     // A GETRF-only level followed by a panel-only level run in ONE executor
@@ -1489,9 +1528,10 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         // per diagonal block factored in this launch: tile-column (L part) and
         // tile-row (U part) completion markers for merged panel work
         std::map<int64_t, std::vector<int>> coldone, rowdone;
+        std::map<int64_t, std::vector<int32_t>> xtid_of;  // diagonal row -> executor tile
         for (size_t q = 0; q < tgetrf[lv].size(); ++q) {
           const int64_t b = tgetrf[lv][q];
-          const int m = hb[b].nrows, nt = (m + XT - 1) / XT;
+          const int m = hb[b].nrows;
           const int32_t stp = static_cast<int32_t>(T_bi[b]);
           if (band.count(b)) {
             // banded diagonal block: one sweeping task per independent segment instead of
@@ -1505,10 +1545,39 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
             }
             if (merge_next) {
               const int done = X.add(X_NOP, b, b, 0, 0, 0, stp, 0, band_tasks);
-              coldone[b].assign(nt, done);
-              rowdone[b].assign(nt, done);
+              coldone[b].assign(1, done);
+              rowdone[b].assign(1, done);
+              xtid_of[b].assign(m, 0);
             }
             continue;
+          }
+          // executor tiling of this diagonal block: subtree-aligned boundaries (uniform 64
+          // columns in dense-scratch mode, where every tile is full anyway)
+          std::vector<int32_t> tb;
+          if (all_full || std::getenv("LBK_UNIFORM_TILES")) {
+            for (int x = 0; x < m; x += XT) tb.push_back(x);
+            tb.push_back(m);
+          } else {
+            tb = subtree_tiles(m, colptr + T_cp[b], rowidx + T_ent[b], XT);
+          }
+          const int nt = static_cast<int>(tb.size()) - 1;
+          if (!xtb_of.count(b)) {
+            xtb_of[b] = static_cast<int64_t>(hxtb.size());
+            hb[b].xtb1 = static_cast<int64_t>(hxtb.size()) + 1;
+            hxtb.insert(hxtb.end(), tb.begin(), tb.end());
+          }
+          std::vector<int32_t> tid_of(m);
+          for (int x = 0; x < nt; ++x)
+            for (int y = tb[x]; y < tb[x + 1]; ++y) tid_of[y] = x;
+          xtid_of[b] = tid_of;
+          // xocc[col tile * nt + row tile]: tiles holding pattern entries
+          std::vector<char> xocc(static_cast<size_t>(nt) * nt, all_full ? 1 : 0);
+          if (!all_full) {
+            const int64_t* scp = colptr + T_cp[b];
+            const int64_t* sri = rowidx + T_ent[b];
+            for (int col = 0; col < m; ++col)
+              for (int64_t e = scp[col]; e < scp[col + 1]; ++e)
+                xocc[static_cast<size_t>(tid_of[col]) * nt + tid_of[sri[e]]] = 1;
           }
           // column maxima at GETRF entry: tasks over (column tile, row chunk of
           // COLMAX_ROWS); every first write into column tile c waits for all of
@@ -1538,8 +1607,8 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
             // chain: this step's LU task also solves L(kb+1, kb) and U(kb, kb+1), the operands
             // of the next diagonal update (both tiles present), so the critical chain has one
             // task and one handoff per step instead of three and two
-            const bool chain = LBK_CHAIN_TRSM && kb + 1 < nt && occ[q][static_cast<size_t>(kb) * nt + kb + 1] &&
-                               occ[q][static_cast<size_t>(kb + 1) * nt + kb];
+            const bool chain = LBK_CHAIN_TRSM && kb + 1 < nt && xocc[static_cast<size_t>(kb) * nt + kb + 1] &&
+                               xocc[static_cast<size_t>(kb + 1) * nt + kb];
             std::vector<int> gdeps = fused ? fused_deps : prev(kb, kb, {});
             if (chain) {
               const std::vector<int> dl = prev(kb + 1, kb, {}), du = prev(kb, kb + 1, {});
@@ -1558,7 +1627,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
             fin_deps.push_back(g);
             for (int r = kb + 1; r < nt; ++r) {
               lt[r] = -1;
-              if (!occ[q][static_cast<size_t>(kb) * nt + r]) continue;
+              if (!xocc[static_cast<size_t>(kb) * nt + r]) continue;
               lt[r] = (chain && r == kb + 1) ? g
                                              : X.add(X_TRSM_L, b, b, r, kb, kb, stp, kb * 4 + 1, prev(r, kb, {g}), {g});
               colw[kb].push_back(lt[r]);
@@ -1567,7 +1636,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
             }
             for (int cc = kb + 1; cc < nt; ++cc) {
               ut[cc] = -1;
-              if (!occ[q][static_cast<size_t>(cc) * nt + kb]) continue;
+              if (!xocc[static_cast<size_t>(cc) * nt + kb]) continue;
               ut[cc] = (chain && cc == kb + 1) ? g
                                                : X.add(X_TRSM_U, b, b, kb, cc, kb, stp, kb * 4 + 1, prev(kb, cc, {g}), {g});
               roww[kb].push_back(ut[cc]);
@@ -1661,7 +1730,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
             if (!has_marks) return -1;
             const int idx = std::min(static_cast<int>(Rd.size()), (kt + 1) * XT) - 1;
             const auto& v = pt[0] == 1 ? coldone[dblk] : rowdone[dblk];
-            return v[std::min(static_cast<int>(v.size()) - 1, Rd[idx] / XT)];
+            return v[std::min(static_cast<int>(v.size()) - 1, xtid_of.at(dblk)[Rd[idx]])];
           };
           if (pt[0] == 1) {  // GESSM: forward substitution down the row blocks
             for (int kb = 0; kb < tr; ++kb)
@@ -1748,6 +1817,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     LBK_CUDA(c->xsptr.upload(xsucc_ptr), st);
     LBK_CUDA(c->xsucc.upload(xsucc), st);
     LBK_CUDA(c->xdeps0.upload(xdeps0), st);
+    LBK_CUDA(c->xtb.upload(hxtb.empty() ? std::vector<int32_t>(1, 0) : hxtb), st);
     LBK_CUDA(c->xdeps.alloc(xdeps0.size()), st);
     LBK_CUDA(c->xheads.alloc(c->levels.size()), st);
     LBK_CUDA(c->perm.alloc(ndiag), st);
@@ -2613,6 +2683,20 @@ int lbk_exec_trace(lbk_ctx* c, double pivot_tol, double static_eps, uint64_t* tr
     }
   c->xtrace.release();
   ok(st);
+  return 0;
+}
+
+// The executor's per-launch task DAG (analysis tooling): sptr[sum(nexec + 1)] = per launch level,
+// local successor offsets; succ[*nsucc] = (local successor << 1) | phase.  NULL buffers: sizes only.
+int lbk_exec_graph(lbk_ctx* c, int32_t* sptr, int32_t* succ, int64_t* nsptr, int64_t* nsucc) {
+  *nsptr = static_cast<int64_t>(c->xsptr.n);
+  *nsucc = static_cast<int64_t>(c->xsucc.n);
+  if (!sptr || !succ) return 0;
+  if (cudaSetDevice(c->device) != cudaSuccess) return LBK_ERR_CUDA;
+  if (c->xsptr.n && cudaMemcpy(sptr, c->xsptr.p, c->xsptr.n * sizeof(int32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return LBK_ERR_CUDA;
+  if (c->xsucc.n && cudaMemcpy(succ, c->xsucc.p, c->xsucc.n * sizeof(int32_t), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return LBK_ERR_CUDA;
   return 0;
 }
 

@@ -78,7 +78,7 @@ struct XLevel {
   int* deps;   // working dependency counters, two per task (phase 1, phase 2), reset per run
   int* head;   // task counter of this level
   int ntasks;
-  unsigned long long* trace;  // optional: per task [dequeue, ready, done, phase 0..3, fenced] in ns (globaltimer)
+  unsigned long long* trace;  // optional: per task [dequeue, ready, done, phase 0..3, operands complete] in ns (globaltimer)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -115,6 +115,12 @@ __device__ __forceinline__ double rcp_fast(double x) {
   r = fma(r, e, r);
   r = fabs(x) < 1e-300 ? copysign(__longlong_as_double(0x7ff0000000000000LL), x) : r;
   return isinf(x) ? copysign(0.0, x) : r;
+}
+
+// First column of executor tile t of diagonal block A (subtree-aligned boundaries, or
+// uniform 64-column tiles when the plan recorded none); tile t spans [xo(t), xo(t + 1)).
+__device__ __forceinline__ int xo(const DevPools& P, const BlockDev& A, int t) {
+  return A.xtb1 ? __ldg(P.xtb + (A.xtb1 - 1) + t) : min(t * XT, A.nrows);
 }
 
 // acc_c -= sum_k l[k] * B(k, c) for the columns c = c0, c0 + 4, ... < ce, three
@@ -918,11 +924,13 @@ __device__ void band_getrf(const BlockDev& A, const DevPools& P, double* sm, int
 }
 
 // Phase-2 dependencies: a task that loaded its target tile waits here for its operands.
-__device__ __forceinline__ void wait_phase2(volatile int* d2) {
+// (trace: the time the operands were complete goes to slot 7 of the task's record)
+__device__ __forceinline__ void wait_phase2(volatile int* d2, unsigned long long* ph = nullptr) {
   if (!d2) return;
   if (threadIdx.x == 0) {
     while (*d2 > 0) __nanosleep(LBK_SPIN_NS);
     __threadfence();
+    if (ph) ph[4] = gtimer();
   }
   __syncthreads();
 }
@@ -937,36 +945,51 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
   const BlockDev A = P.blk[tk.a];
   switch (tk.type) {
     case X_COLMAX: {  // rows [r*COLMAX_ROWS, ...) of column tile c: atomic max into colmax
-      const int m = A.nrows, c0 = tk.c * XT, nc = min(XT, m - c0);
+      const int m = A.nrows, c0 = xo(P, A, tk.c), nc = xo(P, A, tk.c + 1) - c0;
       const int rb = tk.r * COLMAX_ROWS, re = min(m, rb + COLMAX_ROWS);
       const double* G = P.vals + A.ent;
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
       unsigned long long* cmax = reinterpret_cast<unsigned long long*>(P.colmax) + A.dg;
-      for (int c = c0 + warp; c < c0 + nc; c += nw) {
-        const double* col = G + static_cast<size_t>(c) * m;
-        double mx0 = 0.0, mx1 = 0.0, mx2 = 0.0, mx3 = 0.0;
-        int r = rb + lane;
-        for (; r + 96 < re; r += 128) {
-          mx0 = fmax(mx0, fabs(ldcg(col + r)));
-          mx1 = fmax(mx1, fabs(ldcg(col + r + 32)));
-          mx2 = fmax(mx2, fabs(ldcg(col + r + 64)));
-          mx3 = fmax(mx3, fabs(ldcg(col + r + 96)));
+      // two columns per round, 2 x 8 coalesced loads of a lane in flight at once
+      // (latency-bound otherwise: one L2/HBM round trip per 4 loads)
+      static_assert(COLMAX_ROWS == 16 * 32, "16 loads per lane and column");
+      for (int c = c0 + 2 * warp; c < c0 + nc; c += 2 * nw) {
+        const bool two = c + 1 < c0 + nc;
+        const double* col0 = G + static_cast<size_t>(c) * m;
+        const double* col1 = G + static_cast<size_t>(two ? c + 1 : c) * m;
+        double mx = 0.0, my = 0.0;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double v0[8], v1[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int r = rb + lane + 32 * (8 * h + j);
+            v0[j] = r < re ? ldcg(col0 + r) : 0.0;
+            v1[j] = r < re ? ldcg(col1 + r) : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            mx = fmax(mx, fabs(v0[j]));
+            my = fmax(my, fabs(v1[j]));
+          }
         }
-        for (; r < re; r += 32) mx0 = fmax(mx0, fabs(ldcg(col + r)));
-        double mx = fmax(fmax(mx0, mx1), fmax(mx2, mx3));
-        for (int o = 16; o; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        for (int o = 16; o; o >>= 1) {
+          mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          my = fmax(my, __shfl_xor_sync(0xffffffffu, my, o));
+        }
         if (lane == 0 && mx > 0.0) atomic_max_nonneg(cmax + c, mx);
+        if (lane == 0 && two && my > 0.0) atomic_max_nonneg(cmax + c + 1, my);
       }
       break;
     }
     case X_GETRF:
     case X_GETRF_UPD: {
-      const int m = A.nrows, k0 = tk.r * XT, n = min(XT, m - k0);
+      const int m = A.nrows, k0 = xo(P, A, tk.r), n = xo(P, A, tk.r + 1) - k0;
       double* G = P.vals + A.ent + static_cast<size_t>(k0) * m + k0;
       load_tile(T0, G, m, n, n);
-      wait_phase2(d2);  // the operand tiles of the fused update
+      wait_phase2(d2, ph);  // the operand tiles of the fused update
       if (tk.type == X_GETRF_UPD) {  // the last trailing update of this tile first
-        const int u0 = tk.k * XT, nu = min(XT, m - u0);
+        const int u0 = xo(P, A, tk.k), nu = xo(P, A, tk.k + 1) - u0;
         const double* base = P.vals + A.ent;
         load_opA(T1, base + static_cast<size_t>(u0) * m + k0, m, n, nu);
         load_opB(T2, base + static_cast<size_t>(k0) * m + u0, m, nu, n);
@@ -983,7 +1006,7 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       if (tk.chain) {
         // the critical chain of the diagonal block continues through L(k+1, k) and U(k, k+1):
         // solve them here with the factored tile still in shared memory (no handoff, no reload)
-        const int r0 = k0 + XT, nr = min(XT, m - r0);
+        const int r0 = k0 + n, nr = xo(P, A, tk.r + 2) - r0;
         __syncthreads();
         load_tile(T1, P.vals + A.ent + static_cast<size_t>(k0) * m + r0, m, nr, n);  // L tile (r0, k0)
         if (threadIdx.x < XT) rinv[threadIdx.x] = threadIdx.x < n ? 1.0 / T0[threadIdx.x * XTP + threadIdx.x] : 1.0;
@@ -1001,10 +1024,11 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       break;
     }
     case X_TRSM_L: {  // rows of tile (r,k) in registers, U_kk in smem
-      const int m = A.nrows, k0 = tk.k * XT, r0 = tk.r * XT, nk = min(XT, m - k0), nr = min(XT, m - r0);
+      const int m = A.nrows, k0 = xo(P, A, tk.k), r0 = xo(P, A, tk.r), nk = xo(P, A, tk.k + 1) - k0,
+                nr = xo(P, A, tk.r + 1) - r0;
       double* G = P.vals + A.ent + static_cast<size_t>(k0) * m + r0;
       load_tile(T0, G, m, nr, nk);  // the target first: its last update is done (phase 1)
-      wait_phase2(d2);              // the factored diagonal tile
+      wait_phase2(d2, ph);              // the factored diagonal tile
       load_tile(T1, P.vals + A.ent + static_cast<size_t>(k0) * m + k0, m, nk, nk);
       __syncthreads();
       stamp(ph, 0);
@@ -1019,10 +1043,11 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       break;
     }
     case X_TRSM_U: {  // columns of tile (k,c) in registers, L_kk in smem
-      const int m = A.nrows, k0 = tk.k * XT, c0 = tk.c * XT, nk = min(XT, m - k0), nc = min(XT, m - c0);
+      const int m = A.nrows, k0 = xo(P, A, tk.k), c0 = xo(P, A, tk.c), nk = xo(P, A, tk.k + 1) - k0,
+                nc = xo(P, A, tk.c + 1) - c0;
       double* G = P.vals + A.ent + static_cast<size_t>(c0) * m + k0;
       load_tile(T0, G, m, nk, nc);  // the target first (phase 1)
-      wait_phase2(d2);              // the factored diagonal tile
+      wait_phase2(d2, ph);              // the factored diagonal tile
       load_tile(T1, P.vals + A.ent + static_cast<size_t>(k0) * m + k0, m, nk, nk);
       __syncthreads();
       tile_left_solve_blk(T0, T1, nk);
@@ -1030,8 +1055,8 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       break;
     }
     case X_GEMM: {
-      const int m = A.nrows, k0 = tk.k * XT, r0 = tk.r * XT, c0 = tk.c * XT;
-      const int nk = min(XT, m - k0), nr = min(XT, m - r0), nc = min(XT, m - c0);
+      const int m = A.nrows, k0 = xo(P, A, tk.k), r0 = xo(P, A, tk.r), c0 = xo(P, A, tk.c);
+      const int nk = xo(P, A, tk.k + 1) - k0, nr = xo(P, A, tk.r + 1) - r0, nc = xo(P, A, tk.c + 1) - c0;
       const double* base = P.vals + A.ent;
       double* G = P.vals + A.ent + static_cast<size_t>(c0) * m + r0;
       load_tile(T0, G, m, nr, nc);
@@ -1156,12 +1181,11 @@ __device__ void run_late_flush(const XTask& tk, const DevPools& P, double* sm) {
   double* T1 = sm + XREG;
   double* T2 = sm + 2 * XREG;
   const BlockDev A = P.blk[tk.a];
-  const int m = A.nrows;
   if (tk.type == X_TRSM_L) {
-    const int k0 = tk.k * XT, r0 = tk.r * XT, nk = min(XT, m - k0), nr = min(XT, m - r0);
+    const int k0 = xo(P, A, tk.k), r0 = xo(P, A, tk.r), nk = xo(P, A, tk.k + 1) - k0, nr = xo(P, A, tk.r + 1) - r0;
     flush_colmax(T2, nr, nk, true, P.bmax + A.dg + k0, T1);
   } else {
-    const int k0 = tk.r * XT, n = min(XT, m - k0);
+    const int k0 = xo(P, A, tk.r), n = xo(P, A, tk.r + 1) - k0;
     flush_colmax(T1, n, n, false, P.bmax + A.dg + k0, T2);
   }
 }
@@ -1193,7 +1217,6 @@ __device__ __forceinline__ void exec_body(const XLevel& L, const DevPools& P, do
     // column) successors: one thread walking them costs an L2 round trip each)
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0 && L.trace) L.trace[8 * t + 7] = gtimer();
     const bool late = late_flush(tk);
     {
       const int e0 = L.succ_ptr[t], e1 = L.succ_ptr[t + 1];
@@ -1216,7 +1239,7 @@ __device__ __forceinline__ void exec_body(const XLevel& L, const DevPools& P, do
   }
 }
 
-__global__ void __launch_bounds__(256) exec_kernel(XLevel L, DevPools P, double pivot_tol) {
+__global__ void __launch_bounds__(256, 2) exec_kernel(XLevel L, DevPools P, double pivot_tol) {
   exec_body<false>(L, P, pivot_tol);
 }
 

@@ -75,6 +75,7 @@ def _dev():
     d(lib, "lbk_download_work", C.c_int, [vp, f64p, i64p, st])
     d(lib, "lbk_exec_trace", C.c_int, [vp, C.c_double, C.c_double, C.POINTER(C.c_uint64), i32p, i64p, st])
     d(lib, "lbk_plan_levels", C.c_int, [vp, i64p, i32p])
+    d(lib, "lbk_exec_graph", C.c_int, [vp, i32p, i32p, i64p, i64p])
     d(lib, "lbk_set_task_mask", C.c_int, [vp, C.c_int64, i8p, st])
     d(lib, "lbk_set_cuts", C.c_int, [vp, C.c_int64, i8p, st])
     d(lib, "lbk_set_task_defer", C.c_int, [vp, C.c_int64, i8p, st])
@@ -500,6 +501,18 @@ class Engine:
                                 P(info, i32p), C.byref(n), C.byref(st))
         _native.raise_status(st, "lbk_exec_trace")
         return tr, info
+
+    def exec_graph(self):
+        """(sptr, succ) of the executor's task DAG: per launch level nexec + 1 local successor
+        offsets, entries (local successor << 1) | phase (analysis tooling, scripts/exec_dag.py)."""
+        ns, ne = C.c_int64(), C.c_int64()
+        self.lib.lbk_exec_graph(self.ctx, None, None, C.byref(ns), C.byref(ne))
+        sptr = np.zeros(max(ns.value, 1), np.int32)
+        succ = np.zeros(max(ne.value, 1), np.int32)
+        rc = self.lib.lbk_exec_graph(self.ctx, P(sptr, i32p), P(succ, i32p), C.byref(ns), C.byref(ne))
+        if rc:
+            raise DeviceError(f"lbk_exec_graph: code {rc}")
+        return sptr[: ns.value], succ[: ne.value]
 
     def task_routes(self) -> np.ndarray:
         """Kernel family per task: -1 skipped, 0 CSC, 1 DMMA SSSSM, 2 panel, 3 tiled GETRF."""
