@@ -131,8 +131,12 @@ constexpr int SPLITK_MIN_CHUNKS = 4;       // inner chunks per part at least
 // and the operation order inside the tiles change (C2 model: sum of the blocks' critical
 // paths 148 -> 65 ms).  parent(j) = min{i > j : (i, j) in the pattern},
 // fd(j) = first column of j's subtree (contiguous when the order is a postorder).
-static std::vector<int32_t> subtree_tiles(int m, const int64_t* cp, const int64_t* ri, int T) {
+// seg[j] (optional): index of the subtree-cut region holding column j (the panel solves
+// of the block's row / column cut their chain dimension where it changes).
+static std::vector<int32_t> subtree_tiles(int m, const int64_t* cp, const int64_t* ri, int T, int minw,
+                                          std::vector<int32_t>* seg = nullptr) {
   std::vector<int32_t> par(m, -1), fd(m), b{0};
+  if (seg) seg->assign(m, 0);
   for (int j = 0; j < m; ++j) {
     fd[j] = j;
     for (int64_t e = cp[j]; e < cp[j + 1]; ++e) {
@@ -146,14 +150,52 @@ static std::vector<int32_t> subtree_tiles(int m, const int64_t* cp, const int64_
   for (int j = 1; j < m; ++j) {
     mfd = std::min(mfd, fd[j - 1]);  // tile [s, j) holds an ancestor of a column < s iff mfd < s
     const bool new_subtree = par[j - 1] != j;
-    if (j - s == T || (new_subtree && mfd < s)) {
+    const bool cut = new_subtree && mfd < s && j - s >= minw;
+    if (j - s == T || cut) {
       b.push_back(j);
       s = j;
       mfd = m;
     }
+    if (seg) (*seg)[j] = (*seg)[j - 1] + (cut ? 1 : 0);
   }
   if (m > 0) b.push_back(m);
   return b;
+}
+
+// Modelled critical path (us) of a diagonal block's tile LU under tiling tb: the executor's
+// tile DAG (GETRF -> TRSM_L / TRSM_U -> GEMM updates, per-tile update chains, structurally
+// empty tiles skipped) with per-task latencies measured on B200 (a task costs a fixed part
+// plus a part per column of its elimination tile, ~0.8 us per handoff).  Used to keep the
+// subtree-aligned tiling only where it shortens the chain: on blocks whose subtrees are
+// tiny it fragments the tiles and lengthens it (C5's border blocks).
+static double tile_cp_model(int m, const int64_t* cp, const int64_t* ri, const std::vector<int32_t>& tb) {
+  const int nt = static_cast<int>(tb.size()) - 1;
+  if (nt <= 0) return 0.0;
+  std::vector<int32_t> tid(m);
+  for (int x = 0; x < nt; ++x)
+    for (int y = tb[x]; y < tb[x + 1]; ++y) tid[y] = x;
+  std::vector<char> occ(static_cast<size_t>(nt) * nt, 0);  // [row tile * nt + col tile]
+  for (int j = 0; j < m; ++j)
+    for (int64_t e = cp[j]; e < cp[j + 1]; ++e) occ[static_cast<size_t>(tid[ri[e]]) * nt + tid[j]] = 1;
+  std::vector<double> rd(static_cast<size_t>(nt) * nt, 0.0);
+  auto R = [&](int r, int c) -> double& { return rd[static_cast<size_t>(r) * nt + c]; };
+  auto O = [&](int r, int c) { return occ[static_cast<size_t>(r) * nt + c] != 0; };
+  constexpr double H = 0.8;
+  for (int k = 0; k < nt; ++k) {
+    const double w = tb[k + 1] - tb[k];
+    const double tg = R(k, k) + H + 5.0 + 0.27 * w;
+    R(k, k) = tg;
+    for (int r = k + 1; r < nt; ++r) {
+      if (O(r, k)) R(r, k) = std::max(R(r, k), tg) + H + 3.0 + 0.1 * w;
+      if (O(k, r)) R(k, r) = std::max(R(k, r), tg) + H + 3.0 + 0.1 * w;
+    }
+    for (int c = k + 1; c < nt; ++c) {
+      if (!O(k, c)) continue;
+      for (int r = k + 1; r < nt; ++r)
+        if (O(r, k)) R(r, c) = std::max({R(r, c), R(r, k), R(k, c)}) + H + 4.0 + 0.06 * w;
+    }
+  }
+  return *std::max_element(rd.begin(), rd.end());
 }
 
 struct ExecBuilder {
@@ -1360,6 +1402,46 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     std::vector<int32_t> xsucc_ptr, xsucc, xdeps0;
     std::vector<int32_t> hxtb;            // executor tile boundaries (BlockDev::xtb1)
     std::map<int64_t, int64_t> xtb_of;
+    // executor tiling of a diagonal block: subtree-aligned boundaries + subtree-cut region
+    // per column (uniform 64 columns / one region in dense-scratch mode or LBK_UNIFORM_TILES)
+    struct DiagTiling {
+      std::vector<int32_t> tb, seg;
+    };
+    std::map<int64_t, DiagTiling> dtiling;
+    auto diag_tiling = [&](int64_t b) -> const DiagTiling& {
+      auto it = dtiling.find(b);
+      if (it != dtiling.end()) return it->second;
+      DiagTiling& t = dtiling[b];
+      const int m = hb[b].nrows;
+      if (all_full || std::getenv("LBK_UNIFORM_TILES")) {
+        for (int x = 0; x < m; x += XT) t.tb.push_back(x);
+        t.tb.push_back(m);
+        t.seg.assign(m, 0);
+      } else {
+        const int64_t* bcp = colptr + T_cp[b];
+        const int64_t* bri = rowidx + T_ent[b];
+        // candidates: uniform 64-column tiles and subtree-aligned tiles with a minimum width
+        // before a cut of 1 / 8 / 16 / 32 columns; the one with the shortest modelled chain
+        // wins (uniform unless an aligned one is >= 5 % shorter and not fragmented)
+        for (int x = 0; x < m; x += XT) t.tb.push_back(x);
+        t.tb.push_back(m);
+        t.seg.assign(m, 0);
+        double best = 0.95 * tile_cp_model(m, bcp, bri, t.tb);
+        const size_t max_tiles = t.tb.size() * 3 / 2 + 1;
+        for (int minw : {1, 8, 16, 32}) {
+          std::vector<int32_t> sg;
+          std::vector<int32_t> tb = subtree_tiles(m, bcp, bri, XT, minw, &sg);
+          if (tb.size() > max_tiles) continue;
+          const double cpm = tile_cp_model(m, bcp, bri, tb);
+          if (cpm < best) {
+            best = cpm;
+            t.tb.swap(tb);
+            t.seg.swap(sg);
+          }
+        }
+      }
+      return t;
+    };
     c->levels.clear();
     c->subs.clear();
     // A GETRF-only level followed by a panel-only level run in ONE executor
@@ -1553,13 +1635,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           }
           // executor tiling of this diagonal block: subtree-aligned boundaries (uniform 64
           // columns in dense-scratch mode, where every tile is full anyway)
-          std::vector<int32_t> tb;
-          if (all_full || std::getenv("LBK_UNIFORM_TILES")) {
-            for (int x = 0; x < m; x += XT) tb.push_back(x);
-            tb.push_back(m);
-          } else {
-            tb = subtree_tiles(m, colptr + T_cp[b], rowidx + T_ent[b], XT);
-          }
+          const std::vector<int32_t>& tb = diag_tiling(b).tb;
           const int nt = static_cast<int>(tb.size()) - 1;
           if (!xtb_of.count(b)) {
             xtb_of[b] = static_cast<int64_t>(hxtb.size());
@@ -1677,7 +1753,27 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         if (merge_next) merged_into_prev[lv + 1] = 1;
         for (const auto& pt : ptasks_here) {
           const int32_t dblk = pt[1], xb = pt[2], stp = pt[3];
-          const int tr = (hb[xb].nR + XT - 1) / XT, tc = (hb[xb].nC + XT - 1) / XT;
+          const bool gessm = pt[0] == 1;
+          const std::vector<int32_t> Rx = rows_of(xb), Cx = cols_of(xb);
+          // Chain dimension (GESSM: the panel's rows R_X, TSTRF: its columns C_X) tiled at
+          // most XT wide and cut wherever the diagonal factor's subtree-cut region changes,
+          // so the substitution chains of independent subtrees are independent (the other
+          // dimension: uniform XT).  The boundaries go to BlockDev::xtb1 of the panel.
+          const std::vector<int32_t>& Dpos = gessm ? Rx : Cx;
+          const std::vector<int32_t>& dseg = diag_tiling(dblk).seg;
+          std::vector<int32_t> cb{0}, chid(Dpos.size(), 0);
+          for (size_t a = 1; a < Dpos.size(); ++a)
+            if (static_cast<int>(a) - cb.back() == XT || dseg[Dpos[a]] != dseg[Dpos[a - 1]])
+              cb.push_back(static_cast<int32_t>(a));
+          if (!Dpos.empty()) cb.push_back(static_cast<int32_t>(Dpos.size()));
+          const int nch = static_cast<int>(cb.size()) - 1;
+          for (int x = 0; x < nch; ++x)
+            for (int y = cb[x]; y < cb[x + 1]; ++y) chid[y] = x;
+          hb[xb].xtb1 = static_cast<int64_t>(hxtb.size()) + 1;
+          hxtb.insert(hxtb.end(), cb.begin(), cb.end());
+          const int tr = gessm ? nch : (hb[xb].nR + XT - 1) / XT, tc = gessm ? (hb[xb].nC + XT - 1) / XT : nch;
+          auto rtile = [&](int a) { return gessm ? chid[a] : a / XT; };
+          auto ctile = [&](int a) { return gessm ? a / XT : chid[a]; };
           std::vector<int> last(static_cast<size_t>(tr) * tc, -1);
           auto L_ = [&](int r, int cc) -> int& { return last[static_cast<size_t>(cc) * tr + r]; };
           // Tile occupancy from the filled patterns (tiled mode: no swaps, so the
@@ -1686,11 +1782,10 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           // strict L over R_X x R_X) or columns (TSTRF: strict U over C_X x C_X).
           // A panel tile outside the pattern stays zero through the solve (fill
           // closure), and a zero factor tile contributes nothing.
-          const int nd = pt[0] == 1 ? tr : tc;
+          const int nd = nch;
           std::vector<char> occX(static_cast<size_t>(tr) * tc, all_full ? 1 : 0);
           std::vector<char> occD(static_cast<size_t>(nd) * nd, all_full ? 1 : 0);
           if (!all_full) {
-            const std::vector<int32_t> Rx = rows_of(xb), Cx = cols_of(xb);
             std::vector<int32_t> rpos(hb[xb].nrows, -1), cpos(hb[xb].ncols, -1);
             for (size_t a = 0; a < Rx.size(); ++a) rpos[Rx[a]] = static_cast<int32_t>(a);
             for (size_t a = 0; a < Cx.size(); ++a) cpos[Cx[a]] = static_cast<int32_t>(a);
@@ -1698,8 +1793,8 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
             const int64_t* xri = rowidx + T_ent[xb];
             for (int col = 0; col < hb[xb].ncols; ++col)
               for (int64_t e = xcp[col]; e < xcp[col + 1]; ++e)
-                occX[static_cast<size_t>(cpos[col] / XT) * tr + rpos[xri[e]] / XT] = 1;
-            const std::vector<int32_t>& pos = pt[0] == 1 ? rpos : cpos;
+                occX[static_cast<size_t>(ctile(cpos[col])) * tr + rtile(rpos[xri[e]])] = 1;
+            const std::vector<int32_t>& pos = gessm ? rpos : cpos;
             const int64_t* dcp = colptr + T_cp[dblk];
             const int64_t* dri = rowidx + T_ent[dblk];
             for (int col = 0; col < hb[dblk].ncols; ++col) {
@@ -1707,8 +1802,8 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
               if (pc < 0) continue;
               for (int64_t e = dcp[col]; e < dcp[col + 1]; ++e) {
                 const int64_t row = dri[e];
-                const bool keep = pt[0] == 1 ? row > col : row < col;
-                if (keep && pos[row] >= 0) occD[static_cast<size_t>(pc / XT) * nd + pos[row] / XT] = 1;
+                const bool keep = gessm ? row > col : row < col;
+                if (keep && pos[row] >= 0) occD[static_cast<size_t>(chid[pc]) * nd + chid[pos[row]]] = 1;
               }
             }
           }
@@ -1725,11 +1820,11 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           // kt (rows R_kt for GESSM, columns C_kt for TSTRF) waits for the
           // diagonal factor's columns / rows up to the last of them
           const bool has_marks = merge_next && coldone.count(dblk);
-          const std::vector<int32_t> Rd = has_marks ? (pt[0] == 1 ? rows_of(xb) : cols_of(xb)) : std::vector<int32_t>();
+          const std::vector<int32_t>& Rd = Dpos;
           auto mark = [&](int kt) -> int {
             if (!has_marks) return -1;
-            const int idx = std::min(static_cast<int>(Rd.size()), (kt + 1) * XT) - 1;
-            const auto& v = pt[0] == 1 ? coldone[dblk] : rowdone[dblk];
+            const int idx = cb[kt + 1] - 1;
+            const auto& v = gessm ? coldone[dblk] : rowdone[dblk];
             return v[std::min(static_cast<int>(v.size()) - 1, xtid_of.at(dblk)[Rd[idx]])];
           };
           if (pt[0] == 1) {  // GESSM: forward substitution down the row blocks

@@ -123,6 +123,11 @@ __device__ __forceinline__ int xo(const DevPools& P, const BlockDev& A, int t) {
   return A.xtb1 ? __ldg(P.xtb + (A.xtb1 - 1) + t) : min(t * XT, A.nrows);
 }
 
+// Panel blocks: first compressed row (GESSM) / column (TSTRF) of chain tile t (lim = nR / nC).
+__device__ __forceinline__ int xop(const DevPools& P, const BlockDev& A, int t, int lim) {
+  return A.xtb1 ? __ldg(P.xtb + (A.xtb1 - 1) + t) : min(t * XT, lim);
+}
+
 // acc_c -= sum_k l[k] * B(k, c) for the columns c = c0, c0 + 4, ... < ce, three
 // independent accumulation chains at a time.  Col(c) = address of column c of
 // the target (row offset applied), Bk(c) = address of B(0, c) (k contiguous).
@@ -1087,13 +1092,14 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       const BlockDev D = P.blk[tk.d];
       const int m = D.nrows, ld = A.nR;
       const int32_t* Rl = A.store == STORE_RECT ? P.rlist + A.roff : nullptr;
-      const int r0 = tk.r * XT, c0 = tk.c * XT, nr = min(XT, A.nR - r0), nc = min(XT, A.nC - c0);
+      const int r0 = xop(P, A, tk.r, A.nR), c0 = tk.c * XT, nr = xop(P, A, tk.r + 1, A.nR) - r0,
+                nc = min(XT, A.nC - c0);
       double* G = P.vals + A.ent + static_cast<size_t>(c0) * ld + r0;
       const double* Dv = P.vals + D.ent;
       if (tk.type == X_PG_DIAG || tk.type == X_PG_FUSED) {
         load_tile(T0, G, ld, nr, nc);
         if (tk.type == X_PG_FUSED) {  // the update from the previous row step first
-          const int k0 = tk.k * XT, nk = min(XT, A.nR - k0);
+          const int k0 = xop(P, A, tk.k, A.nR), nk = xop(P, A, tk.k + 1, A.nR) - k0;
           if (Rl) load_opA(T1, Dv, m, nr, nk, Rl + r0, Rl + k0);
           else load_opA(T1, Dv + static_cast<size_t>(k0) * m + r0, m, nr, nk);
           load_opB(T2, P.vals + A.ent + static_cast<size_t>(c0) * ld + k0, ld, nk, nc);
@@ -1106,7 +1112,7 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
         tile_left_solve_blk(T0, T1, nr);
         store_tile(G, ld, T0, nr, nc);
       } else {
-        const int k0 = tk.k * XT, nk = min(XT, A.nR - k0);
+        const int k0 = xop(P, A, tk.k, A.nR), nk = xop(P, A, tk.k + 1, A.nR) - k0;
         load_tile(T0, G, ld, nr, nc);
         if (Rl) load_opA(T1, Dv, m, nr, nk, Rl + r0, Rl + k0);
         else load_opA(T1, Dv + static_cast<size_t>(k0) * m + r0, m, nr, nk);
@@ -1124,13 +1130,14 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       const BlockDev D = P.blk[tk.d];
       const int m = D.nrows, ld = A.nR;
       const int32_t* Cl = A.store == STORE_RECT ? P.clist + A.coff : nullptr;
-      const int r0 = tk.r * XT, c0 = tk.c * XT, nr = min(XT, A.nR - r0), nc = min(XT, A.nC - c0);
+      const int r0 = tk.r * XT, c0 = xop(P, A, tk.c, A.nC), nr = min(XT, A.nR - r0),
+                nc = xop(P, A, tk.c + 1, A.nC) - c0;
       double* G = P.vals + A.ent + static_cast<size_t>(c0) * ld + r0;
       const double* Dv = P.vals + D.ent;
       if (tk.type == X_PT_DIAG || tk.type == X_PT_FUSED) {
         load_tile(T0, G, ld, nr, nc);
         if (tk.type == X_PT_FUSED) {  // the update from the previous column step first
-          const int k0 = tk.k * XT, nk = min(XT, A.nC - k0);
+          const int k0 = xop(P, A, tk.k, A.nC), nk = xop(P, A, tk.k + 1, A.nC) - k0;
           load_opA(T1, P.vals + A.ent + static_cast<size_t>(k0) * ld + r0, ld, nr, nk);
           if (Cl) load_opB(T2, Dv, m, nk, nc, Cl + k0, Cl + c0);
           else load_opB(T2, Dv + static_cast<size_t>(c0) * m + k0, m, nk, nc);
@@ -1145,7 +1152,7 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
         tile_right_solve_blk<false>(T0, T1, rinv, nullptr, nc);
         store_tile(G, ld, T0, nr, nc);
       } else {
-        const int k0 = tk.k * XT, nk = min(XT, A.nC - k0);
+        const int k0 = xop(P, A, tk.k, A.nC), nk = xop(P, A, tk.k + 1, A.nC) - k0;
         load_tile(T0, G, ld, nr, nc);
         load_opA(T1, P.vals + A.ent + static_cast<size_t>(k0) * ld + r0, ld, nr, nk);
         if (Cl) load_opB(T2, Dv, m, nk, nc, Cl + k0, Cl + c0);
