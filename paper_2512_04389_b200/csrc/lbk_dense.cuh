@@ -124,40 +124,62 @@ __device__ __forceinline__ void gemm_map_item(const GemmItem it, const GemmTask*
   const int kbase = it.ks;
   auto stageA = [&](int s) { return sm + s * (GBK * SA + GBN * SB); };
   auto stageB = [&](int s) { return sm + s * (GBK * SA + GBN * SB) + GBK * SA; };
-  auto load = [&](int s, int kt) {
-    const int k0 = (kcl ? kcl[kbase + kt] : kbase + kt) * GBK;
+  // The gathered inner indices of a chunk (the chunk list entry, then kL / kU) are two
+  // dependent global loads: they are fetched one chunk ahead into registers, so the
+  // cp.async issue of chunk kt + 2 never waits on them (they were the top stall)
+  constexpr int NA = (GBK * GBM) / 256, NBL = (GBK * GBN) / 256;
+  struct ChunkIdx {
+    int k0;
+    int colA[NA];
+    int rowB;
+  };
+  auto fetch = [&](int kt, ChunkIdx& ci) {
+    ci.k0 = (kcl ? __ldg(kcl + kbase + kt) : kbase + kt) * GBK;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const int kk = (tid + i * 256) / GBM, gk = ci.k0 + kk;
+      ci.colA[i] = gk < K ? (kL ? __ldg(kL + gk) : gk) : -1;
+    }
+    const int gk = ci.k0 + (tid % GBK);
+    ci.rowB = gk < K ? (kU ? __ldg(kU + gk) : gk) : -1;
+  };
+  auto issue = [&](int s, const ChunkIdx& ci) {
     double* As = stageA(s);
     double* Bs = stageB(s);
 #pragma unroll
-    for (int i = 0; i < (GBK * GBM) / 256; ++i) {
+    for (int i = 0; i < NA; ++i) {
       const int idx = tid + i * 256;
       const int kk = idx / GBM, mm = idx % GBM;
-      const int gr = m0 + mm, gk = k0 + kk;
-      const bool v = gr < M && gk < K;
-      const int col = v ? (kL ? kL[gk] : gk) : 0;
-      cp_async8(As + kk * SA + mm, v ? A + static_cast<size_t>(col) * lda + gr : A, v);
+      const int gr = m0 + mm;
+      const bool v = gr < M && ci.colA[i] >= 0;
+      cp_async8(As + kk * SA + mm, v ? A + static_cast<size_t>(ci.colA[i]) * lda + gr : A, v);
     }
 #pragma unroll
-    for (int i = 0; i < (GBK * GBN) / 256; ++i) {
+    for (int i = 0; i < NBL; ++i) {
       const int idx = tid + i * 256;
       const int nn = idx / GBK, kk = idx % GBK;
-      const int gc = n0 + nn, gk = k0 + kk;
-      const bool v = gc < N && gk < K;
-      const int row = v ? (kU ? kU[gk] : gk) : 0;
-      cp_async8(Bs + nn * SB + kk, v ? B + static_cast<size_t>(gc) * ldb + row : B, v);
+      const int gc = n0 + nn;
+      const bool v = gc < N && ci.rowB >= 0;
+      cp_async8(Bs + nn * SB + kk, v ? B + static_cast<size_t>(gc) * ldb + ci.rowB : B, v);
     }
   };
+  ChunkIdx nxt;
 #pragma unroll
   for (int s = 0; s < GSTAGES - 1; ++s) {
-    if (s < nk) load(s, s);
+    if (s < nk) {
+      fetch(s, nxt);
+      issue(s, nxt);
+    }
     cp_async_commit();
   }
+  if (GSTAGES - 1 < nk) fetch(GSTAGES - 1, nxt);
   for (int kt = 0; kt < nk; ++kt) {
     cp_async_wait<GSTAGES - 2>();
     __syncthreads();
     const int pf = kt + GSTAGES - 1;
-    if (pf < nk) load(pf % GSTAGES, pf);
+    if (pf < nk) issue(pf % GSTAGES, nxt);
     cp_async_commit();
+    if (pf + 1 < nk) fetch(pf + 1, nxt);  // consumed next iteration: its latency hides behind this chunk
     const double* As = stageA(kt % GSTAGES);
     const double* Bs = stageB(kt % GSTAGES);
 #pragma unroll
@@ -199,27 +221,32 @@ __device__ __forceinline__ void gemm_epilogue(const double (&acc)[4][4][2], cons
   const int32_t* cmap = tk.cmap >= 0 ? P.maps + tk.cmap : nullptr;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
   const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
+  // per row group, its 8 target entries are all loaded before the first store (the maps
+  // are injective, so no entry is read after another one is written; one dependent
+  // read-modify-write per entry serialised 32 L2 round trips per thread)
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int r = m0 + wm + i * 8 + g;
-    if (r >= M) continue;
-    const int rr = rmap ? rmap[r] : r;
-    if (rr < 0) continue;  // row of L outside the product's support: contributes exact zeros
+    const int rr = r < M ? (rmap ? rmap[r] : r) : -1;  // < 0: row outside the product's support (exact zeros)
+    int cc[4][2];
+    double cv[4][2];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < 4; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = n0 + wn + j * 8 + 2 * t + h;
-        if (c >= N) continue;
-        const int cc = cmap ? cmap[c] : c;
-        if (cc < 0) continue;
-        Cv[static_cast<size_t>(cc) * ldc + rr] -= acc[i][j][h];
+        cc[j][h] = (rr >= 0 && c < N) ? (cmap ? cmap[c] : c) : -1;
+        cv[j][h] = cc[j][h] >= 0 ? Cv[static_cast<size_t>(cc[j][h]) * ldc + rr] : 0.0;
       }
-    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        if (cc[j][h] >= 0) Cv[static_cast<size_t>(cc[j][h]) * ldc + rr] = cv[j][h] - acc[i][j][h];
   }
 }
 
-__global__ void __launch_bounds__(256) gemm_map_kernel(const GemmItem* __restrict__ items,
+__global__ void __launch_bounds__(256, 2) gemm_map_kernel(const GemmItem* __restrict__ items,
                                                        const GemmTask* __restrict__ tasks, DevPools P) {
   extern __shared__ double sm[];
   gemm_map_item(items[blockIdx.x], tasks, P, sm);
@@ -227,7 +254,7 @@ __global__ void __launch_bounds__(256) gemm_map_kernel(const GemmItem* __restric
 
 // Split-K reduction: one CTA per tile sums its partial products in slot order (a fixed
 // order: deterministic) and applies the usual scatter epilogue.
-__global__ void __launch_bounds__(256) gemm_reduce_kernel(const GemmItem* __restrict__ items,
+__global__ void __launch_bounds__(256, 2) gemm_reduce_kernel(const GemmItem* __restrict__ items,
                                                           const GemmTask* __restrict__ tasks, DevPools P) {
   const GemmItem it = items[blockIdx.x];
   double acc[4][4][2];
@@ -251,7 +278,7 @@ __global__ void __launch_bounds__(256) gemm_reduce_kernel(const GemmItem* __rest
 // Throttled variant for the deferred (off-critical-path) SSSSM updates: a
 // fixed number of CTAs loop over the items, so the deferred work never holds
 // more than gridDim.x CTA slots while the next level's critical work runs.
-__global__ void __launch_bounds__(256) gemm_map_loop_kernel(const GemmItem* __restrict__ items, int n,
+__global__ void __launch_bounds__(256, 2) gemm_map_loop_kernel(const GemmItem* __restrict__ items, int n,
                                                             const GemmTask* __restrict__ tasks, DevPools P) {
   extern __shared__ double sm[];
   for (int i = blockIdx.x; i < n; i += gridDim.x) {

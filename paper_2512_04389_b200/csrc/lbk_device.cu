@@ -22,6 +22,8 @@
 #include <cstring>
 #include <new>
 #include <vector>
+#include <queue>
+#include <functional>
 
 #include "../../include/lbk.h"
 #include <iterator>
@@ -1483,13 +1485,60 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       // inner chunks is cut into up to 8 parts writing partial products to a workspace, and
       // a reduction launch adds them in slot order (deterministic) and scatters into C
       std::vector<GemmItem> red;
-      if (LBK_SPLITK && !gem[lv].empty() && static_cast<int>(gem[lv].size()) < SPLITK_TILES) {
-        const int S = std::min(8, SPLITK_TILES / static_cast<int>(gem[lv].size()));
+      // Part length: the candidate (unsplit, or parts of about 1, 1/2, 1/4, 1/8 of the level's
+      // mean chunks per CTA slot) whose greedy longest-first schedule over the 296 CTA slots
+      // has the shortest makespan, a split tile paying one extra chunk for its reduction
+      // (a level of 360 equal tiles otherwise runs as 1 full wave + a 22 % wave).
+      // LBK_SPLITK_OLD: the round-2 rule (only launches under 592 tiles).
+      int split_len = 0;  // 0: no split; else target chunks per part
+      if (LBK_SPLITK && !gem[lv].empty() && !std::getenv("LBK_SPLITK_OLD")) {
+        constexpr int SLOTS = 296;
+        int64_t total = 0;
+        for (const GemmItem& g0 : gem[lv]) total += g0.ke - g0.ks;
+        auto makespan = [&](int len) {
+          std::vector<int64_t> w;
+          for (const GemmItem& g0 : gem[lv]) {
+            const int nk = g0.ke - g0.ks;
+            const int parts = len ? std::min(8, nk / std::max(len, SPLITK_MIN_CHUNKS)) : 1;
+            if (parts < 2) {
+              w.push_back(nk);
+              continue;
+            }
+            for (int q = 0; q < parts; ++q) w.push_back((nk * (q + 1)) / parts - (nk * q) / parts + 1);
+          }
+          std::sort(w.begin(), w.end(), std::greater<int64_t>());
+          std::priority_queue<int64_t, std::vector<int64_t>, std::greater<int64_t>> pq;
+          for (int q = 0; q < SLOTS; ++q) pq.push(0);
+          int64_t mk = 0;
+          for (int64_t x : w) {
+            const int64_t t0 = pq.top();
+            pq.pop();
+            pq.push(t0 + x);
+            mk = std::max(mk, t0 + x);
+          }
+          return mk;
+        };
+        int64_t best = makespan(0);
+        const int64_t mean = std::max<int64_t>(1, total / SLOTS);
+        for (int64_t div : {1, 2, 4, 8}) {
+          const int len = static_cast<int>(std::max<int64_t>(SPLITK_MIN_CHUNKS, mean / div));
+          const int64_t mk = makespan(len);
+          if (mk * 20 < best * 19) {  // >= 5 % shorter
+            best = mk;
+            split_len = len;
+          }
+        }
+      }
+      const bool old_rule = LBK_SPLITK && std::getenv("LBK_SPLITK_OLD") && !gem[lv].empty() &&
+                            static_cast<int>(gem[lv].size()) < SPLITK_TILES;
+      if (split_len > 0 || old_rule) {
+        const int S = old_rule ? std::min(8, SPLITK_TILES / static_cast<int>(gem[lv].size())) : 8;
         std::vector<GemmItem> out;
         int32_t slots = 0;
         for (const GemmItem& g0 : gem[lv]) {
           const int nk = g0.ke - g0.ks;
-          const int parts = std::min(S, nk / SPLITK_MIN_CHUNKS);
+          const int parts = old_rule ? std::min(S, nk / SPLITK_MIN_CHUNKS)
+                                     : std::min(S, nk / std::max(split_len, SPLITK_MIN_CHUNKS));
           if (parts < 2) {
             out.push_back(g0);
             continue;
