@@ -85,6 +85,8 @@ struct Level {
   int32_t ngemmE;
   int64_t gred_off;   // split-K reductions of the critical SSSSM tiles
   int32_t ngred;
+  int64_t absorb_off;  // SSSSM tiles run as tasks of the next executor launch (exact mode: launched here)
+  int32_t nabsorb;
   int64_t panel_off;  // dense GESSM/TSTRF strips
   int32_t npanel;
   int32_t panel_smem;
@@ -262,7 +264,8 @@ struct ExecBuilder {
       for (int i = n - 1; i >= 0; --i) {
         int64_t m = 0;
         for (int s2 : fwd[i]) m = std::max(m, rank[s2]);
-        rank[i] = m + cost_of(t[i].type) + (t[i].chain ? cost_of(X_TRSM_L) + cost_of(X_TRSM_U) : 0);
+        rank[i] = m + (t[i].type == X_SSSSM ? 30 + 26 * t[i].k : cost_of(t[i].type)) +
+                  (t[i].chain ? cost_of(X_TRSM_L) + cost_of(X_TRSM_U) : 0);
       }
       std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return rank[x] > rank[y]; });
     }
@@ -1119,6 +1122,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     std::vector<int32_t> acc_len(nlevels, 1);
     std::vector<std::vector<GemmItem>> gem(nlevels), gemD(nlevels), gemE(nlevels);
     std::vector<GemmTask> gtasks;
+    std::vector<int64_t> gtask_t;  // tree task of each GemmTask
     std::vector<int32_t> hmaps;
     std::vector<std::vector<DenseItem>> pan(nlevels), exa(nlevels);
     std::vector<std::vector<std::array<int32_t, 4>>> ptask(nlevels);  // (kind, diag blk, panel blk, step)
@@ -1344,6 +1348,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           const int32_t task = static_cast<int32_t>(gtasks.size());
           c->route[t] = 1;
           gtasks.push_back(gt);
+          gtask_t.push_back(t);
           const int slack = refine ? rdefer[t] : c->defer.empty() ? 0 : c->defer[t];
           auto& dst = slack >= 3 ? gemE[lv] : slack == 2 ? gemD[lv] : gem[lv];
           // k-chunk skipping: per GBK-chunk of the inner index, the 128-row tiles of L and the
@@ -1454,6 +1459,8 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       return gen[l].empty() && gem[l].empty() && gemD[l].empty() && gemE[l].empty();
     };
     std::vector<char> merged_into_prev(nlevels, 0);
+    int32_t absorbed_lv = -2;  // SSSSM level whose DMMA tiles run inside the next executor launch
+    int64_t absorbed_off = 0, absorbed_n = 0;
     for (int32_t lv = 0; lv < nlevels; ++lv) {
       if (gen[lv].empty() && gem[lv].empty() && gemD[lv].empty() && gemE[lv].empty() && pan[lv].empty() &&
           exa[lv].empty())
@@ -1477,6 +1484,50 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         gem[lv].insert(gem[lv].end(), gemE[lv].begin(), gemE[lv].end());
         gemD[lv].clear();
         gemE[lv].clear();
+      }
+      // An SSSSM-only level followed by an executor-only GETRF level: its DMMA tiles become
+      // executor tasks of the next launch (X_SSSSM), and only the tasks of that launch that
+      // touch an updated block wait for them (the column tiles' COLMAX tasks of a diagonal
+      // block, the first writes into a panel) - no launch barrier between the updates and
+      // the next factorizations, and the executor's idle CTAs (its chains are latency-bound)
+      // run the remaining updates.  Off for distributed plans (cuts at level boundaries),
+      // dense-scratch plans and band launches.  Measured slower (C2 118.7 -> 119.9 ms, C5 7.04 ->
+      // 7.27 ms, profiles/r2_absorb_ab.txt): the updates feeding the next diagonal block's
+      // first column tiles are the longest tiles and outrank every chain task, so the chain
+      // starts no earlier - kept as a variant, LBK_ABSORB=1.
+      auto no_band = [&](int32_t l) {
+        for (int64_t b : tgetrf[l])
+          if (band.count(b)) return false;
+        return true;
+      };
+      const bool absorb = c->use_exec && !all_full && c->cut_after.empty() && std::getenv("LBK_ABSORB") &&
+                          lv + 1 < nlevels && !gem[lv].empty() && gen[lv].empty() && exa[lv].empty() &&
+                          tgetrf[lv].empty() && ptask[lv].empty() && !merged_into_prev[lv] &&
+                          !tgetrf[lv + 1].empty() && gen[lv + 1].empty() && gem[lv + 1].empty() &&
+                          gemD[lv + 1].empty() && gemE[lv + 1].empty() && no_band(lv + 1);
+      if (absorb) {
+        std::stable_sort(gem[lv].begin(), gem[lv].end(),
+                         [&](const GemmItem& x, const GemmItem& y) { return x.ke - x.ks > y.ke - y.ks; });
+        absorbed_lv = lv;
+        absorbed_off = static_cast<int64_t>(mall.size());
+        absorbed_n = static_cast<int64_t>(gem[lv].size());
+        L.absorb_off = absorbed_off;
+        L.nabsorb = static_cast<int32_t>(absorbed_n);
+        mall.insert(mall.end(), gem[lv].begin(), gem[lv].end());
+        for (const GemmItem& gi : gem[lv]) {
+          const GemmTask& gt = gtasks[gi.task];
+          c->route[gtask_t[gi.task]] = 3;
+          const int64_t klen = gi.nkc < 0 ? gt.K : [&] {
+            int64_t kl = 0;
+            for (int q = 0; q < gi.nkc; ++q) kl += std::min(GBK, gt.K - hkch[gi.kc_off + q] * GBK);
+            return kl;
+          }();
+          const double xf = 2.0 * std::min(GBM, hb[gt.a].nR - gi.m0) * static_cast<double>(klen) *
+                            std::min(GBN, hb[gt.b].nC - gi.n0);
+          c->dmma_flops -= xf;
+          c->exec_flops += xf;
+        }
+        gem[lv].clear();
       }
       // longest tiles first (LPT): the block scheduler hands out CTAs in index order,
       // so the long inner loops start early and the level's tail is made of short tiles
@@ -1660,6 +1711,33 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         // tile-row (U part) completion markers for merged panel work
         std::map<int64_t, std::vector<int>> coldone, rowdone;
         std::map<int64_t, std::vector<int32_t>> xtid_of;  // diagonal row -> executor tile
+        // absorbed DMMA SSSSM tiles of the previous level: (task, first and last target column)
+        // per target block
+        std::map<int64_t, std::vector<std::array<int32_t, 3>>> upd_of;
+        if (absorbed_lv == lv - 1) {
+          for (int64_t q = 0; q < absorbed_n; ++q) {
+            const GemmItem& gi = mall[absorbed_off + q];
+            const GemmTask& gt = gtasks[gi.task];
+            const int nk = gi.ke - gi.ks;
+            const int x = X.add(X_SSSSM, absorbed_off + q, gt.c, 0, 0, std::min(nk, 32767), 0, 0, {});
+            int32_t lo = INT32_MAX, hi = -1;
+            for (int n = gi.n0; n < std::min(gi.n0 + GBN, hb[gt.b].nC); ++n) {
+              const int32_t cc = gt.cmap >= 0 ? hmaps[gt.cmap + n] : n;
+              if (cc < 0) continue;
+              lo = std::min(lo, cc);
+              hi = std::max(hi, cc);
+            }
+            if (hi >= 0) upd_of[gt.c].push_back({x, lo, hi});
+          }
+        }
+        auto upd_cols = [&](int64_t blk, int c0, int c1) {  // absorbed updates of target columns [c0, c1)
+          std::vector<int> v;
+          auto it = upd_of.find(blk);
+          if (it != upd_of.end())
+            for (const auto& u : it->second)
+              if (u[1] < c1 && u[2] >= c0) v.push_back(u[0]);
+          return v;
+        };
         for (size_t q = 0; q < tgetrf[lv].size(); ++q) {
           const int64_t b = tgetrf[lv][q];
           const int m = hb[b].nrows;
@@ -1711,7 +1789,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           std::vector<std::vector<int>> colj(nt);
           for (int cc = 0; cc < nt; ++cc)
             for (int rc = 0; rc * COLMAX_ROWS < m; ++rc) {
-              const int col = X.add(X_COLMAX, b, b, rc, cc, 0, stp, -1, {});
+              const int col = X.add(X_COLMAX, b, b, rc, cc, 0, stp, -1, upd_cols(b, tb[cc], tb[cc + 1]));
               colj[cc].push_back(col);
               fin_deps.push_back(col);
             }
@@ -1876,6 +1954,12 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
             const auto& v = gessm ? coldone[dblk] : rowdone[dblk];
             return v[std::min(static_cast<int>(v.size()) - 1, xtid_of.at(dblk)[Rd[idx]])];
           };
+          // first writes into a panel tile wait for the absorbed updates of the panel
+          const std::vector<int> xupd = upd_cols(xb, INT32_MIN, INT32_MAX);
+          auto fw = [&](std::vector<int> v, int r, int cc) {
+            if (L_(r, cc) < 0) v.insert(v.end(), xupd.begin(), xupd.end());
+            return v;
+          };
           if (pt[0] == 1) {  // GESSM: forward substitution down the row blocks
             for (int kb = 0; kb < tr; ++kb)
               for (int cc = 0; cc < tc; ++cc) {
@@ -1883,16 +1967,16 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
                 if (P_(kb, cc) >= 0) PD_(kb, cc).push_back(mark(kb));
                 const int d = P_(kb, cc) >= 0
                                   ? X.add(X_PG_FUSED, xb, dblk, kb, cc, P_(kb, cc), stp, kb * 4 + 1, PD_(kb, cc))
-                                  : X.add(X_PG_DIAG, xb, dblk, kb, cc, kb, stp, kb * 4 + 1, {L_(kb, cc), mark(kb)});
+                                  : X.add(X_PG_DIAG, xb, dblk, kb, cc, kb, stp, kb * 4 + 1, fw({L_(kb, cc), mark(kb)}, kb, cc));
                 L_(kb, cc) = d;
                 for (int r = kb + 1; r < tr; ++r)
                   if (X_(r, cc) && D_(r, kb)) {  // L tile (r, kb)
                     if (r == kb + 1) {
                       P_(r, cc) = kb;
-                      PD_(r, cc) = {d, L_(r, cc)};
+                      PD_(r, cc) = fw({d, L_(r, cc)}, r, cc);
                       continue;
                     }
-                    L_(r, cc) = X.add(X_PG_UPD, xb, dblk, r, cc, kb, stp, kb * 4 + 2, {d, L_(r, cc), mark(kb)});
+                    L_(r, cc) = X.add(X_PG_UPD, xb, dblk, r, cc, kb, stp, kb * 4 + 2, fw({d, L_(r, cc), mark(kb)}, r, cc));
                   }
               }
           } else {  // TSTRF: substitution along the column blocks
@@ -1902,21 +1986,22 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
                 if (P_(r, kb) >= 0) PD_(r, kb).push_back(mark(kb));
                 const int d = P_(r, kb) >= 0
                                   ? X.add(X_PT_FUSED, xb, dblk, r, kb, P_(r, kb), stp, kb * 4 + 1, PD_(r, kb))
-                                  : X.add(X_PT_DIAG, xb, dblk, r, kb, kb, stp, kb * 4 + 1, {L_(r, kb), mark(kb)});
+                                  : X.add(X_PT_DIAG, xb, dblk, r, kb, kb, stp, kb * 4 + 1, fw({L_(r, kb), mark(kb)}, r, kb));
                 L_(r, kb) = d;
                 for (int cc = kb + 1; cc < tc; ++cc)
                   if (X_(r, cc) && D_(kb, cc)) {  // U tile (kb, cc)
                     if (cc == kb + 1) {
                       P_(r, cc) = kb;
-                      PD_(r, cc) = {d, L_(r, cc)};
+                      PD_(r, cc) = fw({d, L_(r, cc)}, r, cc);
                       continue;
                     }
-                    L_(r, cc) = X.add(X_PT_UPD, xb, dblk, r, cc, kb, stp, kb * 4 + 2, {d, L_(r, cc), mark(kb)});
+                    L_(r, cc) = X.add(X_PT_UPD, xb, dblk, r, cc, kb, stp, kb * 4 + 2, fw({d, L_(r, cc), mark(kb)}, r, cc));
                   }
               }
           }
         }
         for (const XTask& x : X.t) {  // executed flops of the tile tasks (full 64-tiles)
+          if (x.type == X_SSSSM) continue;  // counted when absorbed
           const double t3 = 64.0 * 64.0 * 64.0;
           if (x.chain) c->exec_flops += 2 * t3;  // the two solved tiles of the chain
           c->exec_flops += x.type == X_GETRF_UPD                                     ? 2 * t3 + 2 * t3 / 3
@@ -2076,8 +2161,9 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
     // level, after its critical DMMA launch: every kernel family is then timed
     // without the cross-level overlap (which only shares the GPU differently)
     const bool inline_defer = evs != nullptr && (L.ngemmD || L.ngemmE);
-    const bool br[NBRANCH] = {L.ngemm > 0 || inline_defer, (!use_exec && L.npanel > 0) || (exact && L.nexact > 0),
-                              has_t};
+    const bool own_absorbed = L.nabsorb > 0 && (exact || !use_exec);  // no executor launch to run them
+    const bool br[NBRANCH] = {L.ngemm > 0 || inline_defer || own_absorbed,
+                              (!use_exec && L.npanel > 0) || (exact && L.nexact > 0), has_t};
     // instrumented replays: per level [end, gemm b/e, panel b/e, getrf b/e, csc b/e]
     auto rec = [&](int k, cudaStream_t s) {
       if (evs) cudaEventRecordWithFlags((*evs)[1 + l * 13 + k], s, cudaEventRecordExternal);
@@ -2087,6 +2173,8 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
       cudaStreamWaitEvent(c->aux[0], c->fork, 0);
       rec(1, c->aux[0]);
       if (L.ngemm) gemm_map_kernel<<<L.ngemm, 256, GEMM_SMEM, c->aux[0]>>>(c->gitems.p + L.gemm_off, c->gtasks.p, P);
+      if (own_absorbed)
+        gemm_map_kernel<<<L.nabsorb, 256, GEMM_SMEM, c->aux[0]>>>(c->gitems.p + L.absorb_off, c->gtasks.p, P);
       if (L.ngred) gemm_reduce_kernel<<<L.ngred, 256, 0, c->aux[0]>>>(c->gitems.p + L.gred_off, c->gtasks.p, P);
       if (inline_defer) {
         if (L.ngemmD)
@@ -2122,6 +2210,8 @@ void capture_factorization(lbk_ctx* c, double pivot_tol, double static_eps, std:
         X.head = c->xheads.p + l;
         X.ntasks = L.nexec;
         X.trace = (evs && c->xtrace.p) ? c->xtrace.p + 8 * L.exec_off : nullptr;
+        X.gitems = c->gitems.p;
+        X.gtasks = c->gtasks.p;
         if (L.band4 && c->use_bandreg) {
           const int grid = std::max(1, std::min(L.nexec, 148 * std::min(c->exec_per_sm, c->band_per_sm)));
           exec_band_kernel<<<grid, 256, EXEC_SMEM, s2>>>(X, P, pivot_tol);

@@ -41,6 +41,7 @@ constexpr int XTP = XT + 1;     // padded smem column stride
 constexpr int XS = XT + 4;      // DMMA operand stride
 constexpr int XREG = XT * XS;   // one smem tile region (fits either stride)
 constexpr int EXEC_SMEM = (3 * XREG + 4 * XT) * 8;
+static_assert(GEMM_SMEM <= EXEC_SMEM, "absorbed DMMA SSSSM tiles run in the executor's shared memory");
 constexpr int COLMAX_ROWS = 512;  // rows per colmax task
 
 enum XType : int8_t {
@@ -59,6 +60,7 @@ enum XType : int8_t {
   X_PG_FUSED = 12,   // GESSM: X_PG_UPD from step k into tile (r,c), then X_PG_DIAG of (r,c)
   X_PT_FUSED = 13,   // TSTRF: X_PT_UPD from step k into tile (r,c), then X_PT_DIAG of (r,c)
   X_NOP = 14,        // dependency marker (tile column / row of a diagonal factor complete)
+  X_SSSSM = 15,      // DMMA SSSSM output tile a (index into the GemmItems) of the previous level (absorbed)
 };
 
 struct XTask {
@@ -78,6 +80,8 @@ struct XLevel {
   int* deps;   // working dependency counters, two per task (phase 1, phase 2), reset per run
   int* head;   // task counter of this level
   int ntasks;
+  const GemmItem* gitems;     // X_SSSSM tasks: the DMMA SSSSM items and their tasks
+  const GemmTask* gtasks;
   unsigned long long* trace;  // optional: per task [dequeue, ready, done, phase 0..3, operands complete] in ns (globaltimer)
 };
 
@@ -940,13 +944,24 @@ __device__ __forceinline__ void wait_phase2(volatile int* d2, unsigned long long
   __syncthreads();
 }
 
+// the DMMA SSSSM pipeline of an absorbed update tile (inlined: a call would spill)
+__device__ __forceinline__ void run_ssssm(const GemmItem* gitems, const GemmTask* gtasks, int item, const DevPools& P,
+                                       double* sm) {
+  gemm_map_item(gitems[item], gtasks, P, sm);
+}
+
 template <bool kBandReg>
 __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double pivot_tol,
-                         unsigned long long* ph = nullptr, volatile int* d2 = nullptr) {
+                         unsigned long long* ph = nullptr, volatile int* d2 = nullptr,
+                         const GemmItem* gitems = nullptr, const GemmTask* gtasks = nullptr) {
   double* T0 = sm;                  // target tile (XTP stride)
   double* T1 = sm + XREG;           // operand tile (XTP stride) / DMMA A (XS stride)
   double* T2 = sm + 2 * XREG;       // DMMA B (XS stride)
   double* rinv = sm + 3 * XREG;     // XT doubles
+  if (tk.type == X_SSSSM) {  // (tk.a indexes the SSSSM items, not the blocks)
+    run_ssssm(gitems, gtasks, tk.a, P, sm);
+    return;
+  }
   const BlockDev A = P.blk[tk.a];
   switch (tk.type) {
     case X_COLMAX: {  // rows [r*COLMAX_ROWS, ...) of column tile c: atomic max into colmax
@@ -1217,7 +1232,8 @@ __device__ __forceinline__ void exec_body(const XLevel& L, const DevPools& P, do
     const int t = s_t;
     if (t >= L.ntasks) break;
     const XTask tk = L.tasks[t];
-    run_task<kBandReg>(tk, P, sm, pivot_tol, L.trace ? L.trace + 8 * t + 3 : nullptr, L.deps + 2 * t + 1);
+    run_task<kBandReg>(tk, P, sm, pivot_tol, L.trace ? L.trace + 8 * t + 3 : nullptr, L.deps + 2 * t + 1, L.gitems,
+                       L.gtasks);
     // every thread fences its own tile writes before the barrier, so the
     // successor releases after it are ordered behind all of them; the
     // releases are spread over the CTA (a GETRF tile has ~2x(tiles per

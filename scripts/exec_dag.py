@@ -17,7 +17,7 @@ import numpy as np
 sys.path.insert(0, ".")
 
 NAMES = ["COLMAX", "GETRF", "TRSM_L", "TRSM_U", "GEMM", "FINAL", "PG_DIAG", "PG_UPD", "PT_DIAG", "PT_UPD",
-         "BAND", "GETRF_UPD", "PG_FUSED", "PT_FUSED", "NOP"]
+         "BAND", "GETRF_UPD", "PG_FUSED", "PT_FUSED", "NOP", "SSSSM"]
 
 
 def capture(cfg, out):

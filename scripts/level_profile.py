@@ -15,7 +15,7 @@ import bench  # noqa: E402
 from paper_2512_04389_b200.numeric import Engine  # noqa: E402
 
 NAMES = ["COLMAX", "GETRF", "TRSM_L", "TRSM_U", "GEMM", "FINAL", "PG_DIAG", "PG_UPD", "PT_DIAG", "PT_UPD",
-         "BAND", "GETRF_UPD", "PG_FUSED", "PT_FUSED", "NOP"]
+         "BAND", "GETRF_UPD", "PG_FUSED", "PT_FUSED", "NOP", "SSSSM"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("cfg")
