@@ -1494,13 +1494,13 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       // dense-scratch plans and band launches.  Measured slower (C2 118.7 -> 119.9 ms, C5 7.04 ->
       // 7.27 ms, profiles/r2_absorb_ab.txt): the updates feeding the next diagonal block's
       // first column tiles are the longest tiles and outrank every chain task, so the chain
-      // starts no earlier - kept as a variant, LBK_ABSORB=1.
+      // starts no earlier - kept as a variant (-DLBK_ABSORB_TILES=1 and LBK_ABSORB=1).
       auto no_band = [&](int32_t l) {
         for (int64_t b : tgetrf[l])
           if (band.count(b)) return false;
         return true;
       };
-      const bool absorb = c->use_exec && !all_full && c->cut_after.empty() && std::getenv("LBK_ABSORB") &&
+      const bool absorb = LBK_ABSORB_TILES && c->use_exec && !all_full && c->cut_after.empty() && std::getenv("LBK_ABSORB") &&
                           lv + 1 < nlevels && !gem[lv].empty() && gen[lv].empty() && exa[lv].empty() &&
                           tgetrf[lv].empty() && ptask[lv].empty() && !merged_into_prev[lv] &&
                           !tgetrf[lv + 1].empty() && gen[lv + 1].empty() && gem[lv + 1].empty() &&

@@ -584,6 +584,159 @@ __device__ void tile_lu64_blocked(double* T, int n, double* Dd, double* urow, lo
   __syncthreads();
 }
 
+#ifndef LBK_LU_LA
+#define LBK_LU_LA 0  // 1: tile LU with a one-panel lookahead (measured slower: C2 118.5 -> 122.2 ms, profiles/r2_lu_la_ab.txt)
+#endif
+
+// Panel [pb, pe) (pe - pb <= 8) of the n x n tile T factored by warp 0 (the one-warp
+// shuffle panel of tile_lu64_blocked, PB = 8).
+__device__ __noinline__ void panel8_w0(double* T, int pb, int n, double* Dd) {
+  constexpr int PB = 8;
+  const int lane = threadIdx.x & 31, ra = lane, rb = lane + 32;
+  double pa[PB], pc[PB];
+#pragma unroll
+  for (int i = 0; i < PB; ++i) {
+    pa[i] = T[(pb + i) * XTP + ra];
+    pc[i] = T[(pb + i) * XTP + rb];
+  }
+#pragma unroll
+  for (int jj = 0; jj < PB; ++jj) {
+    const int j = pb + jj;
+    if (j < n) {
+      const int src = j & 31;
+      const bool hi = j >= 32;
+      double u[PB];
+#pragma unroll
+      for (int i = jj; i < PB; ++i) u[i] = __shfl_sync(0xffffffffu, hi ? pc[i] : pa[i], src);
+      const double rinv = rcp_nr(u[jj]);
+      if (ra > j && ra < n) {
+        const double d = pa[jj];
+        Dd[j * XTP + ra] = fabs(d);
+        const double l = d * rinv;
+        pa[jj] = l;
+#pragma unroll
+        for (int i = jj + 1; i < PB; ++i) pa[i] = fma(-l, u[i], pa[i]);
+      }
+      if (rb > j && rb < n) {
+        const double d = pc[jj];
+        Dd[j * XTP + rb] = fabs(d);
+        const double l = d * rinv;
+        pc[jj] = l;
+#pragma unroll
+        for (int i = jj + 1; i < PB; ++i) pc[i] = fma(-l, u[i], pc[i]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < PB; ++i) {
+    if (ra >= pb) T[(pb + i) * XTP + ra] = pa[i];
+    if (rb >= pb) T[(pb + i) * XTP + rb] = pc[i];
+  }
+}
+
+// LU of the n x n tile with a one-panel lookahead: after panel p (8 columns) is factored,
+// warp 0 alone brings the NEXT panel's columns up to date (U12 rows + rank-8 update) and
+// factors it right away, while warps 1-7 update the rest of the trailing matrix - the
+// trailing update leaves the panel chain (one barrier per panel instead of three).  Every
+// entry sees the same operations in the same order as tile_lu64_blocked (same fma
+// sequence over k, same U12 substitution): bitwise identical factors, staged |d| included.
+__device__ void tile_lu64_la(double* T, int n, double* Dd) {
+  constexpr int PB = 8;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid < 32) panel8_w0(T, 0, n, Dd);
+  __syncthreads();
+#pragma unroll 1
+  for (int pb = 0;; pb += PB) {
+    const int pe = min(n, pb + PB);
+    if (pe >= n) break;
+    const int pe2 = min(n, pe + PB);
+    if (tid < 32) {
+      // U12 of the next panel's columns c in [pe, pe2): lanes 0..7, one column each
+      if (lane < pe2 - pe) {
+        const int c = pe + lane;
+        double x[PB];
+#pragma unroll
+        for (int i = 0; i < PB; ++i) x[i] = T[c * XTP + pb + i];
+#pragma unroll
+        for (int k = 0; k < PB; ++k)
+#pragma unroll
+          for (int i = k + 1; i < PB; ++i) x[i] = fma(-T[(pb + k) * XTP + pb + i], x[k], x[i]);
+#pragma unroll
+        for (int i = 0; i < PB; ++i) T[c * XTP + pb + i] = x[i];
+      }
+      __syncwarp();
+      // rank-8 update of those columns, rows >= pe: lane owns rows pe + lane and pe + lane + 32
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = pe + lane + 32 * h;
+        if (r < n) {
+          double l[PB];
+#pragma unroll
+          for (int k = 0; k < PB; ++k) l[k] = T[(pb + k) * XTP + r];
+#pragma unroll
+          for (int j = 0; j < PB; ++j) {
+            const int c = pe + j;
+            if (c < pe2) {
+              double a = T[c * XTP + r];
+#pragma unroll
+              for (int k = 0; k < PB; ++k) a = fma(-l[k], T[c * XTP + pb + k], a);
+              T[c * XTP + r] = a;
+            }
+          }
+        }
+      }
+      __syncwarp();
+      panel8_w0(T, pe, n, Dd);
+    } else {
+      const int t2 = tid - 32, nt2 = blockDim.x - 32;
+      // U12 of the remaining columns [pe2, n)
+      for (int c = pe2 + t2; c < n; c += nt2) {
+        double x[PB];
+#pragma unroll
+        for (int i = 0; i < PB; ++i) x[i] = T[c * XTP + pb + i];
+#pragma unroll
+        for (int k = 0; k < PB; ++k)
+#pragma unroll
+          for (int i = k + 1; i < PB; ++i) x[i] = fma(-T[(pb + k) * XTP + pb + i], x[k], x[i]);
+#pragma unroll
+        for (int i = 0; i < PB; ++i) T[c * XTP + pb + i] = x[i];
+      }
+      asm volatile("bar.sync 2, %0;" ::"r"(nt2) : "memory");
+      // rows >= pe, columns >= pe2 in 4 x 4 register tiles
+      const int R = n - pe, C = n - pe2, RG = (R + 3) / 4, CG = (C + 3) / 4;
+      for (int u = t2; u < RG * CG; u += nt2) {
+        const int rg = u % RG, c0 = pe2 + 4 * (u / RG);
+        int rr[4];
+        double a[4][4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          rr[i] = pe + rg + i * RG;
+#pragma unroll
+          for (int j = 0; j < 4; ++j) a[i][j] = (rr[i] < n && c0 + j < n) ? T[(c0 + j) * XTP + rr[i]] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < PB; ++k) {
+          double l[4], w[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) l[i] = T[(pb + k) * XTP + min(rr[i], XT - 1)];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) w[j] = T[min(c0 + j, XT - 1) * XTP + pb + k];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) a[i][j] = fma(-l[i], w[j], a[i][j]);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (rr[i] < n && c0 + j < n) T[(c0 + j) * XTP + rr[i]] = a[i][j];
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // bmax[j] (global, bits) = max over rows r > j (r < nr) of the staged |d_rj|;
 // rows_all: the whole column is "below" (TRSM_L tiles).
 // Thread (column c = tid & 63, row quarter tid >> 6) reduces 16 independent
@@ -944,6 +1097,10 @@ __device__ __forceinline__ void wait_phase2(volatile int* d2, unsigned long long
   __syncthreads();
 }
 
+#ifndef LBK_ABSORB_TILES
+#define LBK_ABSORB_TILES 0  // 1: executor runs absorbed DMMA SSSSM tiles (LBK_ABSORB=1 plans; measured slower)
+#endif
+
 // the DMMA SSSSM pipeline of an absorbed update tile (inlined: a call would spill)
 __device__ __forceinline__ void run_ssssm(const GemmItem* gitems, const GemmTask* gtasks, int item, const DevPools& P,
                                        double* sm) {
@@ -958,10 +1115,12 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
   double* T1 = sm + XREG;           // operand tile (XTP stride) / DMMA A (XS stride)
   double* T2 = sm + 2 * XREG;       // DMMA B (XS stride)
   double* rinv = sm + 3 * XREG;     // XT doubles
+#if LBK_ABSORB_TILES
   if (tk.type == X_SSSSM) {  // (tk.a indexes the SSSSM items, not the blocks)
     run_ssssm(gitems, gtasks, tk.a, P, sm);
     return;
   }
+#endif
   const BlockDev A = P.blk[tk.a];
   switch (tk.type) {
     case X_COLMAX: {  // rows [r*COLMAX_ROWS, ...) of column tile c: atomic max into colmax
@@ -1018,7 +1177,11 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       }
       __syncthreads();
       stamp(ph, 0);
+#if LBK_LU_LA
+      tile_lu64_la(T0, n, T1);
+#else
       tile_lu64_blocked(T0, n, T1, rinv);
+#endif
       stamp(ph, 1);
       store_tile(G, m, T0, n, n);
       if (!LBK_LATE_FLUSH || tk.chain) flush_colmax(T1, n, n, false, P.bmax + A.dg + k0, T2);
