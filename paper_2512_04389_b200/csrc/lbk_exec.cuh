@@ -42,7 +42,7 @@ constexpr int XS = XT + 4;      // DMMA operand stride
 constexpr int XREG = XT * XS;   // one smem tile region (fits either stride)
 constexpr int EXEC_SMEM = (3 * XREG + 4 * XT) * 8;
 static_assert(GEMM_SMEM <= EXEC_SMEM, "absorbed DMMA SSSSM tiles run in the executor's shared memory");
-constexpr int COLMAX_ROWS = 512;  // rows per colmax task
+constexpr int COLMAX_ROWS = 128;  // rows per colmax task (GETRF's first tile waits for a whole column of them)
 
 enum XType : int8_t {
   X_COLMAX = 0,  // colmax / bmax / perm reset of column tile c of diagonal block a
@@ -1129,35 +1129,31 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       const double* G = P.vals + A.ent;
       const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
       unsigned long long* cmax = reinterpret_cast<unsigned long long*>(P.colmax) + A.dg;
-      // two columns per round, 2 x 8 coalesced loads of a lane in flight at once
-      // (latency-bound otherwise: one L2/HBM round trip per 4 loads)
-      static_assert(COLMAX_ROWS == 16 * 32, "16 loads per lane and column");
-      for (int c = c0 + 2 * warp; c < c0 + nc; c += 2 * nw) {
-        const bool two = c + 1 < c0 + nc;
-        const double* col0 = G + static_cast<size_t>(c) * m;
-        const double* col1 = G + static_cast<size_t>(two ? c + 1 : c) * m;
-        double mx = 0.0, my = 0.0;
+      // four columns per round, 4 x 4 coalesced loads of a lane in flight at once
+      // (latency-bound otherwise: the chain of a block starts after its first column's colmax)
+      static_assert(COLMAX_ROWS == 4 * 32, "4 loads per lane and column");
+      for (int cb = c0 + 4 * warp; cb < c0 + nc; cb += 4 * nw) {
+        double v[4][4];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          double v0[8], v1[8];
+        for (int q = 0; q < 4; ++q) {
+          const double* col = G + static_cast<size_t>(min(cb + q, c0 + nc - 1)) * m;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int r = rb + lane + 32 * (8 * h + j);
-            v0[j] = r < re ? ldcg(col0 + r) : 0.0;
-            v1[j] = r < re ? ldcg(col1 + r) : 0.0;
-          }
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            mx = fmax(mx, fabs(v0[j]));
-            my = fmax(my, fabs(v1[j]));
+          for (int j = 0; j < 4; ++j) {
+            const int r = rb + lane + 32 * j;
+            v[q][j] = r < re ? ldcg(col + r) : 0.0;
           }
         }
-        for (int o = 16; o; o >>= 1) {
-          mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-          my = fmax(my, __shfl_xor_sync(0xffffffffu, my, o));
+        double mq[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          mq[q] = fmax(fmax(fabs(v[q][0]), fabs(v[q][1])), fmax(fabs(v[q][2]), fabs(v[q][3])));
+#pragma unroll
+          for (int o = 16; o; o >>= 1) mq[q] = fmax(mq[q], __shfl_xor_sync(0xffffffffu, mq[q], o));
         }
-        if (lane == 0 && mx > 0.0) atomic_max_nonneg(cmax + c, mx);
-        if (lane == 0 && two && my > 0.0) atomic_max_nonneg(cmax + c + 1, my);
+        if (lane < 4 && cb + lane < c0 + nc) {
+          const double mv = lane == 0 ? mq[0] : lane == 1 ? mq[1] : lane == 2 ? mq[2] : mq[3];
+          if (mv > 0.0) atomic_max_nonneg(cmax + cb + lane, mv);
+        }
       }
       break;
     }
