@@ -287,3 +287,45 @@ def test_segment_refined_schedule_is_bitwise_identical(n, border, bodies, seed):
     (v0, p0), l0 = out[1]
     assert v1.tobytes() == v0.tobytes() and p1.tobytes() == p0.tobytes()
     print(f"launch levels: refined {l1}, block-level {l0}")
+
+
+@pytest.mark.parametrize("n,bs", [(16, None), (16, 1024), (20, 2000)])
+def test_subtree_aligned_tiles_vs_uniform_and_oracle(monkeypatch, n, bs):
+    """Executor tiling (lbk_device.cu subtree_tiles / tile_cp_model): diagonal blocks tiled along
+    their elimination subtrees and panel chains cut at the same subtree regions give the same
+    factors as uniform 64-column tiles (LBK_UNIFORM_TILES=1) within the FP64 tolerance, every
+    value checked against the oracle; the task DAGs differ (the aligned tiling was chosen)."""
+    from paper_2512_04389_b200.numeric import Engine
+
+    a = G.poisson3d(n, "nd")
+    g, t = pipeline(a, bs)
+    res = {}
+    for mode in ("uniform", "aligned"):  # (the drop-in factorize below then plans aligned tiles)
+        if mode == "uniform":
+            monkeypatch.setenv("LBK_UNIFORM_TILES", "1")
+        else:
+            monkeypatch.delenv("LBK_UNIFORM_TILES", raising=False)
+        e = Engine(g, t)
+        e.upload()
+        e.run_device()
+        vals, perms = e.download()
+        e.run_device()
+        assert e.download()[0].tobytes() == vals.tobytes()  # deterministic under either tiling
+        _, info = e.exec_trace()
+        res[mode] = (vals, perms, info)
+        e.close()
+    (va, pa, ia), (vu, pu, iu) = res["aligned"], res["uniform"]
+    assert np.array_equal(pa, pu)
+    amax = np.abs(a.values).max()
+    np.testing.assert_allclose(va, vu, rtol=0, atol=1e-11 * amax)
+    if bs is not None:  # blocks of several subtrees: the aligned tiling differs from the uniform one
+        assert len(ia) != len(iu) or not np.array_equal(ia, iu)
+    f = M.factorize(g, t)
+    oa = OS.Csc(a.n, a.col_ptr, a.row_idx, a.values)
+    og = OS.partition(a.n, *OS.symbolic(OS.symmetrize(oa)), oa, g.plan.positions)
+    state, _ = ON.factorize(og, OS.levels(og))
+    lb, ub = ON.export(state)
+    for blocks, ob in ((f.l_blocks, lb), (f.u_blocks, ub)):
+        assert set(blocks) == set(ob)
+        for k in ob:
+            np.testing.assert_allclose(blocks[k].values, ob[k].values, rtol=0, atol=1e-11 * amax)
