@@ -1715,11 +1715,29 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         // per target block
         std::map<int64_t, std::vector<std::array<int32_t, 3>>> upd_of;
         if (absorbed_lv == lv - 1) {
+          // long tiles run as a chain of pieces of <= LBK_ABSORB_PIECE inner chunks (each piece
+          // C -= its partial product, in k order: deterministic), so a CTA is never held for a
+          // whole K loop and the chain tasks of the launch interleave with the updates
+          const char* pc = std::getenv("LBK_ABSORB_PIECE");
+          const int piece = pc ? std::max(1, std::atoi(pc)) : 16;
           for (int64_t q = 0; q < absorbed_n; ++q) {
-            const GemmItem& gi = mall[absorbed_off + q];
+            const GemmItem gi = mall[absorbed_off + q];
             const GemmTask& gt = gtasks[gi.task];
             const int nk = gi.ke - gi.ks;
-            const int x = X.add(X_SSSSM, absorbed_off + q, gt.c, 0, 0, std::min(nk, 32767), 0, 0, {});
+            const int np_ = std::max(1, (nk + piece - 1) / piece);
+            int x = -1;
+            for (int pq = 0; pq < np_; ++pq) {
+              int64_t idx = absorbed_off + q;
+              GemmItem part = gi;
+              if (np_ > 1) {
+                part.ks = gi.ks + static_cast<int32_t>((static_cast<int64_t>(nk) * pq) / np_);
+                part.ke = gi.ks + static_cast<int32_t>((static_cast<int64_t>(nk) * (pq + 1)) / np_);
+                idx = static_cast<int64_t>(mall.size());
+                mall.push_back(part);
+              }
+              x = X.add(X_SSSSM, idx, gt.c, 0, 0, std::min(part.ke - part.ks, 32767), 0, 0,
+                        x >= 0 ? std::vector<int>{x} : std::vector<int>{});
+            }
             int32_t lo = INT32_MAX, hi = -1;
             for (int n = gi.n0; n < std::min(gi.n0 + GBN, hb[gt.b].nC); ++n) {
               const int32_t cc = gt.cmap >= 0 ? hmaps[gt.cmap + n] : n;
