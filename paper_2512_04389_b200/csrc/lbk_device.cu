@@ -22,6 +22,7 @@
 #include <cstring>
 #include <new>
 #include <vector>
+#include <set>
 #include <queue>
 #include <functional>
 
@@ -206,6 +207,8 @@ struct ExecBuilder {
   std::vector<XTask> t;
   std::vector<int64_t> key;
   std::vector<std::vector<int>> preds, preds2;  // phase-1 / phase-2 dependencies
+  std::set<std::pair<int, int>> early;          // (chain-2 GETRF task, successor released after its LU)
+  void mark_early(int p, int s) { early.insert({p, s}); }
   // deps2: dependencies the task waits for only after its phase-1 loads (the target tile of
   // GETRF_UPD / TRSM is loaded while its operands are still being produced)
   int add(int type, int64_t a, int64_t d, int r, int c, int k, int32_t step, int64_t prio, std::vector<int> deps,
@@ -265,16 +268,22 @@ struct ExecBuilder {
         int64_t m = 0;
         for (int s2 : fwd[i]) m = std::max(m, rank[s2]);
         rank[i] = m + (t[i].type == X_SSSSM ? 30 + 26 * t[i].k : cost_of(t[i].type)) +
-                  (t[i].chain ? cost_of(X_TRSM_L) + cost_of(X_TRSM_U) : 0);
+                  (t[i].chain == 1 ? cost_of(X_TRSM_L) + cost_of(X_TRSM_U) : t[i].chain == 2 ? cost_of(X_TRSM_L) : 0);
       }
       std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return rank[x] > rank[y]; });
     }
     for (int i = 0; i < n; ++i) pos[order[i]] = i;
-    // successor entries: (task << 1) | phase
-    std::vector<std::vector<int>> out(n);
+    // successor entries: (task << 1) | phase; a chain-2 GETRF task lists its early successors
+    // first and records their count in pad1
+    std::vector<std::vector<int>> out(n), out_early(n);
     for (int i = 0; i < n; ++i) {
-      for (int p : preds[i]) out[pos[p]].push_back(pos[i] << 1);
-      for (int p : preds2[i]) out[pos[p]].push_back((pos[i] << 1) | 1);
+      for (int p : preds[i]) (early.count({p, i}) ? out_early : out)[pos[p]].push_back(pos[i] << 1);
+      for (int p : preds2[i]) (early.count({p, i}) ? out_early : out)[pos[p]].push_back((pos[i] << 1) | 1);
+    }
+    for (int q = 0; q < n; ++q) {
+      t[q].pad1 = static_cast<int16_t>(out_early[pos[q]].size());
+      if (!out_early[pos[q]].empty()) out[pos[q]].insert(out[pos[q]].begin(), out_early[pos[q]].begin(),
+                                                         out_early[pos[q]].end());
     }
     L->exec_off = static_cast<int64_t>(tasks->size());
     L->nexec = n;
@@ -1459,6 +1468,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
       return gen[l].empty() && gem[l].empty() && gemD[l].empty() && gemE[l].empty();
     };
     std::vector<char> merged_into_prev(nlevels, 0);
+    const bool chain_l = std::getenv("LBK_CHAIN_L") != nullptr;  // chain-2 GETRF tasks (A/B)
     int32_t absorbed_lv = -2;  // SSSSM level whose DMMA tiles run inside the next executor launch
     int64_t absorbed_off = 0, absorbed_n = 0;
     for (int32_t lv = 0; lv < nlevels; ++lv) {
@@ -1830,17 +1840,25 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
             // task and one handoff per step instead of three and two
             const bool chain = LBK_CHAIN_TRSM && kb + 1 < nt && xocc[static_cast<size_t>(kb) * nt + kb + 1] &&
                                xocc[static_cast<size_t>(kb + 1) * nt + kb];
+            // chain-2: this step's LU task also solves L(kb+1, kb) (the operand the next diagonal
+            // update waits for last), after releasing the tasks that need only the factored tile
+            const bool chainL = !chain && chain_l && kb + 1 < nt && xocc[static_cast<size_t>(kb) * nt + kb + 1];
             std::vector<int> gdeps = fused ? fused_deps : prev(kb, kb, {});
             if (chain) {
               const std::vector<int> dl = prev(kb + 1, kb, {}), du = prev(kb, kb + 1, {});
               gdeps.insert(gdeps.end(), dl.begin(), dl.end());
               gdeps.insert(gdeps.end(), du.begin(), du.end());
             }
+            std::vector<int> gdeps2 = fused && !chain ? fused_ops : std::vector<int>{};
+            if (chainL) {  // the L tile's last update: waited for with the operands (phase 2)
+              const std::vector<int> dl = prev(kb + 1, kb, {});
+              gdeps.insert(gdeps.end(), dl.begin(), dl.end());
+              gdeps2.insert(gdeps2.end(), dl.begin(), dl.end());
+            }
             // GETRF_UPD loads its target tile before the two operand tiles exist (phase 2)
-            const int g = fused ? X.add(X_GETRF_UPD, b, b, kb, kb, kb - 1, stp, kb * 4, gdeps,
-                                        chain ? std::vector<int>{} : fused_ops)
-                                : X.add(X_GETRF, b, b, kb, kb, kb, stp, kb * 4, gdeps);
-            X.t[g].chain = chain ? 1 : 0;
+            const int g = fused ? X.add(X_GETRF_UPD, b, b, kb, kb, kb - 1, stp, kb * 4, gdeps, gdeps2)
+                                : X.add(X_GETRF, b, b, kb, kb, kb, stp, kb * 4, gdeps, gdeps2);
+            X.t[g].chain = chain ? 1 : chainL ? 2 : 0;
             fused = false;
             colw[kb].push_back(g);
             roww[kb].push_back(g);
@@ -1849,8 +1867,10 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
             for (int r = kb + 1; r < nt; ++r) {
               lt[r] = -1;
               if (!xocc[static_cast<size_t>(kb) * nt + r]) continue;
-              lt[r] = (chain && r == kb + 1) ? g
-                                             : X.add(X_TRSM_L, b, b, r, kb, kb, stp, kb * 4 + 1, prev(r, kb, {g}), {g});
+              lt[r] = ((chain || chainL) && r == kb + 1)
+                          ? g
+                          : X.add(X_TRSM_L, b, b, r, kb, kb, stp, kb * 4 + 1, prev(r, kb, {g}), {g});
+              if (chainL && lt[r] != g) X.mark_early(g, lt[r]);
               colw[kb].push_back(lt[r]);
               L_(r, kb) = lt[r];
               fin_deps.push_back(lt[r]);
@@ -1860,6 +1880,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
               if (!xocc[static_cast<size_t>(cc) * nt + kb]) continue;
               ut[cc] = (chain && cc == kb + 1) ? g
                                                : X.add(X_TRSM_U, b, b, kb, cc, kb, stp, kb * 4 + 1, prev(kb, cc, {g}), {g});
+              if (chainL) X.mark_early(g, ut[cc]);
               roww[kb].push_back(ut[cc]);
               L_(kb, cc) = ut[cc];
             }
@@ -2021,7 +2042,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
         for (const XTask& x : X.t) {  // executed flops of the tile tasks (full 64-tiles)
           if (x.type == X_SSSSM) continue;  // counted when absorbed
           const double t3 = 64.0 * 64.0 * 64.0;
-          if (x.chain) c->exec_flops += 2 * t3;  // the two solved tiles of the chain
+          if (x.chain) c->exec_flops += x.chain == 1 ? 2 * t3 : t3;  // the solved tiles of the chain
           c->exec_flops += x.type == X_GETRF_UPD                                     ? 2 * t3 + 2 * t3 / 3
                            : x.type == X_PG_FUSED || x.type == X_PT_FUSED              ? 3 * t3
                            : x.type == X_GEMM || x.type == X_PG_UPD || x.type == X_PT_UPD ? 2 * t3

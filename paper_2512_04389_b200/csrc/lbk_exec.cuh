@@ -65,9 +65,10 @@ enum XType : int8_t {
 
 struct XTask {
   int8_t type;
-  int8_t chain;  // X_GETRF / X_GETRF_UPD: then also solve L(r+1, r) and U(r, r+1) (the next step's update operands)
+  int8_t chain;  // X_GETRF / X_GETRF_UPD: 1: then also solve L(r+1, r) and U(r, r+1) (the next step's update
+                 // operands); 2: then also solve L(r+1, r), releasing the other successors first
   int16_t r, c, k;
-  int16_t pad1;
+  int16_t pad1;  // chain == 2: successor entries released early (after the diagonal tile's LU)
   int32_t a;     // block the task writes
   int32_t d;     // diagonal block (panel tasks), = a for GETRF tasks
   int32_t step;  // elimination step (error records)
@@ -1107,10 +1108,29 @@ __device__ __forceinline__ void run_ssssm(const GemmItem* gitems, const GemmTask
   gemm_map_item(gitems[item], gtasks, P, sm);
 }
 
+// Early release of a chain-2 GETRF task (XTask::chain == 2: it also solves L(k+1, k)): its first
+// XTask::pad1 successor entries need only the factored diagonal tile and are released right after
+// it is stored; the rest after the fused solve (exec_body).
+struct EarlyRelease {
+  const XLevel* L;
+  int t;
+  __device__ void operator()() const {
+    __threadfence();
+    __syncthreads();
+    const int e0 = L->succ_ptr[t], ne = L->tasks[t].pad1;
+    for (int e = e0 + threadIdx.x; e < e0 + ne; e += blockDim.x) {
+      const int sx = L->succ[e];
+      atomicSub(L->deps + 2 * (sx >> 1) + (sx & 1), 1);
+    }
+  }
+  __device__ explicit operator bool() const { return L != nullptr; }
+};
+
 template <bool kBandReg>
 __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double pivot_tol,
                          unsigned long long* ph = nullptr, volatile int* d2 = nullptr,
-                         const GemmItem* gitems = nullptr, const GemmTask* gtasks = nullptr) {
+                         const GemmItem* gitems = nullptr, const GemmTask* gtasks = nullptr,
+                         EarlyRelease early = EarlyRelease{nullptr, 0}) {
   double* T0 = sm;                  // target tile (XTP stride)
   double* T1 = sm + XREG;           // operand tile (XTP stride) / DMMA A (XS stride)
   double* T2 = sm + 2 * XREG;       // DMMA B (XS stride)
@@ -1180,6 +1200,7 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
 #endif
       stamp(ph, 1);
       store_tile(G, m, T0, n, n);
+      if (tk.chain == 2 && early) early();  // the tasks that need only this factored tile start now
       if (!LBK_LATE_FLUSH || tk.chain) flush_colmax(T1, n, n, false, P.bmax + A.dg + k0, T2);
       stamp(ph, 2);
       if (tk.chain) {
@@ -1193,11 +1214,13 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
         tile_right_solve_blk<true>(T1, T0, rinv, T2, n);
         store_tile(P.vals + A.ent + static_cast<size_t>(k0) * m + r0, m, T1, nr, n);
         flush_colmax(T2, nr, n, true, P.bmax + A.dg + k0, T1);
-        __syncthreads();
-        load_tile(T1, P.vals + A.ent + static_cast<size_t>(r0) * m + k0, m, n, nr);  // U tile (k0, r0)
-        __syncthreads();
-        tile_left_solve_blk(T1, T0, n);
-        store_tile(P.vals + A.ent + static_cast<size_t>(r0) * m + k0, m, T1, n, nr);
+        if (tk.chain == 1) {
+          __syncthreads();
+          load_tile(T1, P.vals + A.ent + static_cast<size_t>(r0) * m + k0, m, n, nr);  // U tile (k0, r0)
+          __syncthreads();
+          tile_left_solve_blk(T1, T0, n);
+          store_tile(P.vals + A.ent + static_cast<size_t>(r0) * m + k0, m, T1, n, nr);
+        }
         stamp(ph, 3);
       }
       break;
@@ -1392,7 +1415,7 @@ __device__ __forceinline__ void exec_body(const XLevel& L, const DevPools& P, do
     if (t >= L.ntasks) break;
     const XTask tk = L.tasks[t];
     run_task<kBandReg>(tk, P, sm, pivot_tol, L.trace ? L.trace + 8 * t + 3 : nullptr, L.deps + 2 * t + 1, L.gitems,
-                       L.gtasks);
+                       L.gtasks, EarlyRelease{&L, t});
     // every thread fences its own tile writes before the barrier, so the
     // successor releases after it are ordered behind all of them; the
     // releases are spread over the CTA (a GETRF tile has ~2x(tiles per
@@ -1401,7 +1424,8 @@ __device__ __forceinline__ void exec_body(const XLevel& L, const DevPools& P, do
     __syncthreads();
     const bool late = late_flush(tk);
     {
-      const int e0 = L.succ_ptr[t], e1 = L.succ_ptr[t + 1];
+      // (a chain-2 GETRF task released its first tk.pad1 entries inside run_task)
+      const int e0 = L.succ_ptr[t] + (tk.chain == 2 ? tk.pad1 : 0), e1 = L.succ_ptr[t + 1];
       for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
         const int sx = L.succ[e];
         if (!late || L.tasks[sx >> 1].type != X_FINAL) atomicSub(L.deps + 2 * (sx >> 1) + (sx & 1), 1);
