@@ -41,7 +41,12 @@ constexpr int XTP = XT + 1;     // padded smem column stride
 constexpr int XS = XT + 4;      // DMMA operand stride
 constexpr int XREG = XT * XS;   // one smem tile region (fits either stride)
 constexpr int EXEC_SMEM = (3 * XREG + 4 * XT) * 8;
-static_assert(GEMM_SMEM <= EXEC_SMEM, "absorbed DMMA SSSSM tiles run in the executor's shared memory");
+#ifdef LBK_ABSORB_TILES
+#define LBK_ABSORB_TILES_ENABLED LBK_ABSORB_TILES
+#else
+#define LBK_ABSORB_TILES_ENABLED 0
+#endif
+static_assert(!LBK_ABSORB_TILES_ENABLED || GEMM_SMEM <= EXEC_SMEM, "absorbed DMMA SSSSM tiles run in the executor's shared memory");
 constexpr int COLMAX_ROWS = 128;  // rows per colmax task (GETRF's first tile waits for a whole column of them)
 
 enum XType : int8_t {
