@@ -12,9 +12,11 @@ from paper_2512_04389_b200 import generators as G  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "p3d10"
 a = {"p3d10": lambda: G.poisson3d(10, "nd"), "c1": lambda: G.poisson2d(64),
-     "bbd": lambda: G.bbd(6000, 120, 12, seed=3), "dense": lambda: M.generate("dense", 300)}[name]()
+     "bbd": lambda: G.bbd(6000, 120, 12, seed=3), "dense": lambda: M.generate("dense", 300),
+     "p3d12r": lambda: G.poisson3d(12, "nd")}[name]()
 f = M.symbolic_factorize(M.symmetrize_pattern(a))
 plan = (M.regular_plan(a.n, 150) if name == "dense"
+        else M.regular_plan(a.n, 864) if name == "p3d12r"  # blocks of several subtrees: subtree-aligned tiles
         else M.irregular_plan(M.percentage_curve(M.diag_block_pointer(f)), a.n))
 g = M.partition(f, a, plan)
 t = M.dependency_levels(g)
