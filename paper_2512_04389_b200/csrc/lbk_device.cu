@@ -281,9 +281,9 @@ struct ExecBuilder {
       for (int p : preds2[i]) (early.count({p, i}) ? out_early : out)[pos[p]].push_back((pos[i] << 1) | 1);
     }
     for (int q = 0; q < n; ++q) {
+      if (out_early[pos[q]].empty()) continue;  // (pad1 of other task types keeps its own meaning)
       t[q].pad1 = static_cast<int16_t>(out_early[pos[q]].size());
-      if (!out_early[pos[q]].empty()) out[pos[q]].insert(out[pos[q]].begin(), out_early[pos[q]].begin(),
-                                                         out_early[pos[q]].end());
+      out[pos[q]].insert(out[pos[q]].begin(), out_early[pos[q]].begin(), out_early[pos[q]].end());
     }
     L->exec_off = static_cast<int64_t>(tasks->size());
     L->nexec = n;
@@ -1469,6 +1469,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
     };
     std::vector<char> merged_into_prev(nlevels, 0);
     const bool chain_l = std::getenv("LBK_CHAIN_L") != nullptr;  // chain-2 GETRF tasks (A/B)
+    const int panel_agg = std::getenv("LBK_PANEL_AGG") ? std::max(1, std::atoi(std::getenv("LBK_PANEL_AGG"))) : 4;
     int32_t absorbed_lv = -2;  // SSSSM level whose DMMA tiles run inside the next executor launch
     int64_t absorbed_off = 0, absorbed_n = 0;
     for (int32_t lv = 0; lv < nlevels; ++lv) {
@@ -1999,10 +2000,46 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
             if (L_(r, cc) < 0) v.insert(v.end(), xupd.begin(), xupd.end());
             return v;
           };
+          // Updates of a panel tile from consecutive steps k far from its own solve step are
+          // aggregated into one task (up to panel_agg of them, XTask::pad1 = count): it loads the
+          // target once and applies them one after another in k order (the same operations as
+          // separate tasks: bitwise identical), one task, load, store and handoff instead of
+          // several.  The update from the step just before the tile's solve stays fused into it.
+          struct Pend {
+            int k0 = -1, cnt = 0;
+            std::vector<int> deps;
+          };
+          std::map<std::pair<int, int>, Pend> pend_upd;
+          auto flush_upd = [&](int type, int r, int cc) {
+            auto it = pend_upd.find({r, cc});
+            if (it == pend_upd.end() || it->second.cnt == 0) return;
+            Pend& pq = it->second;
+            std::vector<int> dep = pq.deps;
+            dep.push_back(L_(r, cc));
+            const int tsk = X.add(type, xb, dblk, r, cc, pq.k0, stp, pq.k0 * 4 + 2, fw(dep, r, cc));
+            X.t[tsk].pad1 = static_cast<int16_t>(pq.cnt);
+            L_(r, cc) = tsk;
+            pend_upd.erase(it);
+          };
+          auto add_upd = [&](int type, int r, int cc, int kb, int d) {
+            if (panel_agg <= 1) {
+              L_(r, cc) = X.add(type, xb, dblk, r, cc, kb, stp, kb * 4 + 2, fw({d, L_(r, cc), mark(kb)}, r, cc));
+              return;
+            }
+            auto it = pend_upd.find({r, cc});
+            if (it != pend_upd.end() && (it->second.k0 + it->second.cnt != kb || it->second.cnt >= panel_agg))
+              flush_upd(type, r, cc);
+            Pend& pq = pend_upd[{r, cc}];
+            if (pq.cnt == 0) pq.k0 = kb;
+            ++pq.cnt;
+            pq.deps.push_back(d);
+            pq.deps.push_back(mark(kb));
+          };
           if (pt[0] == 1) {  // GESSM: forward substitution down the row blocks
             for (int kb = 0; kb < tr; ++kb)
               for (int cc = 0; cc < tc; ++cc) {
                 if (!X_(kb, cc)) continue;
+                flush_upd(X_PG_UPD, kb, cc);  // (only when the tile has no fused update)
                 if (P_(kb, cc) >= 0) PD_(kb, cc).push_back(mark(kb));
                 const int d = P_(kb, cc) >= 0
                                   ? X.add(X_PG_FUSED, xb, dblk, kb, cc, P_(kb, cc), stp, kb * 4 + 1, PD_(kb, cc))
@@ -2011,17 +2048,19 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
                 for (int r = kb + 1; r < tr; ++r)
                   if (X_(r, cc) && D_(r, kb)) {  // L tile (r, kb)
                     if (r == kb + 1) {
+                      flush_upd(X_PG_UPD, r, cc);
                       P_(r, cc) = kb;
                       PD_(r, cc) = fw({d, L_(r, cc)}, r, cc);
                       continue;
                     }
-                    L_(r, cc) = X.add(X_PG_UPD, xb, dblk, r, cc, kb, stp, kb * 4 + 2, fw({d, L_(r, cc), mark(kb)}, r, cc));
+                    add_upd(X_PG_UPD, r, cc, kb, d);
                   }
               }
           } else {  // TSTRF: substitution along the column blocks
             for (int kb = 0; kb < tc; ++kb)
               for (int r = 0; r < tr; ++r) {
                 if (!X_(r, kb)) continue;
+                flush_upd(X_PT_UPD, r, kb);
                 if (P_(r, kb) >= 0) PD_(r, kb).push_back(mark(kb));
                 const int d = P_(r, kb) >= 0
                                   ? X.add(X_PT_FUSED, xb, dblk, r, kb, P_(r, kb), stp, kb * 4 + 1, PD_(r, kb))
@@ -2030,14 +2069,17 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
                 for (int cc = kb + 1; cc < tc; ++cc)
                   if (X_(r, cc) && D_(kb, cc)) {  // U tile (kb, cc)
                     if (cc == kb + 1) {
+                      flush_upd(X_PT_UPD, r, cc);
                       P_(r, cc) = kb;
                       PD_(r, cc) = fw({d, L_(r, cc)}, r, cc);
                       continue;
                     }
-                    L_(r, cc) = X.add(X_PT_UPD, xb, dblk, r, cc, kb, stp, kb * 4 + 2, fw({d, L_(r, cc), mark(kb)}, r, cc));
+                    add_upd(X_PT_UPD, r, cc, kb, d);
                   }
               }
           }
+          for (auto& kv : std::vector<std::pair<std::pair<int, int>, Pend>>(pend_upd.begin(), pend_upd.end()))
+            flush_upd(pt[0] == 1 ? X_PG_UPD : X_PT_UPD, kv.first.first, kv.first.second);  // (none expected)
         }
         for (const XTask& x : X.t) {  // executed flops of the tile tasks (full 64-tiles)
           if (x.type == X_SSSSM) continue;  // counted when absorbed
@@ -2045,7 +2087,8 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           if (x.chain) c->exec_flops += x.chain == 1 ? 2 * t3 : t3;  // the solved tiles of the chain
           c->exec_flops += x.type == X_GETRF_UPD                                     ? 2 * t3 + 2 * t3 / 3
                            : x.type == X_PG_FUSED || x.type == X_PT_FUSED              ? 3 * t3
-                           : x.type == X_GEMM || x.type == X_PG_UPD || x.type == X_PT_UPD ? 2 * t3
+                           : x.type == X_PG_UPD || x.type == X_PT_UPD                 ? 2 * t3 * std::max<int>(1, x.pad1)
+                           : x.type == X_GEMM                                         ? 2 * t3
                            : x.type == X_GETRF                                       ? 2 * t3 / 3
                            : x.type == X_COLMAX || x.type == X_FINAL                 ? 0
                                                                                      : t3;

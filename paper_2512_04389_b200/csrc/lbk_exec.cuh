@@ -73,7 +73,8 @@ struct XTask {
   int8_t chain;  // X_GETRF / X_GETRF_UPD: 1: then also solve L(r+1, r) and U(r, r+1) (the next step's update
                  // operands); 2: then also solve L(r+1, r), releasing the other successors first
   int16_t r, c, k;
-  int16_t pad1;  // chain == 2: successor entries released early (after the diagonal tile's LU)
+  int16_t pad1;  // chain == 2: successor entries released early (after the diagonal tile's LU);
+                 // X_PG_UPD / X_PT_UPD: number of consecutive steps k.. aggregated (0 / 1: one)
   int32_t a;     // block the task writes
   int32_t d;     // diagonal block (panel tasks), = a for GETRF tasks
   int32_t step;  // elimination step (error records)
@@ -1313,14 +1314,16 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
         __syncthreads();
         tile_left_solve_blk(T0, T1, nr);
         store_tile(G, ld, T0, nr, nc);
-      } else {
-        const int k0 = xop(P, A, tk.k, A.nR), nk = xop(P, A, tk.k + 1, A.nR) - k0;
+      } else {  // tk.pad1 > 1: the updates from steps k .. k + pad1 - 1, in k order (one target load / store)
         load_tile(T0, G, ld, nr, nc);
-        if (Rl) load_opA(T1, Dv, m, nr, nk, Rl + r0, Rl + k0);
-        else load_opA(T1, Dv + static_cast<size_t>(k0) * m + r0, m, nr, nk);
-        load_opB(T2, P.vals + A.ent + static_cast<size_t>(c0) * ld + k0, ld, nk, nc);
-        __syncthreads();
-        tile_mma_sub(T0, T1, T2);
+        for (int q = 0, nq = max(1, static_cast<int>(tk.pad1)); q < nq; ++q) {
+          const int k0 = xop(P, A, tk.k + q, A.nR), nk = xop(P, A, tk.k + q + 1, A.nR) - k0;
+          if (Rl) load_opA(T1, Dv, m, nr, nk, Rl + r0, Rl + k0);
+          else load_opA(T1, Dv + static_cast<size_t>(k0) * m + r0, m, nr, nk);
+          load_opB(T2, P.vals + A.ent + static_cast<size_t>(c0) * ld + k0, ld, nk, nc);
+          __syncthreads();
+          tile_mma_sub(T0, T1, T2);  // (ends with a barrier: T1 / T2 free for the next step)
+        }
         store_tile(G, ld, T0, nr, nc);
       }
       break;
@@ -1353,14 +1356,16 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
         __syncthreads();
         tile_right_solve_blk<false>(T0, T1, rinv, nullptr, nc);
         store_tile(G, ld, T0, nr, nc);
-      } else {
-        const int k0 = xop(P, A, tk.k, A.nC), nk = xop(P, A, tk.k + 1, A.nC) - k0;
+      } else {  // tk.pad1 > 1: the updates from steps k .. k + pad1 - 1, in k order (one target load / store)
         load_tile(T0, G, ld, nr, nc);
-        load_opA(T1, P.vals + A.ent + static_cast<size_t>(k0) * ld + r0, ld, nr, nk);
-        if (Cl) load_opB(T2, Dv, m, nk, nc, Cl + k0, Cl + c0);
-        else load_opB(T2, Dv + static_cast<size_t>(c0) * m + k0, m, nk, nc);
-        __syncthreads();
-        tile_mma_sub(T0, T1, T2);
+        for (int q = 0, nq = max(1, static_cast<int>(tk.pad1)); q < nq; ++q) {
+          const int k0 = xop(P, A, tk.k + q, A.nC), nk = xop(P, A, tk.k + q + 1, A.nC) - k0;
+          load_opA(T1, P.vals + A.ent + static_cast<size_t>(k0) * ld + r0, ld, nr, nk);
+          if (Cl) load_opB(T2, Dv, m, nk, nc, Cl + k0, Cl + c0);
+          else load_opB(T2, Dv + static_cast<size_t>(c0) * m + k0, m, nk, nc);
+          __syncthreads();
+          tile_mma_sub(T0, T1, T2);
+        }
         store_tile(G, ld, T0, nr, nc);
       }
       break;
