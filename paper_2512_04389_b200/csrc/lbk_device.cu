@@ -1823,11 +1823,46 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
               fin_deps.push_back(col);
             }
           auto L_ = [&](int r, int cc) -> int& { return last[static_cast<size_t>(cc) * nt + r]; };
-          auto prev = [&](int r, int cc, std::vector<int> extra) {
+          auto prev_raw = [&](int r, int cc, std::vector<int> extra) {
             const int l = L_(r, cc);
             if (l >= 0) extra.push_back(l);
             else extra.insert(extra.end(), colj[cc].begin(), colj[cc].end());
             return extra;
+          };
+          // trailing updates of a tile from consecutive steps wait here and run as one task
+          // (up to panel_agg of them, XTask::pad1, k order: bitwise identical); any use of the
+          // tile's last writer (prev) emits the pending task first
+          struct GPend {
+            int k0 = -1, cnt = 0;
+            std::vector<int> deps;
+          };
+          std::map<std::pair<int, int>, GPend> gpend;
+          auto flush_gemm = [&](int r, int cc) {
+            auto it = gpend.find({r, cc});
+            if (it == gpend.end()) return;
+            GPend gp = it->second;
+            gpend.erase(it);
+            const int tsk = X.add(X_GEMM, b, b, r, cc, gp.k0, stp, gp.k0 * 4 + 2, prev_raw(r, cc, gp.deps));
+            X.t[tsk].pad1 = static_cast<int16_t>(gp.cnt);
+            L_(r, cc) = tsk;
+          };
+          auto prev = [&](int r, int cc, std::vector<int> extra) {
+            flush_gemm(r, cc);
+            return prev_raw(r, cc, std::move(extra));
+          };
+          auto add_gemm = [&](int r, int cc, int kb, int lt_r, int ut_c) {
+            if (panel_agg <= 1) {
+              L_(r, cc) = X.add(X_GEMM, b, b, r, cc, kb, stp, kb * 4 + 2, prev_raw(r, cc, {lt_r, ut_c}));
+              return;
+            }
+            auto it = gpend.find({r, cc});
+            if (it != gpend.end() && (it->second.k0 + it->second.cnt != kb || it->second.cnt >= panel_agg))
+              flush_gemm(r, cc);
+            GPend& gp = gpend[{r, cc}];
+            if (gp.cnt == 0) gp.k0 = kb;
+            ++gp.cnt;
+            gp.deps.push_back(lt_r);
+            gp.deps.push_back(ut_c);
           };
           // the last update of diagonal tile kb (GEMM(kb, kb, kb-1)) is fused into
           // its LU task: one handoff and one tile round trip less per step of
@@ -1895,11 +1930,11 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
                   fused_ops = {lt[r], ut[cc]};
                   continue;
                 }
-                const int t2 = X.add(X_GEMM, b, b, r, cc, kb, stp, kb * 4 + 2, prev(r, cc, {lt[r], ut[cc]}));
-                L_(r, cc) = t2;
+                add_gemm(r, cc, kb, lt[r], ut[cc]);
               }
             }
           }
+          while (!gpend.empty()) flush_gemm(gpend.begin()->first.first, gpend.begin()->first.second);  // (none expected)
           X.add(X_FINAL, b, b, 0, 0, 0, stp, 1 << 30, fin_deps);
           if (merge_next) {  // chained markers: column t done implies columns < t done
             coldone[b].assign(nt, -1);
@@ -2088,7 +2123,7 @@ int lbk_plan(lbk_ctx* c, int64_t n, int64_t p, const int64_t* positions, int64_t
           c->exec_flops += x.type == X_GETRF_UPD                                     ? 2 * t3 + 2 * t3 / 3
                            : x.type == X_PG_FUSED || x.type == X_PT_FUSED              ? 3 * t3
                            : x.type == X_PG_UPD || x.type == X_PT_UPD                 ? 2 * t3 * std::max<int>(1, x.pad1)
-                           : x.type == X_GEMM                                         ? 2 * t3
+                           : x.type == X_GEMM                                         ? 2 * t3 * std::max<int>(1, x.pad1)
                            : x.type == X_GETRF                                       ? 2 * t3 / 3
                            : x.type == X_COLMAX || x.type == X_FINAL                 ? 0
                                                                                      : t3;

@@ -74,7 +74,7 @@ struct XTask {
                  // operands); 2: then also solve L(r+1, r), releasing the other successors first
   int16_t r, c, k;
   int16_t pad1;  // chain == 2: successor entries released early (after the diagonal tile's LU);
-                 // X_PG_UPD / X_PT_UPD: number of consecutive steps k.. aggregated (0 / 1: one)
+                 // X_GEMM / X_PG_UPD / X_PT_UPD: number of consecutive steps k.. aggregated (0 / 1: one)
   int32_t a;     // block the task writes
   int32_t d;     // diagonal block (panel tasks), = a for GETRF tasks
   int32_t step;  // elimination step (error records)
@@ -1262,16 +1262,19 @@ __device__ void run_task(const XTask& tk, const DevPools& P, double* sm, double 
       store_tile(G, m, T0, nk, nc);
       break;
     }
-    case X_GEMM: {
-      const int m = A.nrows, k0 = xo(P, A, tk.k), r0 = xo(P, A, tk.r), c0 = xo(P, A, tk.c);
-      const int nk = xo(P, A, tk.k + 1) - k0, nr = xo(P, A, tk.r + 1) - r0, nc = xo(P, A, tk.c + 1) - c0;
+    case X_GEMM: {  // tk.pad1 > 1: the updates from steps k .. k + pad1 - 1, in k order (one target load / store)
+      const int m = A.nrows, r0 = xo(P, A, tk.r), c0 = xo(P, A, tk.c);
+      const int nr = xo(P, A, tk.r + 1) - r0, nc = xo(P, A, tk.c + 1) - c0;
       const double* base = P.vals + A.ent;
       double* G = P.vals + A.ent + static_cast<size_t>(c0) * m + r0;
       load_tile(T0, G, m, nr, nc);
-      load_opA(T1, base + static_cast<size_t>(k0) * m + r0, m, nr, nk);
-      load_opB(T2, base + static_cast<size_t>(c0) * m + k0, m, nk, nc);
-      __syncthreads();
-      tile_mma_sub(T0, T1, T2);
+      for (int q = 0, nq = max(1, static_cast<int>(tk.pad1)); q < nq; ++q) {
+        const int k0 = xo(P, A, tk.k + q), nk = xo(P, A, tk.k + q + 1) - k0;
+        load_opA(T1, base + static_cast<size_t>(k0) * m + r0, m, nr, nk);
+        load_opB(T2, base + static_cast<size_t>(c0) * m + k0, m, nk, nc);
+        __syncthreads();
+        tile_mma_sub(T0, T1, T2);
+      }
       store_tile(G, m, T0, nr, nc);
       break;
     }
